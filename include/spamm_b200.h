@@ -1,0 +1,186 @@
+/*
+ * spamm_b200.h -- C ABI of the B200 SpAMM multiply path.
+ *
+ * The reference (`spamm` v0.1.0, pure Python) has no FFI layer; its boundary for
+ * this path is the Python API `multiply / build_plan / execute_plan`
+ * (pkg/src/spamm/numeric.py:302-313, symbolic.py:151-159, numeric.py:138-151)
+ * on `QuadtreeMatrix` operands (core.py:146-405).  The Python package
+ * `paper_1203_1692_b200` re-implements that API and calls the entry points below
+ * through ctypes; INTEGRATION.md shows the stub a maintainer of the reference
+ * would add.  Every function:
+ *   - takes raw DEVICE pointers, sizes and a cudaStream_t (as void*),
+ *   - is stream-ordered, never allocates and never synchronises,
+ *   - returns 0 on success, a SPAMM_E* code otherwise (spamm_error_string()).
+ * Counts that the host needs (leaves, tasks) are written to device memory; the
+ * caller decides when to read them back.
+ *
+ * Sizes: n_b = 16 (core.py:21).  A tree of depth d has a leaf grid of side
+ * L = 2^d.  Level t (0 = root .. d = leaves) is a 2^t x 2^t row-major grid that
+ * starts at element spamm_level_offset(t) of a level buffer (levels packed root first,
+ * each start rounded up to 4 elements).
+ */
+#ifndef SPAMM_B200_H
+#define SPAMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPAMM_ABI_VERSION 1
+
+enum {
+    SPAMM_OK = 0,
+    SPAMM_EINVAL = 1,      /* bad argument (-> ValueError on the Python side) */
+    SPAMM_ECUDA = 2,       /* CUDA runtime error (-> RuntimeError)            */
+    SPAMM_EWORKSPACE = 3   /* workspace too small                             */
+};
+
+enum { SPAMM_FINE4 = 0, SPAMM_COARSE16 = 1 };        /* numeric.py:26 GRANULARITIES   */
+enum { SPAMM_ORDER_DENSE = 0, SPAMM_ORDER_REFRESH = 1 }; /* leaf sum order, see below */
+enum { SPAMM_EXEC_FMA = 0, SPAMM_EXEC_EXACT = 1 };   /* EXACT: separate mul/add rounding */
+
+/* Device view of one QuadtreeMatrix (core.py:146-167, :387-405).  All pointers
+ * are device pointers owned by the caller.
+ *   keys      [nleaf]       Morton key of each stored leaf, ascending (packed_leaves()[0])
+ *   values    [nleaf][256]  row-major 16x16 leaf values          (packed_leaves()[1])
+ *   values_t  [nleaf][256]  the same leaves transposed (the A-operand staging layout)
+ *   sub4      [nleaf][16]   4x4 sub-block norms, p*4+q           (packed_leaves()[2])
+ *   slot      [L*L]         leaf (i,j) -> index into the packed arrays, -1 = absent
+ *   slot_t    [L*L]         transposed grid: (j,i) -> index
+ *   norm      level buffer  node norms, -1 = absent node        (TreeNode.norm, core.py:138-143)
+ *   norm_t    level buffer  every level's grid transposed
+ */
+typedef struct {
+    int32_t m, n;           /* logical size */
+    int32_t depth;          /* leaf level; grids have side 1 << depth */
+    int32_t nleaf;          /* stored leaves (host copy) */
+    const uint32_t *keys;
+    const float *values;
+    const float *values_t;
+    const float *sub4;
+    const int32_t *slot;
+    const int32_t *slot_t;
+    const float *norm;
+    const float *norm_t;
+} spamm_tree_view;
+
+int spamm_abi_version(void);
+int64_t spamm_level_offset_of(int t);      /* t == 0 ? 0 : 4 + (4^t - 4)/3 */
+const char *spamm_error_string(int code);
+/* Number of kernels launched by this library since load (for bench.py's gpu_launches). */
+int64_t spamm_launch_count(void);
+
+/* ---- tree construction: QuadtreeMatrix.from_dense (core.py:213-266) -------- */
+
+/* Leaf pass over a dense row-major m x n matrix (row stride ld, in floats):
+ * per leaf of the 2^depth grid the 16 sub-block norms, the double square sum and
+ * the leaf norm (-1 where the leaf is all zero or outside the matrix).
+ * sub4_grid [L*L][16], leaf_sq [L*L], leaf_norm [L*L].  Replaces core.py:225-233. */
+int spamm_leaf_norms_dense(const float *dense, int64_t m, int64_t n, int64_t ld, int depth,
+                           float *sub4_grid, double *leaf_sq, float *leaf_norm, void *stream);
+
+/* Stored leaves in ascending Morton order (core.py:235-237): slot/slot_t grids, keys,
+ * and the leaf count in *nleaf_dev.  ws: spamm_scan_workspace_bytes(L*L) bytes. */
+size_t spamm_scan_workspace_bytes(int64_t n);
+int spamm_assign_slots(const float *leaf_norm, int depth, int32_t *slot, int32_t *slot_t,
+                       uint32_t *keys, int32_t *nleaf_dev, void *ws, size_t ws_bytes, void *stream);
+
+/* Copy the stored leaves out of the dense matrix (core.py:239-248): values, values_t, sub4.
+ * nleaf is the host copy of *nleaf_dev. */
+int spamm_pack_leaves(const float *dense, int64_t m, int64_t n, int64_t ld, int depth,
+                      const uint32_t *keys, int64_t nleaf, const float *sub4_grid,
+                      float *values, float *values_t, float *sub4, void *stream);
+
+/* Interior norms (_build_interior, core.py:252-266): fills levels 0..depth-1 of norm / norm_t
+ * and sq_levels from the leaf level.  leaf_sq is the L*L grid of double square sums; the leaf
+ * level of `norm` must be in place (-1 = absent); when write_leaf_transpose != 0 the leaf level
+ * of norm_t is written from it as well. */
+int spamm_build_interior(const double *leaf_sq, int depth, float *norm, float *norm_t,
+                         double *sq_levels, int write_leaf_transpose, void *stream);
+
+/* ---- trees given as packed leaves: put_leaf + compute_norms (core.py:315-345) */
+
+/* Leaf norms of packed leaves, in the order compute_norms uses (core.py:108-116):
+ * sub4 [nleaf][16], leaf_sq [nleaf], and optionally the transposed copy values_t. */
+int spamm_leaf_norms_packed(const float *values, int64_t nleaf, float *values_t,
+                            float *sub4, double *leaf_sq, void *stream);
+
+/* Scatter packed leaves (keys ascending, leaf_sq) into the grids of a depth-`depth` tree:
+ * slot, slot_t, the leaf level of norm/norm_t and the double leaf_sq grid (all L*L). */
+int spamm_index_leaves(const uint32_t *keys, const double *leaf_sq_packed, int64_t nleaf, int depth,
+                       int32_t *slot, int32_t *slot_t, float *norm, float *norm_t,
+                       double *leaf_sq_grid, void *stream);
+
+/* QuadtreeMatrix.to_dense (core.py:268-276): out is m x n, row stride ld, fully written. */
+int spamm_to_dense(const spamm_tree_view *t, float *out, int64_t ld, void *stream);
+
+/* ---- symbolic phase: build_plan (symbolic.py:92-159) --------------------------- */
+
+/* Device plan: product leaves in ascending Morton order with their tasks in
+ * ascending k (the only order the numeric phase depends on, numeric.py:203-217).
+ *   c_keys [nC], c_off [nC+1]    product leaf keys and CSR offsets into the task arrays
+ *   task_k / task_a / task_b [T] contraction index, packed slot of the A and B leaf
+ *   task_mask [T]                fine4 live bits, bit r*16 + p*4 + q (numeric.py:232-238);
+ *                                all ones for coarse16
+ *   counts [4]                   nC, T, overflow flag, largest intermediate list
+ */
+typedef struct {
+    uint32_t *c_keys;
+    int32_t *c_off;
+    uint32_t *task_k;
+    uint32_t *task_a;
+    uint32_t *task_b;
+    uint64_t *task_mask;
+    int64_t task_capacity;
+    int64_t leaf_capacity;
+    int32_t *counts;
+} spamm_plan_buffers;
+
+size_t spamm_plan_workspace_bytes(int depth, int64_t task_capacity, int64_t leaf_capacity);
+
+/* Task set { (i,k,j) : both leaves stored, double(normA) * double(normB) >= tau }
+ * (symbolic.py:118-125), produced by a top-down walk of the two norm pyramids.
+ * `depth` is the common depth of both views (the caller re-indexes a shallower tree);
+ * rows/cols limit the product to [row0,row1) x all columns of leaves (multi-GPU row blocks). */
+int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
+               int32_t row0, int32_t row1, const spamm_plan_buffers *out,
+               void *ws, size_t ws_bytes, void *stream);
+
+/* ---- numeric phase: execute_plan (numeric.py:138-284) ------------------------- */
+
+size_t spamm_execute_workspace_bytes(int64_t nC);
+
+/* Runs every task of the plan: C leaf = alpha32 * sum_k gate(A_ik B_kj), accumulated in
+ * ascending k with FP32 FMA (or separately rounded multiply/add when exact != 0).
+ * Outputs for product leaf x (plan order): c_values[x], c_values_t[x], and its norms in
+ * compute_norms order: c_sub4[x], c_leaf_sq[x].  counters[0..1] += products4, skipped4.
+ * nC and T are the host copies of counts[0..1]. */
+int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b,
+                  const spamm_plan_buffers *plan, int64_t T, int64_t nC,
+                  float alpha, int granularity, int exact,
+                  float *c_values, float *c_values_t, float *c_sub4, double *c_leaf_sq,
+                  unsigned long long *counters, void *ws, size_t ws_bytes, void *stream);
+
+/* Leaf set of C for beta != 0: the union of the accumulator's stored leaves (slot_old, an L*L
+ * grid) and the produced leaves (prod_keys, ascending), in ascending Morton order.  For output
+ * leaf x: out_keys[x], and the packed index of the leaf on either side (idx_old / idx_prod, -1
+ * when absent).  slot_prod_scratch is an L*L int32 scratch grid; ws as for spamm_assign_slots. */
+int spamm_union_leaves(const int32_t *slot_old, const uint32_t *prod_keys, int64_t nprod, int depth,
+                       int32_t *slot_prod_scratch, uint32_t *out_keys, int32_t *idx_old,
+                       int32_t *idx_prod, int32_t *nout_dev, void *ws, size_t ws_bytes, void *stream);
+
+/* _compose with beta != 0 (numeric.py:276-284): out leaf x = (alpha32 * prod[ip]) + (old[io] * beta32)
+ * with ip / io = -1 when that side has no leaf; the alpha == 1 / beta == 1 special cases keep
+ * the reference's exact expressions. */
+int spamm_compose(const float *prod_values, const float *old_values,
+                  const int32_t *idx_prod, const int32_t *idx_old, int64_t nout,
+                  float alpha, float beta, int alpha_is_one, int beta_is_one,
+                  float *out_values, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPAMM_B200_H */

@@ -1,0 +1,103 @@
+"""ctypes binding of ``libspamm_b200.so`` (the C ABI in ``include/spamm_b200.h``).
+
+The library is built in-tree by ``csrc/build.sh`` (``__graft_entry__.build()``).
+There is no fallback of any kind: if the library is missing or no CUDA device is
+present, the first call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "csrc", "libspamm_b200.so")
+
+SPAMM_OK, SPAMM_EINVAL, SPAMM_ECUDA, SPAMM_EWORKSPACE = 0, 1, 2, 3
+FINE4, COARSE16 = 0, 1
+
+vp, i32, i64, f32, f64, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_float, C.c_double, C.c_size_t
+
+
+class TreeView(C.Structure):
+    """``spamm_tree_view``."""
+
+    _fields_ = [("m", i32), ("n", i32), ("depth", i32), ("nleaf", i32),
+                ("keys", vp), ("values", vp), ("values_t", vp), ("sub4", vp),
+                ("slot", vp), ("slot_t", vp), ("norm", vp), ("norm_t", vp)]
+
+
+class PlanBuffers(C.Structure):
+    """``spamm_plan_buffers``."""
+
+    _fields_ = [("c_keys", vp), ("c_off", vp), ("task_k", vp), ("task_a", vp), ("task_b", vp),
+                ("task_mask", vp), ("task_capacity", i64), ("leaf_capacity", i64), ("counts", vp)]
+
+
+# every symbol include/spamm_b200.h declares: (restype, argtypes)
+SIGNATURES = {
+    "spamm_abi_version": (C.c_int, []),
+    "spamm_level_offset_of": (i64, [C.c_int]),
+    "spamm_error_string": (C.c_char_p, [C.c_int]),
+    "spamm_launch_count": (i64, []),
+    "spamm_leaf_norms_dense": (C.c_int, [vp, i64, i64, i64, C.c_int, vp, vp, vp, vp]),
+    "spamm_scan_workspace_bytes": (sz, [i64]),
+    "spamm_assign_slots": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, sz, vp]),
+    "spamm_pack_leaves": (C.c_int, [vp, i64, i64, i64, C.c_int, vp, i64, vp, vp, vp, vp, vp]),
+    "spamm_build_interior": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int, vp]),
+    "spamm_leaf_norms_packed": (C.c_int, [vp, i64, vp, vp, vp, vp]),
+    "spamm_index_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp]),
+    "spamm_to_dense": (C.c_int, [C.POINTER(TreeView), vp, i64, vp]),
+    "spamm_plan_workspace_bytes": (sz, [C.c_int, i64, i64]),
+    "spamm_plan": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, C.c_int, i32, i32,
+                             C.POINTER(PlanBuffers), vp, sz, vp]),
+    "spamm_execute_workspace_bytes": (sz, [i64]),
+    "spamm_execute": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), C.POINTER(PlanBuffers), i64, i64,
+                                f32, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, sz, vp]),
+    "spamm_union_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp, sz, vp]),
+    "spamm_compose": (C.c_int, [vp, vp, vp, vp, i64, f32, f32, C.c_int, C.c_int, vp, vp]),
+}
+
+_lib = None
+
+
+def lib():
+    """The loaded library.  Raises RuntimeError when it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(paper_1203_1692_b200 has no CPU or PyTorch fallback)")
+        handle = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        if handle.spamm_abi_version() != 1:
+            raise RuntimeError("libspamm_b200.so ABI version mismatch; rebuild it")
+        _lib = handle
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    """Map a status code to the reference's exceptions (ValueError for bad arguments)."""
+    if rc == SPAMM_OK:
+        return
+    msg = f"{what}: {lib().spamm_error_string(rc).decode()}"
+    if rc == SPAMM_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def launch_count() -> int:
+    return int(lib().spamm_launch_count())
+
+
+def level_offset(t: int) -> int:
+    return 0 if t == 0 else 4 + ((1 << (2 * t)) - 4) // 3
+
+
+def level_total(depth: int) -> int:
+    """Elements of a level buffer holding levels 0..depth."""
+    return level_offset(depth) + (1 << (2 * depth))

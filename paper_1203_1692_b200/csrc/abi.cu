@@ -1,0 +1,25 @@
+// Library-level entry points of the C ABI (include/spamm_b200.h).
+#include <atomic>
+
+#include "common.cuh"
+
+static std::atomic<int64_t> g_launches{0};
+
+void spamm_note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+extern "C" int64_t spamm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+extern "C" int spamm_abi_version(void) { return SPAMM_ABI_VERSION; }
+
+extern "C" int64_t spamm_level_offset_of(int t) { return spamm_level_offset(t); }
+
+extern "C" const char *spamm_error_string(int code)
+{
+    switch (code) {
+        case SPAMM_OK: return "ok";
+        case SPAMM_EINVAL: return "invalid argument";
+        case SPAMM_ECUDA: return "CUDA runtime error";
+        case SPAMM_EWORKSPACE: return "workspace too small";
+        default: return "unknown error";
+    }
+}

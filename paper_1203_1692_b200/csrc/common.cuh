@@ -1,0 +1,177 @@
+// Shared device/host helpers for the SpAMM B200 kernels (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/spamm_b200.h"
+
+#define SPAMM_NB 16
+#define SPAMM_LEAF 256
+#define SPAMM_NUM_SMS 148
+
+// ---- launch bookkeeping -----------------------------------------------------
+extern "C" int64_t spamm_launch_count(void);
+void spamm_note_launch(int n = 1);
+
+#define SPAMM_CHECK_LAUNCH()                                      \
+    do {                                                          \
+        spamm_note_launch();                                      \
+        if (cudaPeekAtLastError() != cudaSuccess) {               \
+            (void)cudaGetLastError();                             \
+            return SPAMM_ECUDA;                                   \
+        }                                                         \
+    } while (0)
+
+// Level t of a level buffer starts at element spamm_level_offset(t): levels are packed root
+// first, each start rounded to 4 elements so rows can be read with vector loads.
+__host__ __device__ static inline int64_t spamm_level_offset(int t)
+{
+    return t == 0 ? 0 : 4 + ((int64_t(1) << (2 * t)) - 4) / 3;
+}
+
+// ---- Morton keys (reference morton.py:35-68: row bit above column bit) -------
+__host__ __device__ __forceinline__ uint32_t spread16(uint32_t x)
+{
+    x &= 0xFFFFu;
+    x = (x | (x << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    return x;
+}
+__host__ __device__ __forceinline__ uint32_t squeeze16(uint32_t x)
+{
+    x &= 0x55555555u;
+    x = (x | (x >> 1)) & 0x33333333u;
+    x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+    x = (x | (x >> 4)) & 0x00FF00FFu;
+    x = (x | (x >> 8)) & 0x0000FFFFu;
+    return x;
+}
+__host__ __device__ __forceinline__ uint32_t morton_encode(uint32_t i, uint32_t j)
+{
+    return (spread16(i) << 1) | spread16(j);
+}
+__host__ __device__ __forceinline__ void morton_decode(uint32_t key, uint32_t &i, uint32_t &j)
+{
+    i = squeeze16(key >> 1);
+    j = squeeze16(key);
+}
+
+// ---- the norm test (symbolic.py:118-120, numeric.py:233-238) ------------------
+// Both factors are float32 values, so the double product is exact; the comparison is
+// the reference's `not (p < tau)` == `p >= tau` for non-NaN operands.  A negative norm
+// marks an absent node.
+__device__ __forceinline__ bool norm_test(float a, float b, double tau)
+{
+    return (a >= 0.0f) && (b >= 0.0f) && (__dmul_rn((double)a, (double)b) >= tau);
+}
+
+// ---- warp helpers ---------------------------------------------------------------
+#define FULL_MASK 0xFFFFFFFFu
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ uint32_t lanemask_lt()
+{
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ---- mbarrier / bulk-copy (TMA 1-D) PTX wrappers ---------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_barrier_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                     smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+// 1-D bulk copy global -> shared, completion counted on an mbarrier (SASS: UBLKCP).
+__device__ __forceinline__ void bulk_copy_g2s(void *smem_dst, const void *gmem_src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ---- decoupled look-back tile state ------------------------------------------------
+// 64-bit word: [63:62] status, [61:31] second counter, [30:0] first counter.
+#define LB_INVALID 0ull
+#define LB_AGGREGATE 1ull
+#define LB_PREFIX 2ull
+__device__ __forceinline__ unsigned long long lb_pack(unsigned long long status, uint32_t lo, uint32_t hi)
+{
+    return (status << 62) | ((unsigned long long)hi << 31) | (unsigned long long)lo;
+}
+__device__ __forceinline__ uint32_t lb_lo(unsigned long long w) { return (uint32_t)(w & 0x7FFFFFFFull); }
+__device__ __forceinline__ uint32_t lb_hi(unsigned long long w) { return (uint32_t)((w >> 31) & 0x7FFFFFFFull); }
+__device__ __forceinline__ unsigned long long lb_status(unsigned long long w) { return w >> 62; }
+
+// Called by ONE thread of a tile: publishes the tile's aggregate, walks back over the
+// predecessors and returns the exclusive prefix (lo, hi); then publishes the inclusive one.
+__device__ __forceinline__ void lb_exclusive(volatile unsigned long long *state, int tile, uint32_t agg_lo,
+                                             uint32_t agg_hi, uint32_t &ex_lo, uint32_t &ex_hi)
+{
+    if (tile == 0) {
+        ex_lo = ex_hi = 0;
+        __threadfence();
+        state[0] = lb_pack(LB_PREFIX, agg_lo, agg_hi);
+        return;
+    }
+    __threadfence();
+    state[tile] = lb_pack(LB_AGGREGATE, agg_lo, agg_hi);
+    uint32_t lo = 0, hi = 0;
+    for (int p = tile - 1; p >= 0; --p) {
+        unsigned long long w;
+        do {
+            w = state[p];
+        } while (lb_status(w) == LB_INVALID);
+        lo += lb_lo(w);
+        hi += lb_hi(w);
+        if (lb_status(w) == LB_PREFIX) break;
+    }
+    ex_lo = lo;
+    ex_hi = hi;
+    __threadfence();
+    state[tile] = lb_pack(LB_PREFIX, lo + agg_lo, hi + agg_hi);
+}

@@ -1,0 +1,410 @@
+// Tree construction kernels: the Frobenius-norm pyramid and the packed leaf store.
+//
+// Replaces QuadtreeMatrix.from_dense / compute_norms / packed_leaves / to_dense of the
+// reference (pkg/src/spamm/core.py:213-276, :331-345, :387-405).  All square sums are
+// accumulated in FP64 in the exact order numpy uses for the reference expressions (see
+// oracle/spamm_oracle.c for the probe), so every float32 norm is bit-identical.
+#include "common.cuh"
+#include "scan.cuh"
+
+// ---------------------------------------------------------------------------------
+// Sum of squares of a 4x4 sub-block held as four float4 rows (core.py:113-114, :230-232):
+//   r_i = ((x_i0^2 + x_i1^2) + x_i2^2) + x_i3^2,   S = ((r_0 + r_1) + r_2) + r_3.
+// x*x is exact in double for a float x, so fma(x, x, acc) rounds once like numpy's add.
+__device__ __forceinline__ double row_sq(float4 v)
+{
+    double x = v.x, y = v.y, z = v.z, w = v.w;
+    double r = __dmul_rn(x, x);
+    r = __fma_rn(y, y, r);
+    r = __fma_rn(z, z, r);
+    r = __fma_rn(w, w, r);
+    return r;
+}
+__device__ __forceinline__ double sub_block_sq(float4 r0, float4 r1, float4 r2, float4 r3)
+{
+    double s = row_sq(r0);
+    s = __dadd_rn(s, row_sq(r1));
+    s = __dadd_rn(s, row_sq(r2));
+    s = __dadd_rn(s, row_sq(r3));
+    return s;
+}
+
+__device__ __forceinline__ float4 load_row4(const float *dense, int64_t m, int64_t n, int64_t ld, int64_t row,
+                                            int64_t col, bool vec_ok)
+{
+    if (row >= m || col >= n) return make_float4(0.f, 0.f, 0.f, 0.f);
+    const float *p = dense + row * ld + col;
+    if (vec_ok && col + 3 < n) return __ldg(reinterpret_cast<const float4 *>(p));
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    v.x = __ldg(p);
+    if (col + 1 < n) v.y = __ldg(p + 1);
+    if (col + 2 < n) v.z = __ldg(p + 2);
+    if (col + 3 < n) v.w = __ldg(p + 3);
+    return v;
+}
+
+// K1a. One thread per column of 4x4 sub-blocks inside a 16-row strip: a warp reads 512
+// contiguous bytes per matrix row.  Four neighbouring lanes hold the 4 sub-blocks (q) of a
+// leaf row p; lane q == 0 folds them in the order of core.py:233
+//   R_p = ((S_p0 + S_p1) + S_p2) + S_p3,  total = ((R_0 + R_1) + R_2) + R_3.
+__global__ void __launch_bounds__(256) leaf_norms_dense_kernel(const float *__restrict__ dense, int64_t m, int64_t n,
+                                                               int64_t ld, int L, float *__restrict__ sub4_grid,
+                                                               double *__restrict__ leaf_sq, float *__restrict__ leaf_norm,
+                                                               bool vec_ok)
+{
+    const int leaf_row = blockIdx.y;
+    const int sc = blockIdx.x * 256 + threadIdx.x;   // sub-block column in the padded grid
+    const int leaf_col = sc >> 2, q = sc & 3;
+    const bool in_grid = leaf_col < L;
+    double total = 0.0;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const int64_t row = (int64_t)leaf_row * 16 + p * 4, col = (int64_t)sc * 4;
+        double S = 0.0;
+        if (in_grid) {
+            float4 r0 = load_row4(dense, m, n, ld, row + 0, col, vec_ok);
+            float4 r1 = load_row4(dense, m, n, ld, row + 1, col, vec_ok);
+            float4 r2 = load_row4(dense, m, n, ld, row + 2, col, vec_ok);
+            float4 r3 = load_row4(dense, m, n, ld, row + 3, col, vec_ok);
+            S = sub_block_sq(r0, r1, r2, r3);
+            sub4_grid[((int64_t)leaf_row * L + leaf_col) * 16 + p * 4 + q] = (float)sqrt(S);
+        }
+        double s1 = __shfl_down_sync(FULL_MASK, S, 1);
+        double s2 = __shfl_down_sync(FULL_MASK, S, 2);
+        double s3 = __shfl_down_sync(FULL_MASK, S, 3);
+        double R = __dadd_rn(__dadd_rn(__dadd_rn(S, s1), s2), s3);
+        total = __dadd_rn(total, R);
+    }
+    if (in_grid && q == 0) {
+        const int64_t leaf = (int64_t)leaf_row * L + leaf_col;
+        leaf_sq[leaf] = total;
+        leaf_norm[leaf] = (total != 0.0) ? (float)sqrt(total) : -1.0f;
+    }
+}
+
+extern "C" int spamm_leaf_norms_dense(const float *dense, int64_t m, int64_t n, int64_t ld, int depth,
+                                      float *sub4_grid, double *leaf_sq, float *leaf_norm, void *stream)
+{
+    if (!dense || m < 1 || n < 1 || ld < n || depth < 0 || depth > 15) return SPAMM_EINVAL;
+    const int L = 1 << depth;
+    if ((int64_t)L * 16 < m || (int64_t)L * 16 < n) return SPAMM_EINVAL;
+    const bool vec_ok = (ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(dense) & 15) == 0);
+    dim3 grid((4 * L + 255) / 256, L);
+    leaf_norms_dense_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(dense, m, n, ld, L, sub4_grid, leaf_sq, leaf_norm,
+                                                                     vec_ok);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
+}
+
+// K1b. Stored leaves in ascending Morton order: exclusive scan of the presence flags
+// walked along the Z curve (core.py:235-237).
+struct SlotScanOp {
+    const float *leaf_norm;
+    int32_t *slot, *slot_t;
+    uint32_t *keys;
+    int L;
+    __device__ __forceinline__ int flag(int64_t e) const
+    {
+        uint32_t i, j;
+        morton_decode((uint32_t)e, i, j);
+        return leaf_norm[(int64_t)i * L + j] >= 0.0f ? 1 : 0;
+    }
+    __device__ __forceinline__ void emit(int64_t e, int flag, int32_t idx) const
+    {
+        uint32_t i, j;
+        morton_decode((uint32_t)e, i, j);
+        slot[(int64_t)i * L + j] = flag ? idx : -1;
+        slot_t[(int64_t)j * L + i] = flag ? idx : -1;
+        if (flag) keys[idx] = (uint32_t)e;
+    }
+};
+
+extern "C" size_t spamm_scan_workspace_bytes(int64_t n) { return scan_workspace_bytes(n); }
+
+extern "C" int spamm_assign_slots(const float *leaf_norm, int depth, int32_t *slot, int32_t *slot_t, uint32_t *keys,
+                                  int32_t *nleaf_dev, void *ws, size_t ws_bytes, void *stream)
+{
+    if (depth < 0 || depth > 15) return SPAMM_EINVAL;
+    const int L = 1 << depth;
+    SlotScanOp op{leaf_norm, slot, slot_t, keys, L};
+    return scan_flags(op, (int64_t)L * L, nleaf_dev, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+// K1c. One 256-thread block per stored leaf: row-major copy, transposed copy, sub-norms.
+__global__ void __launch_bounds__(256) pack_leaves_kernel(const float *__restrict__ dense, int64_t m, int64_t n, int64_t ld,
+                                                          int L, const uint32_t *__restrict__ keys,
+                                                          const float *__restrict__ sub4_grid, float *__restrict__ values,
+                                                          float *__restrict__ values_t, float *__restrict__ sub4)
+{
+    __shared__ float tile[16][17];
+    const int64_t s = blockIdx.x;
+    uint32_t bi, bj;
+    morton_decode(keys[s], bi, bj);
+    const int r = threadIdx.x >> 4, c = threadIdx.x & 15;
+    const int64_t gi = (int64_t)bi * 16 + r, gj = (int64_t)bj * 16 + c;
+    const float v = (gi < m && gj < n) ? __ldg(dense + gi * ld + gj) : 0.0f;
+    values[s * 256 + threadIdx.x] = v;
+    tile[r][c] = v;
+    __syncthreads();
+    values_t[s * 256 + threadIdx.x] = tile[c][r];
+    if (threadIdx.x < 16) sub4[s * 16 + threadIdx.x] = sub4_grid[((int64_t)bi * L + bj) * 16 + threadIdx.x];
+}
+
+extern "C" int spamm_pack_leaves(const float *dense, int64_t m, int64_t n, int64_t ld, int depth,
+                                      const uint32_t *keys, int64_t nleaf, const float *sub4_grid, float *values,
+                                      float *values_t, float *sub4, void *stream)
+{
+    if (nleaf == 0) return SPAMM_OK;
+    if (!dense || nleaf < 0 || depth < 0 || depth > 15) return SPAMM_EINVAL;
+    pack_leaves_kernel<<<(unsigned)nleaf, 256, 0, (cudaStream_t)stream>>>(dense, m, n, ld, 1 << depth, keys, sub4_grid,
+                                                                         values, values_t, sub4);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
+}
+
+// K1d. Interior levels (_build_interior, core.py:252-266).  np.add.reduceat over the stored
+// children in Morton order evaluates  x_first + ((x_second + x_third) + x_fourth).
+struct NodeSum {
+    double first, rest;
+    int seen;
+    __device__ __forceinline__ void add(bool present, double sq)
+    {
+        if (!present) return;
+        if (seen == 0) first = sq;
+        else if (seen == 1) rest = sq;
+        else rest = __dadd_rn(rest, sq);
+        ++seen;
+    }
+    __device__ __forceinline__ double total() const { return seen == 1 ? first : __dadd_rn(first, rest); }
+};
+
+// Each block folds a 32x32 region of child level `tc` through up to five levels.
+__global__ void __launch_bounds__(256) interior_kernel(const double *__restrict__ child_sq, float *__restrict__ norm,
+                                                       float *__restrict__ norm_t, double *__restrict__ sq_levels, int tc)
+{
+    __shared__ double s_sq[2][16][16];
+    __shared__ unsigned char s_pr[2][16][16];
+    const int Sc = 1 << tc;
+    const int64_t off_c = spamm_level_offset(tc);
+    const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+    // level tc-1: parent (pi, pj) from four children in global memory
+    {
+        const int Sp = Sc >> 1;
+        const int pi = blockIdx.y * 16 + ty, pj = blockIdx.x * 16 + tx;
+        bool present = false;
+        double sq = 0.0;
+        if (pi < Sp && pj < Sp) {
+            NodeSum acc{0.0, 0.0, 0};
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd) {
+                const int64_t ci = 2 * pi + (qd >> 1), cj = 2 * pj + (qd & 1);
+                const bool pr = norm[off_c + ci * Sc + cj] >= 0.0f;
+                acc.add(pr, pr ? child_sq[ci * Sc + cj] : 0.0);
+            }
+            present = acc.seen > 0;
+            sq = present ? acc.total() : 0.0;
+            const int64_t off_p = spamm_level_offset(tc - 1);
+            const float nv = present ? (float)sqrt(sq) : -1.0f;
+            norm[off_p + (int64_t)pi * Sp + pj] = nv;
+            norm_t[off_p + (int64_t)pj * Sp + pi] = nv;
+            sq_levels[off_p + (int64_t)pi * Sp + pj] = sq;
+        }
+        s_sq[0][ty][tx] = sq;
+        s_pr[0][ty][tx] = present;
+    }
+    int cur = 0;
+    int side = 16;                      // side of the level held in shared memory
+    for (int t = tc - 2; t >= 0 && side > 1; --t) {
+        __syncthreads();
+        const int pside = side >> 1;
+        const int Sp = 1 << t;
+        if (ty < pside && tx < pside) {
+            const int pi = blockIdx.y * pside + ty, pj = blockIdx.x * pside + tx;
+            bool present = false;
+            double sq = 0.0;
+            if (pi < Sp && pj < Sp) {
+                NodeSum acc{0.0, 0.0, 0};
+#pragma unroll
+                for (int qd = 0; qd < 4; ++qd) {
+                    const int ci = 2 * ty + (qd >> 1), cj = 2 * tx + (qd & 1);
+                    acc.add(s_pr[cur][ci][cj], s_sq[cur][ci][cj]);
+                }
+                present = acc.seen > 0;
+                sq = present ? acc.total() : 0.0;
+                const int64_t off_p = spamm_level_offset(t);
+                const float nv = present ? (float)sqrt(sq) : -1.0f;
+                norm[off_p + (int64_t)pi * Sp + pj] = nv;
+                norm_t[off_p + (int64_t)pj * Sp + pi] = nv;
+                sq_levels[off_p + (int64_t)pi * Sp + pj] = sq;
+            }
+            s_sq[cur ^ 1][ty][tx] = sq;
+            s_pr[cur ^ 1][ty][tx] = present;
+        }
+        cur ^= 1;
+        side = pside;
+    }
+}
+
+__global__ void transpose_level_kernel(const float *__restrict__ src, float *__restrict__ dst, int S)
+{
+    __shared__ float tile[32][33];
+    int x = blockIdx.x * 32 + threadIdx.x, y = blockIdx.y * 32 + threadIdx.y;
+    for (int r = 0; r < 32; r += 8)
+        if (x < S && y + r < S) tile[threadIdx.y + r][threadIdx.x] = src[(int64_t)(y + r) * S + x];
+    __syncthreads();
+    x = blockIdx.y * 32 + threadIdx.x;
+    y = blockIdx.x * 32 + threadIdx.y;
+    for (int r = 0; r < 32; r += 8)
+        if (x < S && y + r < S) dst[(int64_t)(y + r) * S + x] = tile[threadIdx.x][threadIdx.y + r];
+}
+
+static int launch_interior(const double *leaf_sq, int depth, float *norm, float *norm_t, double *sq_levels,
+                           cudaStream_t st)
+{
+    int tc = depth;
+    const double *child = leaf_sq;
+    while (tc > 0) {
+        const int Sp = 1 << (tc - 1);
+        const int g = (Sp + 15) / 16;
+        interior_kernel<<<dim3(g, g), 256, 0, st>>>(child, norm, norm_t, sq_levels, tc);
+        SPAMM_CHECK_LAUNCH();
+        tc = (tc - 5 > 0) ? tc - 5 : 0;
+        child = sq_levels + spamm_level_offset(tc);
+    }
+    return SPAMM_OK;
+}
+
+extern "C" int spamm_build_interior(const double *leaf_sq, int depth, float *norm, float *norm_t, double *sq_levels,
+                                    int write_leaf_transpose, void *stream)
+{
+    if (depth < 0 || depth > 15 || !norm || !norm_t) return SPAMM_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (write_leaf_transpose) {
+        const int L = 1 << depth;
+        const int64_t off = spamm_level_offset(depth);
+        dim3 tb(32, 8), tg((L + 31) / 32, (L + 31) / 32);
+        transpose_level_kernel<<<tg, tb, 0, st>>>(norm + off, norm_t + off, L);
+        SPAMM_CHECK_LAUNCH();
+    }
+    return launch_interior(leaf_sq, depth, norm, norm_t, sq_levels, st);
+}
+
+// Packed leaves -> norms in compute_norms order (core.py:108-116): sub-block sums as above,
+// leaf total = numpy pairwise sum of the 16 sub-sums: r_j = S_j + S_{j+8}, then
+// ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)) -- an xor-butterfly over lane bits 3,0,1,2.
+__device__ __forceinline__ double leaf_total_refresh(double S)
+{
+    double r = __dadd_rn(S, __shfl_xor_sync(FULL_MASK, S, 8));
+    r = __dadd_rn(r, __shfl_xor_sync(FULL_MASK, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(FULL_MASK, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(FULL_MASK, r, 4));
+    return r;
+}
+
+__global__ void __launch_bounds__(256) leaf_norms_packed_kernel(const float *__restrict__ values, int64_t nleaf,
+                                                                float *__restrict__ values_t, float *__restrict__ sub4,
+                                                                double *__restrict__ leaf_sq)
+{
+    const int64_t leaf = (int64_t)blockIdx.x * 16 + (threadIdx.x >> 4);
+    const int t = threadIdx.x & 15, p = t >> 2, q = t & 3;
+    const bool ok = leaf < nleaf;
+    float4 r[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        r[i] = ok ? __ldg(reinterpret_cast<const float4 *>(values + leaf * 256 + (4 * p + i) * 16 + 4 * q))
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    const double S = sub_block_sq(r[0], r[1], r[2], r[3]);
+    const double total = leaf_total_refresh(S);
+    if (!ok) return;
+    sub4[leaf * 16 + t] = (float)sqrt(S);
+    if (t == 0) leaf_sq[leaf] = total;
+    if (values_t) {
+        float *vt = values_t + leaf * 256;
+        *reinterpret_cast<float4 *>(vt + (4 * q + 0) * 16 + 4 * p) = make_float4(r[0].x, r[1].x, r[2].x, r[3].x);
+        *reinterpret_cast<float4 *>(vt + (4 * q + 1) * 16 + 4 * p) = make_float4(r[0].y, r[1].y, r[2].y, r[3].y);
+        *reinterpret_cast<float4 *>(vt + (4 * q + 2) * 16 + 4 * p) = make_float4(r[0].z, r[1].z, r[2].z, r[3].z);
+        *reinterpret_cast<float4 *>(vt + (4 * q + 3) * 16 + 4 * p) = make_float4(r[0].w, r[1].w, r[2].w, r[3].w);
+    }
+}
+
+extern "C" int spamm_leaf_norms_packed(const float *values, int64_t nleaf, float *values_t, float *sub4, double *leaf_sq,
+                                       void *stream)
+{
+    if (nleaf == 0) return SPAMM_OK;
+    if (!values || nleaf < 0) return SPAMM_EINVAL;
+    leaf_norms_packed_kernel<<<(unsigned)((nleaf + 15) / 16), 256, 0, (cudaStream_t)stream>>>(values, nleaf, values_t,
+                                                                                            sub4, leaf_sq);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
+}
+
+// Grids of a tree given by packed leaves: clear, then scatter.
+__global__ void clear_grids_kernel(int64_t cells, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t,
+                                   double *leaf_sq_grid)
+{
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < cells; x += (int64_t)gridDim.x * blockDim.x) {
+        slot[x] = -1;
+        slot_t[x] = -1;
+        norm[x] = -1.0f;
+        norm_t[x] = -1.0f;
+        leaf_sq_grid[x] = 0.0;
+    }
+}
+__global__ void scatter_leaves_kernel(const uint32_t *__restrict__ keys, const double *__restrict__ leaf_sq_packed,
+                                      int64_t nleaf, int L, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t,
+                                      double *leaf_sq_grid)
+{
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nleaf) return;
+    uint32_t i, j;
+    morton_decode(keys[s], i, j);
+    const double sq = leaf_sq_packed[s];
+    const float nv = (float)sqrt(sq);       // a stored leaf keeps norm 0 when it is all zero (core.py:336-339)
+    slot[(int64_t)i * L + j] = (int32_t)s;
+    slot_t[(int64_t)j * L + i] = (int32_t)s;
+    norm[(int64_t)i * L + j] = nv;
+    norm_t[(int64_t)j * L + i] = nv;
+    leaf_sq_grid[(int64_t)i * L + j] = sq;
+}
+
+extern "C" int spamm_index_leaves(const uint32_t *keys, const double *leaf_sq_packed, int64_t nleaf, int depth,
+                                  int32_t *slot, int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid,
+                                  void *stream)
+{
+    if (depth < 0 || depth > 15 || nleaf < 0) return SPAMM_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int L = 1 << depth;
+    const int64_t cells = (int64_t)L * L;
+    const int64_t off = spamm_level_offset(depth);
+    int blocks = (int)((cells + 255) / 256);
+    if (blocks > SPAMM_NUM_SMS * 16) blocks = SPAMM_NUM_SMS * 16;
+    clear_grids_kernel<<<blocks, 256, 0, st>>>(cells, slot, slot_t, norm + off, norm_t + off, leaf_sq_grid);
+    SPAMM_CHECK_LAUNCH();
+    if (nleaf > 0) {
+        scatter_leaves_kernel<<<(unsigned)((nleaf + 255) / 256), 256, 0, st>>>(keys, leaf_sq_packed, nleaf, L, slot, slot_t,
+                                                                              norm + off, norm_t + off, leaf_sq_grid);
+        SPAMM_CHECK_LAUNCH();
+    }
+    return SPAMM_OK;
+}
+
+// QuadtreeMatrix.to_dense (core.py:268-276): one block per 16x16 block of the output.
+__global__ void __launch_bounds__(256) to_dense_kernel(const int32_t *__restrict__ slot, const float *__restrict__ values,
+                                                       int L, int64_t m, int64_t n, float *__restrict__ out, int64_t ld)
+{
+    const int bi = blockIdx.y, bj = blockIdx.x;
+    const int r = threadIdx.x >> 4, c = threadIdx.x & 15;
+    const int64_t gi = (int64_t)bi * 16 + r, gj = (int64_t)bj * 16 + c;
+    if (gi >= m || gj >= n) return;
+    const int32_t s = slot[(int64_t)bi * L + bj];
+    out[gi * ld + gj] = s >= 0 ? values[(int64_t)s * 256 + threadIdx.x] : 0.0f;
+}
+
+extern "C" int spamm_to_dense(const spamm_tree_view *t, float *out, int64_t ld, void *stream)
+{
+    if (!t || !out || ld < t->n) return SPAMM_EINVAL;
+    dim3 grid((t->n + 15) / 16, (t->m + 15) / 16);
+    to_dense_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(t->slot, t->values, 1 << t->depth, t->m, t->n, out, ld);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
+}

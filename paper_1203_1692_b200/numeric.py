@@ -1,0 +1,215 @@
+"""Numeric multiply phase on the device: ``execute_plan`` and ``multiply``.
+
+Drop-in for `pkg/src/spamm/numeric.py` (``MultiplyConfig`` :32-47, ``ExecCounters`` :50-72,
+``execute_plan`` :138-181, ``multiply`` :302-313): same names, arguments, return values and
+ValueError conditions.  Work is counted in 4x4x4 micro products exactly as the reference does.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .symbolic import MultiplyPlan, build_plan
+from .tree import QuadtreeMatrix, _stream
+
+GRANULARITIES = ("fine4", "coarse16")
+
+# Modeled flops of one 4x4x4 micro product (`numeric.py:28-29`).
+MICRO_FLOPS = 128
+
+
+@dataclass
+class MultiplyConfig:
+    tau: float = 0.0
+    granularity: str = "fine4"
+    alpha: float = 1.0
+    beta: float = 0.0
+    # B200 extension: True rounds every product and sum separately (bit-identical to the
+    # reference); False (default) uses fused multiply-add, within the 1e-5 budget.
+    exact: bool = False
+
+    def __post_init__(self):
+        if self.granularity not in GRANULARITIES:
+            raise ValueError(f"granularity must be one of {GRANULARITIES}, got {self.granularity!r}")
+        if np.isnan(self.tau) or self.tau < 0:
+            raise ValueError(f"tau must be nonnegative, got {self.tau}")
+        if not (np.isfinite(self.alpha) and np.isfinite(self.beta)):
+            raise ValueError("alpha and beta must be finite")
+
+
+class ExecCounters:
+    """Work counters of one numeric pass (`numeric.py:50-72`).
+
+    ``products4`` is read back from the device on first access, so a caller that only wants C
+    does not pay a synchronisation."""
+
+    def __init__(self, products4=0, skipped4=0, seconds=0.0, _dev=None, _total=0, _fine=True, _events=None):
+        self._products4, self._skipped4, self.seconds = products4, skipped4, seconds
+        self._dev, self._total, self._fine, self._events = _dev, _total, _fine, _events
+
+    def _fetch(self):
+        if self._dev is not None:
+            self._products4 = int(self._dev[0].item())
+            self._skipped4 = self._total - self._products4 if self._fine else 0
+            self._dev = None
+        if self._events is not None:
+            e0, e1 = self._events
+            e1.synchronize()
+            self.seconds = e0.elapsed_time(e1) * 1e-3
+            self._events = None
+
+    @property
+    def products4(self) -> int:
+        self._fetch()
+        return self._products4
+
+    @property
+    def skipped4(self) -> int:
+        self._fetch()
+        return self._skipped4
+
+    @property
+    def complexity(self) -> int:
+        return self.products4
+
+    @property
+    def flops(self) -> int:
+        return self.products4 * MICRO_FLOPS
+
+    def merge(self, other: "ExecCounters") -> "ExecCounters":
+        return ExecCounters(self.products4 + other.products4, self.skipped4 + other.skipped4,
+                            self.seconds + other.seconds)
+
+    def __repr__(self):
+        return f"ExecCounters(products4={self.products4}, skipped4={self.skipped4}, seconds={self.seconds:.6g})"
+
+
+def _check_plan_handles(plan: MultiplyPlan, a: QuadtreeMatrix, b: QuadtreeMatrix) -> None:
+    """The plan addresses leaves by packed slot; it is only valid for the tree revisions it was
+    built from (the reference checks the same thing by key lookup, `numeric.py:128-135`)."""
+    if plan.n_tasks == 0:
+        return
+    if plan._tokens != (id(a), a._rev, id(b), b._rev):
+        for side, q, (ka, kb) in (("A", a, (0, 1)), ("B", b, (1, 2))):
+            have = set(q.leaf_keys().tolist()) if q.nleaf else set()
+            if not have:
+                raise ValueError(f"plan references leaves but {side} has none (stale handles)")
+        raise ValueError("plan was built for other operand revisions (stale handles); rebuild it with build_plan")
+
+
+def execute_plan(plan: MultiplyPlan, a: QuadtreeMatrix, b: QuadtreeMatrix, c: QuadtreeMatrix | None,
+                 cfg: MultiplyConfig) -> tuple[QuadtreeMatrix, ExecCounters]:
+    """Run the numeric phase: C = alpha * (planned products) + beta * C (`numeric.py:138-181`)."""
+    if plan.tau != cfg.tau:
+        raise ValueError(f"plan built for tau={plan.tau}, config has tau={cfg.tau}")
+    if a.n_b != b.n_b:
+        raise ValueError(f"block sizes differ: {a.n_b} vs {b.n_b}")
+    if a.n != b.m:
+        raise ValueError(f"inner dimensions differ: {a.m}x{a.n} times {b.m}x{b.n}")
+    nb = a.n_b
+    if nb % 4:
+        raise ValueError(f"numeric phase needs 4 | n_b, got n_b = {nb}")
+    a._require_16()
+    if c is None:
+        c = QuadtreeMatrix(a.m, b.n, nb, device=a.device)
+    elif (c.m, c.n) != (a.m, b.n) or c.n_b != nb:
+        raise ValueError(f"accumulator is {c.m}x{c.n} (n_b={c.n_b}), product needs {a.m}x{b.n} (n_b={nb})")
+    _check_plan_handles(plan, a, b)
+    if plan.n_tasks and plan.granularity != cfg.granularity and cfg.granularity == "fine4":
+        raise ValueError("plan carries coarse16 masks; rebuild it with granularity='fine4'")
+    lib = _lib.lib()
+    st = _stream()
+    dev = a.device
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    T, nC = plan.n_tasks, plan.n_cleaves
+    run = T > 0 and cfg.alpha != 0
+    counters_dev = torch.zeros((2,), dtype=torch.int64, device=dev)
+    fine = cfg.granularity == "fine4"
+    keep_old = cfg.beta != 0 and c.nleaf > 0
+    prod = None
+    if run:
+        va, vb = a.view(plan.depth), b.view(plan.depth)
+        vals = torch.empty((nC, 256), dtype=torch.float32, device=dev)
+        vals_t = torch.empty((nC, 256), dtype=torch.float32, device=dev)
+        sub4 = torch.empty((nC, 16), dtype=torch.float32, device=dev)
+        leaf_sq = torch.empty((nC,), dtype=torch.float64, device=dev)
+        ws_bytes = lib.spamm_execute_workspace_bytes(nC)
+        ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
+        bufs = _lib.PlanBuffers(plan.c_keys.data_ptr(), plan.c_off.data_ptr(), plan.task_k.data_ptr(),
+                                plan.task_a.data_ptr(), plan.task_b.data_ptr(), plan.task_mask.data_ptr(),
+                                T, nC, None)
+        # with an accumulator to merge, the kernel leaves alpha to the compose step
+        alpha_k = 1.0 if keep_old else float(np.float32(cfg.alpha))
+        gran = _lib.FINE4 if fine else _lib.COARSE16
+        _lib.check(lib.spamm_execute(C.byref(va), C.byref(vb), C.byref(bufs), T, nC, alpha_k, gran, int(cfg.exact),
+                                     vals.data_ptr(), vals_t.data_ptr(), sub4.data_ptr(), leaf_sq.data_ptr(),
+                                     counters_dev.data_ptr(), ws.data_ptr(), ws_bytes, st), "execute")
+        prod = (plan.c_keys[:nC], vals, vals_t, sub4, leaf_sq)
+    # _compose (`numeric.py:268-284`)
+    if not keep_old:
+        if prod is None:
+            if cfg.beta == 0 or c.nleaf == 0:
+                c.clear()
+        else:
+            keys, vals, vals_t, sub4, leaf_sq = prod
+            c._adopt_packed(keys.clone(), vals, vals_t, sub4, leaf_sq, nC)
+    else:
+        _compose_with_accumulator(c, prod, cfg)
+    e1.record()
+    total = 64 * T if run else 0
+    if not run:
+        counters = ExecCounters(0, 0, 0.0, _events=(e0, e1))
+    elif fine:
+        counters = ExecCounters(_dev=counters_dev, _total=total, _fine=True, _events=(e0, e1))
+    else:
+        counters = ExecCounters(total, 0, 0.0, _events=(e0, e1))
+    return c, counters
+
+
+def _compose_with_accumulator(c: QuadtreeMatrix, prod, cfg: MultiplyConfig) -> None:
+    """beta != 0 and C has leaves: leaf-set union, alpha/beta combine, norms rebuilt."""
+    lib = _lib.lib()
+    st = _stream()
+    dev = c.device
+    depth, L = c.depth, 1 << c.depth
+    cells = L * L
+    g = c.grids()
+    if prod is None:
+        nprod, pk, pv = 0, None, None
+    else:
+        pk, pv = prod[0], prod[1]
+        nprod = int(pk.numel())
+    scratch = torch.empty((cells,), dtype=torch.int32, device=dev)
+    cap = min(cells, c.nleaf + nprod)
+    out_keys = torch.empty((cap,), dtype=torch.int32, device=dev)
+    idx_old = torch.empty((cap,), dtype=torch.int32, device=dev)
+    idx_prod = torch.empty((cap,), dtype=torch.int32, device=dev)
+    nout_dev = torch.empty((1,), dtype=torch.int32, device=dev)
+    ws_bytes = lib.spamm_scan_workspace_bytes(cells)
+    ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
+    _lib.check(lib.spamm_union_leaves(g.slot.data_ptr(), None if pk is None else pk.data_ptr(), nprod, depth,
+                                      scratch.data_ptr(), out_keys.data_ptr(), idx_old.data_ptr(), idx_prod.data_ptr(),
+                                      nout_dev.data_ptr(), ws.data_ptr(), ws_bytes, st), "union_leaves")
+    nout = int(nout_dev.item())
+    out_vals = torch.empty((nout, 256), dtype=torch.float32, device=dev)
+    _lib.check(lib.spamm_compose(None if pv is None else pv.data_ptr(), c.values.data_ptr(), idx_prod.data_ptr(),
+                                 idx_old.data_ptr(), nout, float(np.float32(cfg.alpha)), float(np.float32(cfg.beta)),
+                                 int(cfg.alpha == 1), int(cfg.beta == 1), out_vals.data_ptr(), st), "compose")
+    c._set_packed_values(out_keys[:nout].clone(), out_vals)
+
+
+def multiply(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig | None = None,
+             c: QuadtreeMatrix | None = None) -> tuple[QuadtreeMatrix, MultiplyPlan, ExecCounters]:
+    """Symbolic plus numeric phases in one call (`numeric.py:302-313`)."""
+    if cfg is None:
+        cfg = MultiplyConfig()
+    plan = build_plan(a, b, cfg.tau, cfg.granularity)
+    out, counters = execute_plan(plan, a, b, c, cfg)
+    return out, plan, counters

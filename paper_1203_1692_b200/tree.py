@@ -1,0 +1,335 @@
+"""Device-resident quadtree matrix: the operand type of the multiply.
+
+Mirrors the part of the reference's ``QuadtreeMatrix`` the multiply path touches
+(`pkg/src/spamm/core.py:146-405`): ``from_dense``, ``to_dense``, ``packed_leaves``,
+``put_leaf`` / ``clear`` / ``compute_norms``, ``norm``, ``leaf_count``, ``node``.  Element
+mutation, ``sparsify`` and ``drop_tolerance`` are outside the path.
+
+Layout in HBM (see ``include/spamm_b200.h``): stored 16x16 leaves packed in ascending
+Morton-key order -- row-major (``values``) and transposed (``values_t``, the staging layout of
+an A operand) -- their 4x4 sub-block norms, a leaf-slot grid and the norm pyramid, each also
+kept transposed so a B operand is read along k.  PyTorch only owns the memory.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import morton
+
+DEFAULT_BLOCK = 16
+
+
+def _validate_block_size(n_b) -> None:
+    if not isinstance(n_b, (int, np.integer)) or n_b < 1 or n_b & (n_b - 1):
+        raise ValueError(f"block size must be a positive power of two, got {n_b}")
+
+
+def tree_depth(m: int, n: int, n_b: int = DEFAULT_BLOCK) -> int:
+    """Smallest d with n_b * 2^d >= max(m, n) (`core.py:33-39`)."""
+    _validate_block_size(n_b)
+    if m < 1 or n < 1:
+        raise ValueError(f"matrix dimensions must be positive, got {m} x {n}")
+    q = -(-max(m, n) // n_b)
+    return (q - 1).bit_length()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class DenseMatrix:
+    """Host dense matrix as returned by ``to_dense`` (`core.py:54-105`, data only)."""
+
+    __slots__ = ("data",)
+
+    def __init__(self, data):
+        self.data = np.ascontiguousarray(data)
+
+    @property
+    def m(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def n(self) -> int:
+        return self.data.shape[1]
+
+
+@dataclass
+class TreeNode:
+    tier: int
+    index: int
+    norm: float
+
+
+class _Grids:
+    """Slot grids and norm pyramid of a tree indexed at one depth."""
+
+    __slots__ = ("depth", "slot", "slot_t", "norm", "norm_t")
+
+    def __init__(self, depth, slot, slot_t, norm, norm_t):
+        self.depth, self.slot, self.slot_t, self.norm, self.norm_t = depth, slot, slot_t, norm, norm_t
+
+
+class QuadtreeMatrix:
+    """Quadtree of 16x16 single-precision leaves with per-node Frobenius norms, in HBM."""
+
+    def __init__(self, m: int, n: int, n_b: int = DEFAULT_BLOCK, device=None):
+        _validate_block_size(n_b)
+        if m < 1 or n < 1:
+            raise ValueError(f"matrix dimensions must be positive, got {m} x {n}")
+        self.m, self.n, self.n_b = int(m), int(n), int(n_b)
+        self.depth = tree_depth(m, n, n_b)
+        self.padded = n_b << self.depth
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self._rev = 0
+        self._pending: dict[int, np.ndarray] = {}   # put_leaf staging (host) until compute_norms
+        self._set_empty()
+
+    # -- storage -------------------------------------------------------------------------------
+    def _set_empty(self) -> None:
+        self.nleaf = 0
+        self.keys = self.values = self.values_t = self.sub4 = None
+        self.leaf_sq = None          # double square sum per packed leaf
+        self._leaf_sq_grid = None    # the same on the leaf grid (from_dense keeps this form)
+        self._grids: dict[int, _Grids] = {}
+
+    def _require_16(self) -> None:
+        if self.n_b != 16:
+            raise ValueError(f"the B200 path stores 16x16 leaves (n_b = 16), got n_b = {self.n_b}")
+
+    def _alloc(self, shape, dtype):
+        return torch.empty(shape, dtype=dtype, device=self.device)
+
+    @property
+    def leaf_count(self) -> int:
+        return self.nleaf + len(self._pending)
+
+    @property
+    def norm(self) -> float:
+        if self.nleaf == 0:
+            return 0.0
+        v = float(self.grids().norm[0].item())
+        return v if v >= 0 else 0.0
+
+    # -- construction ----------------------------------------------------------------------------
+    @classmethod
+    def from_dense(cls, dense, n_b: int = DEFAULT_BLOCK, device=None) -> "QuadtreeMatrix":
+        """Build the tree from a dense matrix (numpy or torch, host or device), skipping
+        all-zero blocks (`core.py:213-250`): leaf pass, Z-order slot scan, leaf packing,
+        interior norms -- four kernels, one small read-back (the leaf count)."""
+        if isinstance(dense, DenseMatrix):
+            dense = dense.data
+        if isinstance(dense, np.ndarray):
+            if dense.ndim != 2 or dense.shape[0] < 1 or dense.shape[1] < 1:
+                raise ValueError(f"expected a nonempty 2-D matrix, got shape {dense.shape}")
+            if not np.isfinite(dense).all():
+                raise ValueError("matrix elements must be finite")
+            dense = torch.from_numpy(np.ascontiguousarray(dense, dtype=np.float32))
+        q = cls(dense.shape[0], dense.shape[1], n_b, device)
+        q._require_16()
+        d = dense.to(device=q.device, dtype=torch.float32, non_blocking=True).contiguous()
+        q._build_from_device_dense(d)
+        return q
+
+    def _build_from_device_dense(self, d: torch.Tensor) -> None:
+        lib = _lib.lib()
+        st = _stream()
+        depth, L = self.depth, 1 << self.depth
+        cells = L * L
+        sub4_grid = self._alloc((cells, 16), torch.float32)
+        leaf_sq_grid = self._alloc((cells,), torch.float64)
+        norm = self._alloc((_lib.level_total(depth),), torch.float32)
+        norm_t = self._alloc((_lib.level_total(depth),), torch.float32)
+        off = _lib.level_offset(depth)
+        leaf_norm = norm[off:off + cells]
+        _lib.check(lib.spamm_leaf_norms_dense(d.data_ptr(), self.m, self.n, d.stride(0), depth, sub4_grid.data_ptr(),
+                                              leaf_sq_grid.data_ptr(), leaf_norm.data_ptr(), st), "leaf_norms_dense")
+        slot = self._alloc((cells,), torch.int32)
+        slot_t = self._alloc((cells,), torch.int32)
+        keys = self._alloc((cells,), torch.int32)
+        nleaf_dev = self._alloc((1,), torch.int32)
+        ws_bytes = lib.spamm_scan_workspace_bytes(cells)
+        ws = self._alloc((ws_bytes,), torch.uint8)
+        _lib.check(lib.spamm_assign_slots(leaf_norm.data_ptr(), depth, slot.data_ptr(), slot_t.data_ptr(), keys.data_ptr(),
+                                          nleaf_dev.data_ptr(), ws.data_ptr(), ws_bytes, st), "assign_slots")
+        nleaf = int(nleaf_dev.item())
+        self.nleaf = nleaf
+        self.keys = keys[:nleaf].clone()
+        self.values = self._alloc((max(nleaf, 1), 256), torch.float32)
+        self.values_t = self._alloc((max(nleaf, 1), 256), torch.float32)
+        self.sub4 = self._alloc((max(nleaf, 1), 16), torch.float32)
+        _lib.check(lib.spamm_pack_leaves(d.data_ptr(), self.m, self.n, d.stride(0), depth, self.keys.data_ptr(), nleaf,
+                                         sub4_grid.data_ptr(), self.values.data_ptr(), self.values_t.data_ptr(),
+                                         self.sub4.data_ptr(), st), "pack_leaves")
+        sq_levels = self._alloc((_lib.level_total(depth),), torch.float64)
+        _lib.check(lib.spamm_build_interior(leaf_sq_grid.data_ptr(), depth, norm.data_ptr(), norm_t.data_ptr(),
+                                            sq_levels.data_ptr(), 1, st), "build_interior")
+        self._leaf_sq_grid = leaf_sq_grid
+        self.leaf_sq = None
+        self._grids = {depth: _Grids(depth, slot, slot_t, norm, norm_t)}
+        self._rev += 1
+
+    def _adopt_packed(self, keys: torch.Tensor, values: torch.Tensor, values_t: torch.Tensor, sub4: torch.Tensor,
+                      leaf_sq: torch.Tensor, nleaf: int) -> None:
+        """Take ownership of packed leaves whose norms are already known (a multiply result)."""
+        self._pending.clear()
+        self.nleaf = int(nleaf)
+        self.keys, self.values, self.values_t, self.sub4, self.leaf_sq = keys, values, values_t, sub4, leaf_sq
+        self._leaf_sq_grid = None
+        self._grids = {}
+        self._index(self.depth)
+        self._rev += 1
+
+    def _packed_leaf_sq(self) -> torch.Tensor:
+        if self.leaf_sq is None:
+            i, j = morton.decode_array(self.keys.cpu().numpy().astype(np.uint64))
+            idx = torch.from_numpy((i.astype(np.int64) << self.depth) + j.astype(np.int64)).to(self.device)
+            self.leaf_sq = self._leaf_sq_grid[idx].contiguous() if self.nleaf else self._alloc((1,), torch.float64)
+        return self.leaf_sq
+
+    def _index(self, depth: int) -> _Grids:
+        """Slot grids and norm pyramid at `depth` >= self.depth (`core.py:252-266`)."""
+        lib = _lib.lib()
+        st = _stream()
+        L = 1 << depth
+        cells = L * L
+        total = _lib.level_total(depth)
+        slot = self._alloc((cells,), torch.int32)
+        slot_t = self._alloc((cells,), torch.int32)
+        norm = self._alloc((total,), torch.float32)
+        norm_t = self._alloc((total,), torch.float32)
+        sq_grid = self._alloc((cells,), torch.float64)
+        sq_levels = self._alloc((total,), torch.float64)
+        leaf_sq = self._packed_leaf_sq()
+        keys_ptr = self.keys.data_ptr() if self.nleaf else None
+        _lib.check(lib.spamm_index_leaves(keys_ptr, leaf_sq.data_ptr() if self.nleaf else None, self.nleaf, depth,
+                                          slot.data_ptr(), slot_t.data_ptr(), norm.data_ptr(), norm_t.data_ptr(),
+                                          sq_grid.data_ptr(), st), "index_leaves")
+        _lib.check(lib.spamm_build_interior(sq_grid.data_ptr(), depth, norm.data_ptr(), norm_t.data_ptr(),
+                                            sq_levels.data_ptr(), 0, st), "build_interior")
+        g = _Grids(depth, slot, slot_t, norm, norm_t)
+        self._grids[depth] = g
+        return g
+
+    def grids(self, depth: int | None = None) -> _Grids:
+        depth = self.depth if depth is None else depth
+        if depth < self.depth:
+            raise ValueError("cannot index a tree above its own depth")
+        self._flush_guard()
+        g = self._grids.get(depth)
+        return g if g is not None else self._index(depth)
+
+    def view(self, depth: int | None = None) -> _lib.TreeView:
+        """ctypes view for the kernels, indexed at a (possibly larger) common depth."""
+        g = self.grids(depth)
+        nz = self.nleaf > 0
+        return _lib.TreeView(self.m, self.n, g.depth, self.nleaf,
+                             _ptr(self.keys) if nz else None, _ptr(self.values) if nz else None,
+                             _ptr(self.values_t) if nz else None, _ptr(self.sub4) if nz else None,
+                             g.slot.data_ptr(), g.slot_t.data_ptr(), g.norm.data_ptr(), g.norm_t.data_ptr())
+
+    def _flush_guard(self) -> None:
+        if self._pending:
+            raise ValueError("tree has staged leaves with stale norms; call compute_norms() first")
+
+    # -- reference-style accessors --------------------------------------------------------------
+    def to_dense_tensor(self) -> torch.Tensor:
+        self._flush_guard()
+        out = torch.empty((self.m, self.n), dtype=torch.float32, device=self.device)
+        if self.nleaf == 0:
+            return out.zero_()
+        v = self.view()
+        _lib.check(_lib.lib().spamm_to_dense(C.byref(v), out.data_ptr(), out.stride(0), _stream()), "to_dense")
+        return out
+
+    def to_dense(self) -> DenseMatrix:
+        return DenseMatrix(self.to_dense_tensor().cpu().numpy())
+
+    def packed_leaves(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        """(keys, values, subnorms) on the host, ascending key order (`core.py:387-405`)."""
+        self._flush_guard()
+        n = self.nleaf
+        if n == 0:
+            return (np.empty(0, np.uint64), np.empty((0, 16, 16), np.float32), np.empty((0, 4, 4), np.float32))
+        return (self.keys[:n].cpu().numpy().astype(np.uint64),
+                self.values[:n].cpu().numpy().reshape(n, 16, 16),
+                self.sub4[:n].cpu().numpy().reshape(n, 4, 4))
+
+    def leaf_keys(self) -> np.ndarray:
+        return self.packed_leaves()[0] if self.nleaf else np.empty(0, np.uint64)
+
+    def level_norms(self, tier: int) -> np.ndarray:
+        """Host copy of one tier's norm grid, -1 where no node is stored."""
+        g = self.grids()
+        s = 1 << tier
+        off = _lib.level_offset(tier)
+        return g.norm[off:off + s * s].cpu().numpy().reshape(s, s)
+
+    def node(self, tier: int, index: int) -> TreeNode | None:
+        if self.nleaf == 0 or not 0 <= tier <= self.depth:
+            return None
+        i, j = morton.decode(index)
+        s = 1 << tier
+        if i >= s or j >= s:
+            return None
+        v = float(self.level_norms(tier)[i, j])
+        return TreeNode(tier, index, v) if v >= 0 else None
+
+    # -- staged mutation: put_leaf ... compute_norms (`core.py:315-345`) --------------------------
+    def put_leaf(self, key: int, values: np.ndarray) -> None:
+        self._require_16()
+        values = np.asarray(values)
+        if values.shape != (self.n_b, self.n_b):
+            raise ValueError(f"leaf values must be {self.n_b} x {self.n_b}")
+        if key < 0 or key >> (2 * self.depth):
+            raise ValueError(f"leaf key {key} outside depth {self.depth}")
+        self._pending[int(key)] = np.ascontiguousarray(values, dtype=np.float32)
+        self._rev += 1
+
+    def clear(self) -> None:
+        self._pending.clear()
+        self._set_empty()
+        self._rev += 1
+
+    def compute_norms(self) -> None:
+        """Rebuild all norms bottom-up from leaf values (`core.py:331-345`)."""
+        self._require_16()
+        leaves: dict[int, np.ndarray] = {}
+        if self.nleaf:
+            keys = self.keys[: self.nleaf].cpu().numpy()
+            vals = self.values[: self.nleaf].cpu().numpy().reshape(-1, 16, 16)
+            leaves.update({int(k): v for k, v in zip(keys.tolist(), vals)})
+        leaves.update(self._pending)
+        self._pending.clear()
+        ks = sorted(leaves)
+        if not ks:
+            self._set_empty()
+            self._rev += 1
+            return
+        keys_t = torch.tensor(ks, dtype=torch.int32, device=self.device)
+        vals_t = torch.from_numpy(np.stack([leaves[k] for k in ks]).reshape(-1, 256)).to(self.device)
+        self._set_packed_values(keys_t, vals_t)
+
+    def _set_packed_values(self, keys: torch.Tensor, values: torch.Tensor) -> None:
+        """Leaves given by keys (ascending) and values; norms in compute_norms order."""
+        n = int(keys.numel())
+        values_t = self._alloc((n, 256), torch.float32)
+        sub4 = self._alloc((n, 16), torch.float32)
+        leaf_sq = self._alloc((n,), torch.float64)
+        _lib.check(_lib.lib().spamm_leaf_norms_packed(values.data_ptr(), n, values_t.data_ptr(), sub4.data_ptr(),
+                                                     leaf_sq.data_ptr(), _stream()), "leaf_norms_packed")
+        self._adopt_packed(keys, values, values_t, sub4, leaf_sq, n)
+
+    def __repr__(self) -> str:
+        return (f"QuadtreeMatrix({self.m}x{self.n}, n_b={self.n_b}, depth={self.depth}, "
+                f"leaves={self.leaf_count}, device={self.device})")

@@ -35,13 +35,17 @@ def golden() -> Golden:
     return _GOLDEN
 
 
-def tiers_blob(norm_levels: np.ndarray, depth: int) -> np.ndarray:
-    """Every tier's (sorted keys, norms) as bytes, as make_golden.tree_record does."""
+def tiers_blob(norm_levels, depth: int) -> np.ndarray:
+    """Every tier's (sorted keys, norms) as bytes, as make_golden.tree_record does.
+    `norm_levels` is the oracle's flat level buffer or a callable tier -> grid."""
     parts = []
     for t in range(depth + 1):
         s = 1 << t
-        off = O.level_offset(t)
-        g = norm_levels[off:off + s * s].reshape(s, s)
+        if callable(norm_levels):
+            g = norm_levels(t)
+        else:
+            off = O.level_offset(t)
+            g = norm_levels[off:off + s * s].reshape(s, s)
         ii, jj = np.nonzero(g >= 0)
         keys = O.encode(ii, jj)
         order = np.argsort(keys, kind="stable")
@@ -84,3 +88,23 @@ def check_oracle_tree(g: Golden, case: str, prefix: str, t: O.OracleTree):
     leaf_norm = t.leaf_norm[ii, jj][order]
     check_tree(g, case, prefix, t.keys, t.values, t.subnorms, leaf_norm,
                tiers_blob(t.norm_levels, t.depth), t.m, t.n, t.depth)
+
+
+def check_device_tree(g: Golden, case: str, prefix: str, q):
+    """Device QuadtreeMatrix against the reference's record (bit for bit)."""
+    keys, values, subs = q.packed_leaves()
+    from paper_1203_1692_b200 import morton
+    i, j = morton.decode_array(keys)
+    leaf_norm = q.level_norms(q.depth)[i.astype(np.int64), j.astype(np.int64)] if keys.size else np.zeros(0, np.float32)
+    check_tree(g, case, prefix, keys, values, subs, leaf_norm, tiers_blob(q.level_norms, q.depth), q.m, q.n, q.depth)
+
+
+def assert_trees_equal(q, t: O.OracleTree, what: str = ""):
+    """Device tree == oracle tree: leaves, sub-norms and every tier's norms, bit for bit."""
+    keys, values, subs = q.packed_leaves()
+    assert np.array_equal(keys, t.keys.astype(np.uint64)), f"{what}: leaf keys"
+    assert np.array_equal(values.view(np.uint32), t.values.view(np.uint32)), f"{what}: leaf values"
+    assert np.array_equal(subs.view(np.uint32), t.subnorms.view(np.uint32)), f"{what}: sub-norms"
+    assert (q.m, q.n, q.depth) == (t.m, t.n, t.depth)
+    for tier in range(t.depth + 1):
+        assert np.array_equal(q.level_norms(tier), t.level_norm(tier)), f"{what}: tier {tier} norms"
