@@ -191,6 +191,8 @@ class QuadtreeMatrix:
         self._rev += 1
 
     def _packed_leaf_sq(self) -> torch.Tensor:
+        if self.nleaf == 0:
+            return torch.zeros((1,), dtype=torch.float64, device=self.device)
         if self.leaf_sq is None:
             i, j = morton.decode_array(self.keys.cpu().numpy().astype(np.uint64))
             idx = torch.from_numpy((i.astype(np.int64) << self.depth) + j.astype(np.int64)).to(self.device)
