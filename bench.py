@@ -153,27 +153,22 @@ def kernel_time_execute(P, torch, plan, qa, qb, cfg, reps, flush):
     from paper_1203_1692_b200 import _lib
     lib = _lib.lib()
     dev = qa.device
-    T, nC = plan.n_tasks, plan.n_cleaves
+    nC = plan.n_cleaves
     va, vb = qa.view(plan.depth), qb.view(plan.depth)
-    vals = torch.empty((nC, 256), dtype=torch.float32, device=dev)
+    vals = torch.empty((nC, _lib.REC), dtype=torch.float32, device=dev)
     vals_t = torch.empty_like(vals)
-    sub4 = torch.empty((nC, 16), dtype=torch.float32, device=dev)
     leaf_sq = torch.empty((nC,), dtype=torch.float64, device=dev)
     cnt = torch.zeros((2,), dtype=torch.int64, device=dev)
-    ws_bytes = lib.spamm_execute_workspace_bytes(nC)
-    ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
-    bufs = _lib.PlanBuffers(plan.c_keys.data_ptr(), plan.c_off.data_ptr(), plan.task_k.data_ptr(), plan.task_a.data_ptr(),
-                            plan.task_b.data_ptr(), plan.task_mask.data_ptr(), T, nC, None)
+    bufs = plan.buffers()
     st = torch.cuda.current_stream().cuda_stream
     times = []
     for it in range(reps + 2):
         flush.fill_(it)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _lib.check(lib.spamm_execute(C.byref(va), C.byref(vb), C.byref(bufs), T, nC, 1.0,
+        _lib.check(lib.spamm_execute(C.byref(va), C.byref(vb), C.byref(bufs), plan.n_steps, nC, float(cfg.tau), 1.0,
                                      0 if cfg.granularity == "fine4" else 1, 0, vals.data_ptr(), vals_t.data_ptr(),
-                                     sub4.data_ptr(), leaf_sq.data_ptr(), cnt.data_ptr(), ws.data_ptr(), ws_bytes, st),
-                   "execute")
+                                     leaf_sq.data_ptr(), cnt.data_ptr(), st), "execute")
         e1.record()
         torch.cuda.synchronize()
         if it >= 2:
@@ -230,7 +225,7 @@ def run_own(args) -> None:
     k3_tflops = flops / (k3_ms * 1e-3) / 1e12
     # compulsory traffic of the kernel: every stored A leaf (transposed copy) and B leaf once, C leaves
     # written in both layouts, task records
-    alg_bytes = 1024 * (qa.nleaf + qb.nleaf + 2 * plan.n_cleaves) + 20 * len(plan)
+    alg_bytes = 1088 * (qa.nleaf + qb.nleaf + 2 * plan.n_cleaves) + 64 * plan.n_steps
 
     # ---- end to end through the public API with host buffers
     host_a = torch.from_numpy(a_d).pin_memory()

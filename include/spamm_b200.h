@@ -45,9 +45,10 @@ enum { SPAMM_EXEC_FMA = 0, SPAMM_EXEC_EXACT = 1 };   /* EXACT: separate mul/add 
 /* Device view of one QuadtreeMatrix (core.py:146-167, :387-405).  All pointers
  * are device pointers owned by the caller.
  *   keys      [nleaf]       Morton key of each stored leaf, ascending (packed_leaves()[0])
- *   values    [nleaf][256]  row-major 16x16 leaf values          (packed_leaves()[1])
- *   values_t  [nleaf][256]  the same leaves transposed (the A-operand staging layout)
- *   sub4      [nleaf][16]   4x4 sub-block norms, p*4+q           (packed_leaves()[2])
+ *   values    [nleaf][272]  row-major 16x16 leaf values (packed_leaves()[1]) followed by the
+ *                           16 sub-block norms transposed, tail[q*4+r] = sub[r][q]
+ *   values_t  [nleaf][272]  the leaf transposed (the A-operand staging layout) followed by
+ *                           the sub-block norms row-major, tail[p*4+r]  (packed_leaves()[2])
  *   slot      [L*L]         leaf (i,j) -> index into the packed arrays, -1 = absent
  *   slot_t    [L*L]         transposed grid: (j,i) -> index
  *   norm      level buffer  node norms, -1 = absent node        (TreeNode.norm, core.py:138-143)
@@ -60,7 +61,6 @@ typedef struct {
     const uint32_t *keys;
     const float *values;
     const float *values_t;
-    const float *sub4;
     const int32_t *slot;
     const int32_t *slot_t;
     const float *norm;
@@ -88,11 +88,11 @@ size_t spamm_scan_workspace_bytes(int64_t n);
 int spamm_assign_slots(const float *leaf_norm, int depth, int32_t *slot, int32_t *slot_t,
                        uint32_t *keys, int32_t *nleaf_dev, void *ws, size_t ws_bytes, void *stream);
 
-/* Copy the stored leaves out of the dense matrix (core.py:239-248): values, values_t, sub4.
+/* Copy the stored leaves out of the dense matrix (core.py:239-248): values, values_t records.
  * nleaf is the host copy of *nleaf_dev. */
 int spamm_pack_leaves(const float *dense, int64_t m, int64_t n, int64_t ld, int depth,
                       const uint32_t *keys, int64_t nleaf, const float *sub4_grid,
-                      float *values, float *values_t, float *sub4, void *stream);
+                      float *values, float *values_t, void *stream);
 
 /* Interior norms (_build_interior, core.py:252-266): fills levels 0..depth-1 of norm / norm_t
  * and sq_levels from the leaf level.  leaf_sq is the L*L grid of double square sums; the leaf
@@ -103,10 +103,10 @@ int spamm_build_interior(const double *leaf_sq, int depth, float *norm, float *n
 
 /* ---- trees given as packed leaves: put_leaf + compute_norms (core.py:315-345) */
 
-/* Leaf norms of packed leaves, in the order compute_norms uses (core.py:108-116):
- * sub4 [nleaf][16], leaf_sq [nleaf], and optionally the transposed copy values_t. */
-int spamm_leaf_norms_packed(const float *values, int64_t nleaf, float *values_t,
-                            float *sub4, double *leaf_sq, void *stream);
+/* Leaf norms of packed leaves, in the order compute_norms uses (core.py:108-116): fills the
+ * sub-norm tails of the `values` records, the whole `values_t` records and leaf_sq [nleaf]. */
+int spamm_leaf_norms_packed(float *values, int64_t nleaf, float *values_t, double *leaf_sq,
+                            void *stream);
 
 /* Scatter packed leaves (keys ascending, leaf_sq) into the grids of a depth-`depth` tree:
  * slot, slot_t, the leaf level of norm/norm_t and the double leaf_sq grid (all L*L). */
@@ -119,50 +119,66 @@ int spamm_to_dense(const spamm_tree_view *t, float *out, int64_t ld, void *strea
 
 /* ---- symbolic phase: build_plan (symbolic.py:92-159) --------------------------- */
 
-/* Device plan: product leaves in ascending Morton order with their tasks in
- * ascending k (the only order the numeric phase depends on, numeric.py:203-217).
- *   c_keys [nC], c_off [nC+1]    product leaf keys and CSR offsets into the task arrays
- *   task_k / task_a / task_b [T] contraction index, packed slot of the A and B leaf
- *   task_mask [T]                fine4 live bits, bit r*16 + p*4 + q (numeric.py:232-238);
- *                                all ones for coarse16
- *   counts [4]                   nC, T, overflow flag, largest intermediate list
- */
+/* The compacted task list.  Product leaves are grouped in super-tiles of 4x4 leaves (16
+ * consecutive Morton keys); for every super-tile (I,J) and, in ascending order, every k that
+ * has at least one surviving task, the plan holds one 64-byte step record.  Bit
+ * pos = morton4(di,dj) of `live` stands for the task (i,k,j) = (4I+di, k, 4J+dj); tasks of one
+ * product leaf therefore appear in ascending k, the only order the numeric phase depends on
+ * (numeric.py:203-217).  The records of a super-tile are contiguous, super-tiles ascend in
+ * Morton order. */
+#define SPAMM_STEP_LIVE 0xFFFFu
+#define STEP_FIRST (1u << 16)   /* first record of its super-tile */
+#define STEP_LAST (1u << 17)    /* last record of its super-tile  */
 typedef struct {
-    uint32_t *c_keys;
-    int32_t *c_off;
-    uint32_t *task_k;
-    uint32_t *task_a;
-    uint32_t *task_b;
-    uint64_t *task_mask;
-    int64_t task_capacity;
+    uint32_t k;            /* contraction leaf index                                       */
+    uint32_t live_flags;   /* bits 0-15 live tasks, STEP_FIRST, STEP_LAST                  */
+    uint32_t c_base;       /* packed index of the super-tile's first product leaf          */
+    uint32_t tile;         /* Morton index of the super-tile (product leaf key >> 4)       */
+    uint32_t a_slot[4];    /* packed slot of leaf A(4I+di, k), valid where a task needs it */
+    uint32_t b_slot[4];    /* packed slot of leaf B(k, 4J+dj)                              */
+    uint32_t present;      /* product leaves of the super-tile (same bit numbering)        */
+    uint32_t pad[3];
+} spamm_step;
+
+/* counts[]: [0] product leaves nC, [1] scratch (the numeric kernel's tile counter),
+ * [2] overflow flag, [3] largest intermediate list, [4] step records, [5] super-tile nodes,
+ * [6..7] tasks T as one uint64 */
+#define SPAMM_PLAN_COUNTS 8
+typedef struct {
+    spamm_step *steps;       /* [step_capacity]                                   */
+    uint32_t *c_keys;        /* [leaf_capacity] product leaf keys, ascending      */
+    int32_t *tile_off;       /* [leaf_capacity + 1] first step of each super-tile node */
+    int64_t step_capacity;
     int64_t leaf_capacity;
-    int32_t *counts;
+    int32_t *counts;         /* [SPAMM_PLAN_COUNTS]                               */
 } spamm_plan_buffers;
 
-size_t spamm_plan_workspace_bytes(int depth, int64_t task_capacity, int64_t leaf_capacity);
+size_t spamm_plan_workspace_bytes(int depth, int64_t step_capacity, int64_t leaf_capacity);
 
 /* Task set { (i,k,j) : both leaves stored, double(normA) * double(normB) >= tau }
- * (symbolic.py:118-125), produced by a top-down walk of the two norm pyramids.
- * `depth` is the common depth of both views (the caller re-indexes a shallower tree);
- * rows/cols limit the product to [row0,row1) x all columns of leaves (multi-GPU row blocks). */
-int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
+ * (symbolic.py:118-125), produced by a top-down walk of the two norm pyramids.  Both views
+ * must be indexed at the same depth (the caller re-indexes a shallower tree); [row0,row1)
+ * limits the product to those rows of leaves (row blocks of the multi-GPU split).  When
+ * counts[2] is set a capacity was too small and the buffers are incomplete. */
+int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, double tau,
                int32_t row0, int32_t row1, const spamm_plan_buffers *out,
                void *ws, size_t ws_bytes, void *stream);
 
 /* ---- numeric phase: execute_plan (numeric.py:138-284) ------------------------- */
 
-size_t spamm_execute_workspace_bytes(int64_t nC);
-
 /* Runs every task of the plan: C leaf = alpha32 * sum_k gate(A_ik B_kj), accumulated in
- * ascending k with FP32 FMA (or separately rounded multiply/add when exact != 0).
- * Outputs for product leaf x (plan order): c_values[x], c_values_t[x], and its norms in
- * compute_norms order: c_sub4[x], c_leaf_sq[x].  counters[0..1] += products4, skipped4.
- * nC and T are the host copies of counts[0..1]. */
+ * ascending k in FP32 -- fused multiply-add, or separately rounded multiply and add when
+ * exact != 0 (bit-identical to numeric.py:252-259).  With SPAMM_FINE4 each 4x4x4 micro product
+ * (p,q,r) runs iff double(subA[p][r]) * double(subB[r][q]) >= tau (numeric.py:232-238), with
+ * SPAMM_COARSE16 all 64 run.  Outputs for product leaf x (plan order): the 272-float records
+ * c_values[x] / c_values_t[x] (values + sub-norms, see spamm_tree_view) and c_leaf_sq[x], the
+ * norms in compute_norms order (core.py:108-116).  counters[0] += executed micro products.
+ * nsteps and nC are the host copies of counts[4] and counts[0]. */
 int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b,
-                  const spamm_plan_buffers *plan, int64_t T, int64_t nC,
-                  float alpha, int granularity, int exact,
-                  float *c_values, float *c_values_t, float *c_sub4, double *c_leaf_sq,
-                  unsigned long long *counters, void *ws, size_t ws_bytes, void *stream);
+                  const spamm_plan_buffers *plan, int64_t nsteps, int64_t nC,
+                  double tau, float alpha, int granularity, int exact,
+                  float *c_values, float *c_values_t, double *c_leaf_sq,
+                  unsigned long long *counters, void *stream);
 
 /* Leaf set of C for beta != 0: the union of the accumulator's stored leaves (slot_old, an L*L
  * grid) and the produced leaves (prod_keys, ascending), in ascending Morton order.  For output

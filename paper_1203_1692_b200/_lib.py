@@ -23,15 +23,20 @@ class TreeView(C.Structure):
     """``spamm_tree_view``."""
 
     _fields_ = [("m", i32), ("n", i32), ("depth", i32), ("nleaf", i32),
-                ("keys", vp), ("values", vp), ("values_t", vp), ("sub4", vp),
+                ("keys", vp), ("values", vp), ("values_t", vp),
                 ("slot", vp), ("slot_t", vp), ("norm", vp), ("norm_t", vp)]
 
 
 class PlanBuffers(C.Structure):
     """``spamm_plan_buffers``."""
 
-    _fields_ = [("c_keys", vp), ("c_off", vp), ("task_k", vp), ("task_a", vp), ("task_b", vp),
-                ("task_mask", vp), ("task_capacity", i64), ("leaf_capacity", i64), ("counts", vp)]
+    _fields_ = [("steps", vp), ("c_keys", vp), ("tile_off", vp), ("step_capacity", i64), ("leaf_capacity", i64),
+                ("counts", vp)]
+
+
+REC = 272           # floats per stored leaf record: 256 values + 16 sub-block norms
+STEP_WORDS = 16     # uint32 words per step record (struct spamm_step)
+PLAN_COUNTS = 8
 
 
 # every symbol include/spamm_b200.h declares: (restype, argtypes)
@@ -43,17 +48,16 @@ SIGNATURES = {
     "spamm_leaf_norms_dense": (C.c_int, [vp, i64, i64, i64, C.c_int, vp, vp, vp, vp]),
     "spamm_scan_workspace_bytes": (sz, [i64]),
     "spamm_assign_slots": (C.c_int, [vp, C.c_int, vp, vp, vp, vp, vp, sz, vp]),
-    "spamm_pack_leaves": (C.c_int, [vp, i64, i64, i64, C.c_int, vp, i64, vp, vp, vp, vp, vp]),
+    "spamm_pack_leaves": (C.c_int, [vp, i64, i64, i64, C.c_int, vp, i64, vp, vp, vp, vp]),
     "spamm_build_interior": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int, vp]),
-    "spamm_leaf_norms_packed": (C.c_int, [vp, i64, vp, vp, vp, vp]),
+    "spamm_leaf_norms_packed": (C.c_int, [vp, i64, vp, vp, vp]),
     "spamm_index_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp]),
     "spamm_to_dense": (C.c_int, [C.POINTER(TreeView), vp, i64, vp]),
     "spamm_plan_workspace_bytes": (sz, [C.c_int, i64, i64]),
-    "spamm_plan": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, C.c_int, i32, i32,
+    "spamm_plan": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, i32, i32,
                              C.POINTER(PlanBuffers), vp, sz, vp]),
-    "spamm_execute_workspace_bytes": (sz, [i64]),
     "spamm_execute": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), C.POINTER(PlanBuffers), i64, i64,
-                                f32, C.c_int, C.c_int, vp, vp, vp, vp, vp, vp, sz, vp]),
+                                f64, f32, C.c_int, C.c_int, vp, vp, vp, vp, vp]),
     "spamm_union_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp, sz, vp]),
     "spamm_compose": (C.c_int, [vp, vp, vp, vp, i64, f32, f32, C.c_int, C.c_int, vp, vp]),
 }

@@ -8,6 +8,8 @@
 
 #define SPAMM_NB 16
 #define SPAMM_LEAF 256
+#define SPAMM_REC 272              // floats per stored leaf: 256 values + 16 sub-block norms
+#define SPAMM_REC_BYTES 1088
 #define SPAMM_NUM_SMS 148
 
 // ---- launch bookkeeping -----------------------------------------------------

@@ -2,19 +2,25 @@
 //
 // Replaces symbolic.build_plan / convolve (pkg/src/spamm/symbolic.py:92-159).  The task set is
 //   { (i,k,j) : leaves A_ik and B_kj stored,  double(|A_ik|) * double(|B_kj|) >= tau }
-// (symbolic.py:118-125).  Because every parent norm bounds its children's (norms are the
-// correctly rounded square roots of FP64 sums of non-negative terms, core.py:252-266), a
-// node product below tau can be dropped at any level without losing a leaf task -- the same
-// argument that makes reference.recursive_spamm (reference.py:72-129) equal to the flat plan.
+// (symbolic.py:118-125).  Because every parent norm bounds its children's (norms are correctly
+// rounded square roots of FP64 sums of non-negative terms, core.py:252-266), a node product below
+// tau can be dropped at any level without losing a leaf task -- the argument that makes
+// reference.recursive_spamm (reference.py:72-129) equal to the flat plan.
 //
-// Layout of one level: the product nodes (i,j) that still have candidates, in ascending
-// Morton order, each with its ascending list of contraction indices k (CSR).  Going one level
-// down, node (i,j) with list {k} yields children (2i+di, 2j+dj) with candidates {2k, 2k+1};
-// order is preserved by construction, so the leaf level comes out sorted by product leaf
-// (Morton) and ascending k -- the accumulation order the numeric phase needs
-// (numeric.py:203-217) -- without any sort.  Survivors are counted with warp ballots and
-// placed with a decoupled look-back prefix sum; nothing returns to the host between levels.
+// One level is the list of product nodes (i,j) that still have candidates, in ascending Morton
+// order, each with its ascending list of contraction indices k (CSR).  Going one level down,
+// node (i,j) with list {k} yields children (2i+di, 2j+dj) with candidates {2k, 2k+1}; order is
+// preserved by construction.  Survivors are counted with warp ballots and placed with a
+// decoupled look-back prefix sum; nothing returns to the host between levels.
+//
+// The walk stops two levels above the leaves: a node there is a 4x4 super-tile of product
+// leaves, the unit of work of the numeric kernel.  The last kernel tests the leaf norms of every
+// candidate k directly and emits, per super-tile and in ascending k, one 64-byte STEP record
+//   (k, 16 live bits = the tasks (4I+di, k, 4J+dj) that survive, the A and B leaf slots)
+// so the compacted task list comes out already in the order and grouping the numeric phase
+// consumes: ascending k per product leaf (numeric.py:203-217), leaves in Morton order.
 #include "common.cuh"
+#include "plan_format.cuh"
 
 #define PLAN_WARPS 8
 #define PLAN_THREADS (PLAN_WARPS * 32)
@@ -27,62 +33,19 @@ struct LevelBuf {
 };
 
 struct PlanShared {      // lives at the start of the workspace, zeroed once per plan
-    unsigned int tile_counter[PLAN_MAX_LEVELS];
+    unsigned int tile_counter[PLAN_MAX_LEVELS + 1];
     int32_t counts[PLAN_MAX_LEVELS + 1][2];   // (nodes, candidates) per level
 };
 
-struct LeafOut {
-    const int32_t *slot_a;     // A grid, row-major (i,k)
-    const int32_t *slot_bt;    // B grid transposed (j,k)
-    const float *sub_a;
-    const float *sub_b;
-    uint32_t *task_a, *task_b;
-    uint64_t *task_mask;
-    int L;
-};
-
-// fine4 gate of one task (numeric.py:232-238): bit r*16 + p*4 + q.
-__device__ __forceinline__ uint64_t fine_mask(const float *__restrict__ sa, const float *__restrict__ sb, double tau)
-{
-    float a[16], b[16];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-        float4 va = __ldg(reinterpret_cast<const float4 *>(sa) + x);
-        float4 vb = __ldg(reinterpret_cast<const float4 *>(sb) + x);
-        a[4 * x] = va.x; a[4 * x + 1] = va.y; a[4 * x + 2] = va.z; a[4 * x + 3] = va.w;
-        b[4 * x] = vb.x; b[4 * x + 1] = vb.y; b[4 * x + 2] = vb.z; b[4 * x + 3] = vb.w;
-    }
-    uint64_t m = 0;
-#pragma unroll
-    for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int p = 0; p < 4; ++p)
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (__dmul_rn((double)a[p * 4 + r], (double)b[r * 4 + q]) >= tau) m |= 1ull << (r * 16 + p * 4 + q);
-    return m;
-}
-
-template <bool FINE>
-__device__ __forceinline__ void emit_leaf_task(const LeafOut &lo, int64_t pos, uint32_t i, uint32_t k, uint32_t j,
-                                               double tau)
-{
-    const int32_t sa = lo.slot_a[(int64_t)i * lo.L + k];
-    const int32_t sb = lo.slot_bt[(int64_t)j * lo.L + k];
-    lo.task_a[pos] = (uint32_t)sa;
-    lo.task_b[pos] = (uint32_t)sb;
-    lo.task_mask[pos] = FINE ? fine_mask(lo.sub_a + (int64_t)sa * 16, lo.sub_b + (int64_t)sb * 16, tau) : ~0ull;
-}
-
 // ---- start level: dense enumeration by one block ---------------------------------------
 // side = 2^level <= 16, so at most 256 product nodes with at most 16 candidates each.
-template <bool LEAF, bool FINE>
 __global__ void __launch_bounds__(256) plan_root_kernel(const float *__restrict__ norm_a, const float *__restrict__ norm_bt,
                                                         int level, int shift, int row0, int row1, double tau, LevelBuf out,
                                                         int32_t *counts_out, int64_t cap_nodes, int64_t cap_tasks,
-                                                        int32_t *overflow, LeafOut lo)
+                                                        int32_t *overflow)
 {
     __shared__ uint32_t s_cnt[256], s_act[256];
+    __shared__ uint32_t s_wc[8], s_wa[8];
     const int S = 1 << level;
     const int c = threadIdx.x;
     uint32_t i = 0, j = 0, live = 0;
@@ -93,23 +56,30 @@ __global__ void __launch_bounds__(256) plan_root_kernel(const float *__restrict_
             for (int k = 0; k < S; ++k)
                 if (norm_test(norm_a[i * S + k], norm_bt[j * S + k], tau)) live |= 1u << k;
     }
-    const uint32_t cnt = __popc(live);
-    s_cnt[c] = cnt;
-    s_act[c] = cnt > 0;
-    __syncthreads();
-    if (c == 0) {   // tiny serial exclusive scan
-        uint32_t rc = 0, ra = 0;
-        for (int x = 0; x < 256; ++x) {
-            uint32_t tc = s_cnt[x], ta = s_act[x];
-            s_cnt[x] = rc; s_act[x] = ra;
-            rc += tc; ra += ta;
-        }
-        counts_out[0] = (int32_t)ra;
-        counts_out[1] = (int32_t)rc;
-        if ((int64_t)ra > cap_nodes || (int64_t)rc > cap_tasks) *overflow = 1;
-        else out.off[ra] = (int32_t)rc;
+    const uint32_t cnt = __popc(live), act = cnt > 0;
+    // block exclusive scan of (cnt, act): warp shuffles + 8 warp totals
+    uint32_t ic = cnt, ia = act;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t vc = __shfl_up_sync(FULL_MASK, ic, d), va = __shfl_up_sync(FULL_MASK, ia, d);
+        if (lane_id() >= (uint32_t)d) { ic += vc; ia += va; }
     }
+    if (lane_id() == 31) { s_wc[c >> 5] = ic; s_wa[c >> 5] = ia; }
     __syncthreads();
+    uint32_t bc = 0, ba = 0, tc = 0, ta = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+        if (w < (c >> 5)) { bc += s_wc[w]; ba += s_wa[w]; }
+        tc += s_wc[w]; ta += s_wa[w];
+    }
+    s_cnt[c] = bc + ic - cnt;
+    s_act[c] = ba + ia - act;
+    if (c == 0) {
+        counts_out[0] = (int32_t)ta;
+        counts_out[1] = (int32_t)tc;
+        if ((int64_t)ta > cap_nodes || (int64_t)tc > cap_tasks) *overflow = 1;
+        else out.off[ta] = (int32_t)tc;
+    }
     if (cnt == 0) return;
     const uint32_t an = s_act[c];
     uint32_t kb = s_cnt[c];
@@ -117,11 +87,7 @@ __global__ void __launch_bounds__(256) plan_root_kernel(const float *__restrict_
     out.node[an] = (uint32_t)c;
     out.off[an] = (int32_t)kb;
     for (int k = 0; k < S; ++k)
-        if (live >> k & 1) {
-            out.ks[kb] = (uint32_t)k;
-            if (LEAF) emit_leaf_task<FINE>(lo, kb, i, (uint32_t)k, j, tau);
-            ++kb;
-        }
+        if (live >> k & 1) out.ks[kb++] = (uint32_t)k;
 }
 
 // ---- one level down ------------------------------------------------------------------------
@@ -140,7 +106,6 @@ struct ExpandArgs {
     int32_t *max_list;
     unsigned int *tile_counter;
     volatile unsigned long long *tile_state;
-    LeafOut lo;
 };
 
 // pass bits of one parent candidate k: bit (c*2 + dk), c = di*2 + dj
@@ -162,7 +127,6 @@ __device__ __forceinline__ uint32_t child_tests(const ExpandArgs &a, uint32_t pi
     return bits & rowmask;
 }
 
-template <bool LEAF, bool FINE>
 __global__ void __launch_bounds__(PLAN_THREADS) plan_expand_kernel(ExpandArgs a)
 {
     __shared__ int s_tile;
@@ -187,7 +151,6 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_expand_kernel(ExpandArgs a)
             morton_decode(pm, pi, pj);
             s = a.in.off[pidx];
             e = a.in.off[pidx + 1];
-            // children rows 2pi, 2pi+1 against the kept leaf-row range
             const bool r0 = ((int)((2 * pi + 1) << a.shift) > a.row0) && ((int)((2 * pi) << a.shift) < a.row1);
             const bool r1 = ((int)((2 * pi + 2) << a.shift) > a.row0) && ((int)((2 * pi + 1) << a.shift) < a.row1);
             rowmask = (r0 ? 0x0Fu : 0u) | (r1 ? 0xF0u : 0u);
@@ -233,7 +196,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_expand_kernel(ExpandArgs a)
         // phase 3: place nodes and candidates in order
         int64_t kb = (int64_t)s_base_lo + s_wtasks[warp];
         int64_t nb = (int64_t)s_base_hi + s_wact[warp];
-        if (nb + wact > a.cap_nodes || kb + wtasks > a.cap_tasks) {   // flagged by the last tile too
+        if (nb + wact > a.cap_nodes || kb + wtasks > a.cap_tasks) {
             if (lane == 0) *a.overflow = 1;
             continue;
         }
@@ -264,20 +227,167 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_expand_kernel(ExpandArgs a)
                 const uint32_t b0 = __ballot_sync(FULL_MASK, p0), b1 = __ballot_sync(FULL_MASK, p1);
                 if ((b0 | b1) == 0) continue;
                 int64_t pos = base[c] + __popc(b0 & lt) + __popc(b1 & lt);
-                const uint32_t ci = 2 * pi + (c >> 1), cj = 2 * pj + (c & 1);
-                if (p0) {
-                    a.out.ks[pos] = 2 * k;
-                    if (LEAF) emit_leaf_task<FINE>(a.lo, pos, ci, 2 * k, cj, a.tau);
-                    ++pos;
-                }
-                if (p1) {
-                    a.out.ks[pos] = 2 * k + 1;
-                    if (LEAF) emit_leaf_task<FINE>(a.lo, pos, ci, 2 * k + 1, cj, a.tau);
-                }
+                if (p0) a.out.ks[pos++] = 2 * k;
+                if (p1) a.out.ks[pos] = 2 * k + 1;
                 base[c] += __popc(b0) + __popc(b1);
             }
         }
     }
+}
+
+// ---- last stage: super-tile nodes -> step records --------------------------------------------
+struct TileArgs {
+    const float *norm_a;      // leaf level grid of A, row-major (i,k)
+    const float *norm_bt;     // leaf level grid of B transposed (j,k)
+    const int32_t *slot_a;    // leaf slots of A (i,k)
+    const int32_t *slot_bt;   // leaf slots of B transposed (j,k)
+    int L;                    // leaf grid side
+    int sub;                  // leaves per super-tile side: 4 (2 or 1 for depth 1 or 0)
+    int row0, row1;
+    double tau;
+    LevelBuf in;
+    const int32_t *counts_in;
+    spamm_step *steps;
+    uint32_t *c_keys;
+    int32_t *tile_off;
+    int64_t cap_steps, cap_leaves;
+    int32_t *counts;          // plan counts: [0] nC, [1] T, [2] overflow, [3] max list, [4] steps
+    unsigned int *tile_counter;
+    volatile unsigned long long *tile_state;
+};
+
+// live bits of candidate k of super-tile (I,J): bit pos(di,dj) for every surviving leaf task
+__device__ __forceinline__ uint32_t tile_tests(const TileArgs &a, uint32_t I, uint32_t J, uint32_t k, uint32_t rowok)
+{
+    float na[4], nb[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+        na[d] = -1.0f;
+        nb[d] = -1.0f;
+        if (d < a.sub) {
+            if (rowok >> d & 1u) na[d] = __ldg(a.norm_a + (int64_t)(a.sub * I + d) * a.L + k);
+            nb[d] = __ldg(a.norm_bt + (int64_t)(a.sub * J + d) * a.L + k);
+        }
+    }
+    uint32_t live = 0;
+#pragma unroll
+    for (int di = 0; di < 4; ++di)
+#pragma unroll
+        for (int dj = 0; dj < 4; ++dj)
+            if (norm_test(na[di], nb[dj], a.tau)) live |= 1u << step_pos(di, dj);
+    return live;
+}
+
+__global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
+{
+    __shared__ int s_tile;
+    __shared__ uint32_t s_wsteps[PLAN_WARPS], s_wleaves[PLAN_WARPS];
+    __shared__ uint32_t s_base_lo, s_base_hi;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = lane_id();
+    const int n_nodes = a.counts_in[0];
+    const int ntiles = (n_nodes + PLAN_WARPS - 1) / PLAN_WARPS;
+    const int sub = a.sub, per = 32 / sub;       // candidates per parent entry, parent entries per warp pass
+    unsigned long long tasks_total = 0;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_counter, 1u);
+        __syncthreads();
+        const int tile = s_tile;
+        if (tile >= ntiles) break;
+        const int pidx = tile * PLAN_WARPS + warp;
+        const bool valid = pidx < n_nodes;
+        uint32_t pm = 0, I = 0, J = 0, rowok = 0;
+        int s = 0, e = 0;
+        if (valid) {
+            pm = a.in.node[pidx];
+            morton_decode(pm, I, J);
+            s = a.in.off[pidx];
+            e = a.in.off[pidx + 1];
+            for (int d = 0; d < sub; ++d) {
+                const int row = (int)(sub * I + d);
+                if (row >= a.row0 && row < a.row1) rowok |= 1u << d;
+            }
+        }
+        // phase 1: count steps and product leaves of this super-tile
+        uint32_t nsteps = 0, present = 0, ntasks = 0;
+        for (int b = s; b < e; b += per) {
+            const int t = b + (int)lane / sub;
+            uint32_t live = 0;
+            if (t < e) live = tile_tests(a, I, J, sub * a.in.ks[t] + (lane % sub), rowok);
+            nsteps += __popc(__ballot_sync(FULL_MASK, live != 0));
+            present |= live;
+            ntasks += __popc(live);
+        }
+        present = __reduce_or_sync(FULL_MASK, present);
+        ntasks = __reduce_add_sync(FULL_MASK, ntasks);
+        const uint32_t nleaves = __popc(present);
+        if (lane == 0) { s_wsteps[warp] = nsteps; s_wleaves[warp] = nleaves; tasks_total += ntasks; }
+        __syncthreads();
+        // phase 2: block scan + look-back over (steps, product leaves)
+        if (threadIdx.x == 0) {
+            uint32_t rs = 0, rl = 0;
+            for (int w = 0; w < PLAN_WARPS; ++w) {
+                uint32_t vs = s_wsteps[w], vl = s_wleaves[w];
+                s_wsteps[w] = rs; s_wleaves[w] = rl;
+                rs += vs; rl += vl;
+            }
+            uint32_t ex_lo, ex_hi;
+            lb_exclusive(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
+            s_base_lo = ex_lo;
+            s_base_hi = ex_hi;
+            if (tile == ntiles - 1) {
+                const int64_t tot_s = (int64_t)ex_lo + rs, tot_l = (int64_t)ex_hi + rl;
+                a.counts[0] = (int32_t)tot_l;
+                a.counts[4] = (int32_t)tot_s;
+                a.counts[5] = n_nodes;
+                a.tile_off[n_nodes] = (int32_t)tot_s;
+                if (tot_s > a.cap_steps || tot_l > a.cap_leaves) a.counts[2] = 1;
+            }
+        }
+        __syncthreads();
+        if (valid && lane == 0) a.tile_off[pidx] = (int32_t)(s_base_lo + s_wsteps[warp]);
+        if (!valid || nsteps == 0) continue;
+        // phase 3: product leaf keys and step records, in ascending k
+        int64_t sb = (int64_t)s_base_lo + s_wsteps[warp];
+        const int64_t cb = (int64_t)s_base_hi + s_wleaves[warp];
+        if (sb + nsteps > a.cap_steps || cb + nleaves > a.cap_leaves) {
+            if (lane == 0) a.counts[2] = 1;
+            continue;
+        }
+        if (lane < 16 && (present >> lane & 1u))
+            a.c_keys[cb + __popc(present & ((1u << lane) - 1u))] = pm * (uint32_t)(sub * sub) + lane;
+        const int64_t s_first = sb, s_last = sb + nsteps - 1;
+        const uint32_t lt = lanemask_lt();
+        for (int b = s; b < e; b += per) {
+            const int t = b + (int)lane / sub;
+            uint32_t live = 0, k = 0;
+            if (t < e) {
+                k = sub * a.in.ks[t] + (lane % sub);
+                live = tile_tests(a, I, J, k, rowok);
+            }
+            const uint32_t bal = __ballot_sync(FULL_MASK, live != 0);
+            if (live) {
+                const int64_t x = sb + __popc(bal & lt);
+                uint32_t flags = live;
+                if (x == s_first) flags |= STEP_FIRST;
+                if (x == s_last) flags |= STEP_LAST;
+                uint32_t sa[4], sbb[4];
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    sa[d] = (live & step_rowmask(d)) ? (uint32_t)__ldg(a.slot_a + (int64_t)(sub * I + d) * a.L + k) : 0u;
+                    sbb[d] = (live & step_colmask(d)) ? (uint32_t)__ldg(a.slot_bt + (int64_t)(sub * J + d) * a.L + k) : 0u;
+                }
+                uint4 *rec = reinterpret_cast<uint4 *>(a.steps + x);
+                rec[0] = make_uint4(k, flags, (uint32_t)cb, pm);
+                rec[1] = make_uint4(sa[0], sa[1], sa[2], sa[3]);
+                rec[2] = make_uint4(sbb[0], sbb[1], sbb[2], sbb[3]);
+                rec[3] = make_uint4(present, 0u, 0u, 0u);
+            }
+            sb += __popc(bal);
+        }
+    }
+    if (lane == 0 && tasks_total) atomicAdd(reinterpret_cast<unsigned long long *>(a.counts + 6), tasks_total);
 }
 
 // ---- host side ---------------------------------------------------------------------------------
@@ -285,70 +395,68 @@ static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; 
 
 struct PlanWorkspace {
     PlanShared *shared;
-    unsigned long long *tile_state[PLAN_MAX_LEVELS];   // per parent level
+    unsigned long long *tile_state[PLAN_MAX_LEVELS + 1];   // per parent level
     LevelBuf buf[2];
     size_t zero_bytes;                // prefix of the workspace that must be cleared per plan
     size_t total;
 };
 
-static PlanWorkspace carve(void *ws, int64_t task_cap, int64_t leaf_cap)
+static PlanWorkspace carve(void *ws, int64_t list_cap, int64_t node_cap)
 {
     PlanWorkspace w;
     char *p = reinterpret_cast<char *>(ws);
     size_t o = 0;
     w.shared = reinterpret_cast<PlanShared *>(p + o);
     o = align_up(o + sizeof(PlanShared), 256);
-    for (int lvl = 0; lvl < PLAN_MAX_LEVELS; ++lvl) {   // a level has at most min(4^lvl, leaf_cap) nodes
-        int64_t nodes = (lvl < 15) ? (int64_t(1) << (2 * lvl)) : leaf_cap;
-        if (nodes > leaf_cap) nodes = leaf_cap;
+    for (int lvl = 0; lvl <= PLAN_MAX_LEVELS; ++lvl) {   // a level has at most min(4^lvl, node_cap) nodes
+        int64_t nodes = (lvl < 15) ? (int64_t(1) << (2 * lvl)) : node_cap;
+        if (nodes > node_cap) nodes = node_cap;
         w.tile_state[lvl] = reinterpret_cast<unsigned long long *>(p + o);
         o = align_up(o + sizeof(unsigned long long) * (size_t)((nodes + PLAN_WARPS - 1) / PLAN_WARPS + 1), 256);
     }
     w.zero_bytes = o;
     for (int x = 0; x < 2; ++x) {
         w.buf[x].node = reinterpret_cast<uint32_t *>(p + o);
-        o = align_up(o + 4 * (size_t)(leaf_cap + 1), 256);
+        o = align_up(o + 4 * (size_t)(node_cap + 1), 256);
         w.buf[x].off = reinterpret_cast<int32_t *>(p + o);
-        o = align_up(o + 4 * (size_t)(leaf_cap + 2), 256);
+        o = align_up(o + 4 * (size_t)(node_cap + 2), 256);
         w.buf[x].ks = reinterpret_cast<uint32_t *>(p + o);
-        o = align_up(o + 4 * (size_t)(task_cap + 1), 256);
+        o = align_up(o + 4 * (size_t)(list_cap + 1), 256);
     }
     w.total = o;
     return w;
 }
 
-extern "C" size_t spamm_plan_workspace_bytes(int depth, int64_t task_capacity, int64_t leaf_capacity)
+extern "C" size_t spamm_plan_workspace_bytes(int depth, int64_t step_capacity, int64_t leaf_capacity)
 {
     (void)depth;
-    return carve(nullptr, task_capacity, leaf_capacity).total;
+    return carve(nullptr, step_capacity, leaf_capacity).total;
 }
 
-template <bool FINE>
-static int run_plan(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
-                    const spamm_plan_buffers *out, const PlanWorkspace &w, cudaStream_t st)
+extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
+                          const spamm_plan_buffers *out, void *ws, size_t ws_bytes, void *stream)
 {
+    if (!a || !b || !out || !ws) return SPAMM_EINVAL;
+    if (!(tau >= 0.0)) return SPAMM_EINVAL;                       // NaN or negative (symbolic.py:99-100)
+    if (a->depth != b->depth || a->depth < 0 || a->depth > 15) return SPAMM_EINVAL;
+    if (out->step_capacity < 1 || out->leaf_capacity < 1 || out->step_capacity >= (int64_t(1) << 31) - 64) return SPAMM_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    PlanWorkspace w = carve(ws, out->step_capacity, out->leaf_capacity);
+    if (ws_bytes < w.total) return SPAMM_EWORKSPACE;
+    if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return SPAMM_ECUDA;
+    if (cudaMemsetAsync(out->counts, 0, SPAMM_PLAN_COUNTS * sizeof(int32_t), st) != cudaSuccess) return SPAMM_ECUDA;
+
     const int depth = a->depth;
-    const int L = 1 << depth;
-    LeafOut lo{a->slot, b->slot_t, a->sub4, b->sub4, out->task_a, out->task_b, out->task_mask, L};
-    LevelBuf final_buf{out->c_keys, out->c_off, out->task_k};
+    const int tl = depth >= 2 ? depth - 2 : 0;          // super-tile level
+    const int l0 = tl < 4 ? tl : 4;                     // start level
     int32_t *overflow = out->counts + 2, *max_list = out->counts + 3;
-    const int l0 = depth == 0 ? 0 : (depth - 1 < 4 ? depth - 1 : 4);
     int cur = 0;
-    {
-        const float *na = a->norm + spamm_level_offset(l0), *nbt = b->norm_t + spamm_level_offset(l0);
-        if (depth == 0) {
-            plan_root_kernel<true, FINE><<<1, 256, 0, st>>>(na, nbt, 0, 0, row0, row1, tau, final_buf, out->counts,
-                                                           out->leaf_capacity, out->task_capacity, overflow, lo);
-            SPAMM_CHECK_LAUNCH();
-            return SPAMM_OK;
-        }
-        plan_root_kernel<false, FINE><<<1, 256, 0, st>>>(na, nbt, l0, depth - l0, row0, row1, tau, w.buf[cur],
-                                                        w.shared->counts[l0], out->leaf_capacity, out->task_capacity,
-                                                        overflow, lo);
-        SPAMM_CHECK_LAUNCH();
-    }
-    for (int lvl = l0; lvl < depth; ++lvl) {
-        const bool last = (lvl + 1 == depth);
+    plan_root_kernel<<<1, 256, 0, st>>>(a->norm + spamm_level_offset(l0), b->norm_t + spamm_level_offset(l0), l0,
+                                        depth - l0, row0, row1, tau, w.buf[cur], w.shared->counts[l0],
+                                        out->leaf_capacity, out->step_capacity, overflow);
+    SPAMM_CHECK_LAUNCH();
+    const int grid = SPAMM_NUM_SMS * 4;
+    for (int lvl = l0; lvl < tl; ++lvl) {
         ExpandArgs x;
         x.norm_a = a->norm + spamm_level_offset(lvl + 1);
         x.norm_bt = b->norm_t + spamm_level_offset(lvl + 1);
@@ -356,36 +464,35 @@ static int run_plan(const spamm_tree_view *a, const spamm_tree_view *b, double t
         x.shift = depth - (lvl + 1);
         x.row0 = row0; x.row1 = row1; x.tau = tau;
         x.in = w.buf[cur];
-        x.out = last ? final_buf : w.buf[cur ^ 1];
+        x.out = w.buf[cur ^ 1];
         x.counts_in = w.shared->counts[lvl];
-        x.counts_out = last ? out->counts : w.shared->counts[lvl + 1];
-        x.cap_nodes = out->leaf_capacity; x.cap_tasks = out->task_capacity;
+        x.counts_out = w.shared->counts[lvl + 1];
+        x.cap_nodes = out->leaf_capacity; x.cap_tasks = out->step_capacity;
         x.overflow = overflow; x.max_list = max_list;
         x.tile_counter = &w.shared->tile_counter[lvl];
         x.tile_state = w.tile_state[lvl];
-        x.lo = lo;
-        const int grid = SPAMM_NUM_SMS * 4;
-        if (last) plan_expand_kernel<true, FINE><<<grid, PLAN_THREADS, 0, st>>>(x);
-        else plan_expand_kernel<false, FINE><<<grid, PLAN_THREADS, 0, st>>>(x);
+        plan_expand_kernel<<<grid, PLAN_THREADS, 0, st>>>(x);
         SPAMM_CHECK_LAUNCH();
         cur ^= 1;
     }
+    TileArgs t;
+    t.norm_a = a->norm + spamm_level_offset(depth);
+    t.norm_bt = b->norm_t + spamm_level_offset(depth);
+    t.slot_a = a->slot;
+    t.slot_bt = b->slot_t;
+    t.L = 1 << depth;
+    t.sub = 1 << (depth - tl);
+    t.row0 = row0; t.row1 = row1; t.tau = tau;
+    t.in = w.buf[cur];
+    t.counts_in = w.shared->counts[tl];
+    t.steps = out->steps;
+    t.c_keys = out->c_keys;
+    t.tile_off = out->tile_off;
+    t.cap_steps = out->step_capacity; t.cap_leaves = out->leaf_capacity;
+    t.counts = out->counts;
+    t.tile_counter = &w.shared->tile_counter[PLAN_MAX_LEVELS];
+    t.tile_state = w.tile_state[PLAN_MAX_LEVELS];
+    plan_tiles_kernel<<<grid, PLAN_THREADS, 0, st>>>(t);
+    SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
-}
-
-extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity, int32_t row0,
-                          int32_t row1, const spamm_plan_buffers *out, void *ws, size_t ws_bytes, void *stream)
-{
-    if (!a || !b || !out || !ws) return SPAMM_EINVAL;
-    if (!(tau >= 0.0)) return SPAMM_EINVAL;                       // NaN or negative (symbolic.py:99-100)
-    if (a->depth != b->depth || a->depth < 0 || a->depth > 15) return SPAMM_EINVAL;
-    if (granularity != SPAMM_FINE4 && granularity != SPAMM_COARSE16) return SPAMM_EINVAL;
-    if (out->task_capacity < 1 || out->leaf_capacity < 1 || out->task_capacity >= (int64_t(1) << 31) - 64) return SPAMM_EINVAL;
-    cudaStream_t st = (cudaStream_t)stream;
-    PlanWorkspace w = carve(ws, out->task_capacity, out->leaf_capacity);
-    if (ws_bytes < w.total) return SPAMM_EWORKSPACE;
-    if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return SPAMM_ECUDA;
-    if (cudaMemsetAsync(out->counts, 0, 4 * sizeof(int32_t), st) != cudaSuccess) return SPAMM_ECUDA;
-    return granularity == SPAMM_FINE4 ? run_plan<true>(a, b, tau, row0, row1, out, w, st)
-                                      : run_plan<false>(a, b, tau, row0, row1, out, w, st);
 }

@@ -130,11 +130,14 @@ extern "C" int spamm_assign_slots(const float *leaf_norm, int depth, int32_t *sl
     return scan_flags(op, (int64_t)L * L, nleaf_dev, ws, ws_bytes, (cudaStream_t)stream);
 }
 
-// K1c. One 256-thread block per stored leaf: row-major copy, transposed copy, sub-norms.
+// K1c. One 256-thread block per stored leaf.  A stored leaf is a 272-float record: 256 values
+// followed by its 16 sub-block norms, so one bulk copy stages both.  `values` holds the leaf
+// row-major with the sub-norms transposed (tail[q*4+r] = sub4[r][q], what a B operand reads);
+// `values_t` holds the transposed leaf with the sub-norms row-major (what an A operand reads).
 __global__ void __launch_bounds__(256) pack_leaves_kernel(const float *__restrict__ dense, int64_t m, int64_t n, int64_t ld,
                                                           int L, const uint32_t *__restrict__ keys,
                                                           const float *__restrict__ sub4_grid, float *__restrict__ values,
-                                                          float *__restrict__ values_t, float *__restrict__ sub4)
+                                                          float *__restrict__ values_t)
 {
     __shared__ float tile[16][17];
     const int64_t s = blockIdx.x;
@@ -143,21 +146,25 @@ __global__ void __launch_bounds__(256) pack_leaves_kernel(const float *__restric
     const int r = threadIdx.x >> 4, c = threadIdx.x & 15;
     const int64_t gi = (int64_t)bi * 16 + r, gj = (int64_t)bj * 16 + c;
     const float v = (gi < m && gj < n) ? __ldg(dense + gi * ld + gj) : 0.0f;
-    values[s * 256 + threadIdx.x] = v;
+    values[s * SPAMM_REC + threadIdx.x] = v;
     tile[r][c] = v;
     __syncthreads();
-    values_t[s * 256 + threadIdx.x] = tile[c][r];
-    if (threadIdx.x < 16) sub4[s * 16 + threadIdx.x] = sub4_grid[((int64_t)bi * L + bj) * 16 + threadIdx.x];
+    values_t[s * SPAMM_REC + threadIdx.x] = tile[c][r];
+    if (threadIdx.x < 16) {
+        const float sn = sub4_grid[((int64_t)bi * L + bj) * 16 + threadIdx.x];   // threadIdx.x = p*4+q
+        values_t[s * SPAMM_REC + 256 + threadIdx.x] = sn;
+        values[s * SPAMM_REC + 256 + (threadIdx.x & 3) * 4 + (threadIdx.x >> 2)] = sn;
+    }
 }
 
 extern "C" int spamm_pack_leaves(const float *dense, int64_t m, int64_t n, int64_t ld, int depth,
-                                      const uint32_t *keys, int64_t nleaf, const float *sub4_grid, float *values,
-                                      float *values_t, float *sub4, void *stream)
+                                 const uint32_t *keys, int64_t nleaf, const float *sub4_grid, float *values,
+                                 float *values_t, void *stream)
 {
     if (nleaf == 0) return SPAMM_OK;
     if (!dense || nleaf < 0 || depth < 0 || depth > 15) return SPAMM_EINVAL;
     pack_leaves_kernel<<<(unsigned)nleaf, 256, 0, (cudaStream_t)stream>>>(dense, m, n, ld, 1 << depth, keys, sub4_grid,
-                                                                         values, values_t, sub4);
+                                                                         values, values_t);
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
 }
@@ -301,8 +308,8 @@ __device__ __forceinline__ double leaf_total_refresh(double S)
     return r;
 }
 
-__global__ void __launch_bounds__(256) leaf_norms_packed_kernel(const float *__restrict__ values, int64_t nleaf,
-                                                                float *__restrict__ values_t, float *__restrict__ sub4,
+__global__ void __launch_bounds__(256) leaf_norms_packed_kernel(float *__restrict__ values, int64_t nleaf,
+                                                                float *__restrict__ values_t,
                                                                 double *__restrict__ leaf_sq)
 {
     const int64_t leaf = (int64_t)blockIdx.x * 16 + (threadIdx.x >> 4);
@@ -311,29 +318,28 @@ __global__ void __launch_bounds__(256) leaf_norms_packed_kernel(const float *__r
     float4 r[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-        r[i] = ok ? __ldg(reinterpret_cast<const float4 *>(values + leaf * 256 + (4 * p + i) * 16 + 4 * q))
+        r[i] = ok ? *reinterpret_cast<const float4 *>(values + leaf * SPAMM_REC + (4 * p + i) * 16 + 4 * q)
                   : make_float4(0.f, 0.f, 0.f, 0.f);
     const double S = sub_block_sq(r[0], r[1], r[2], r[3]);
     const double total = leaf_total_refresh(S);
     if (!ok) return;
-    sub4[leaf * 16 + t] = (float)sqrt(S);
+    const float sn = (float)sqrt(S);
+    values[leaf * SPAMM_REC + 256 + q * 4 + p] = sn;
     if (t == 0) leaf_sq[leaf] = total;
-    if (values_t) {
-        float *vt = values_t + leaf * 256;
-        *reinterpret_cast<float4 *>(vt + (4 * q + 0) * 16 + 4 * p) = make_float4(r[0].x, r[1].x, r[2].x, r[3].x);
-        *reinterpret_cast<float4 *>(vt + (4 * q + 1) * 16 + 4 * p) = make_float4(r[0].y, r[1].y, r[2].y, r[3].y);
-        *reinterpret_cast<float4 *>(vt + (4 * q + 2) * 16 + 4 * p) = make_float4(r[0].z, r[1].z, r[2].z, r[3].z);
-        *reinterpret_cast<float4 *>(vt + (4 * q + 3) * 16 + 4 * p) = make_float4(r[0].w, r[1].w, r[2].w, r[3].w);
-    }
+    float *vt = values_t + leaf * SPAMM_REC;
+    vt[256 + t] = sn;
+    *reinterpret_cast<float4 *>(vt + (4 * q + 0) * 16 + 4 * p) = make_float4(r[0].x, r[1].x, r[2].x, r[3].x);
+    *reinterpret_cast<float4 *>(vt + (4 * q + 1) * 16 + 4 * p) = make_float4(r[0].y, r[1].y, r[2].y, r[3].y);
+    *reinterpret_cast<float4 *>(vt + (4 * q + 2) * 16 + 4 * p) = make_float4(r[0].z, r[1].z, r[2].z, r[3].z);
+    *reinterpret_cast<float4 *>(vt + (4 * q + 3) * 16 + 4 * p) = make_float4(r[0].w, r[1].w, r[2].w, r[3].w);
 }
 
-extern "C" int spamm_leaf_norms_packed(const float *values, int64_t nleaf, float *values_t, float *sub4, double *leaf_sq,
-                                       void *stream)
+extern "C" int spamm_leaf_norms_packed(float *values, int64_t nleaf, float *values_t, double *leaf_sq, void *stream)
 {
     if (nleaf == 0) return SPAMM_OK;
-    if (!values || nleaf < 0) return SPAMM_EINVAL;
+    if (!values || !values_t || nleaf < 0) return SPAMM_EINVAL;
     leaf_norms_packed_kernel<<<(unsigned)((nleaf + 15) / 16), 256, 0, (cudaStream_t)stream>>>(values, nleaf, values_t,
-                                                                                            sub4, leaf_sq);
+                                                                                            leaf_sq);
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
 }
@@ -397,7 +403,7 @@ __global__ void __launch_bounds__(256) to_dense_kernel(const int32_t *__restrict
     const int64_t gi = (int64_t)bi * 16 + r, gj = (int64_t)bj * 16 + c;
     if (gi >= m || gj >= n) return;
     const int32_t s = slot[(int64_t)bi * L + bj];
-    out[gi * ld + gj] = s >= 0 ? values[(int64_t)s * 256 + threadIdx.x] : 0.0f;
+    out[gi * ld + gj] = s >= 0 ? values[(int64_t)s * SPAMM_REC + threadIdx.x] : 0.0f;
 }
 
 extern "C" int spamm_to_dense(const spamm_tree_view *t, float *out, int64_t ld, void *stream)

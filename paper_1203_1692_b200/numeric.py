@@ -121,8 +121,6 @@ def execute_plan(plan: MultiplyPlan, a: QuadtreeMatrix, b: QuadtreeMatrix, c: Qu
     elif (c.m, c.n) != (a.m, b.n) or c.n_b != nb:
         raise ValueError(f"accumulator is {c.m}x{c.n} (n_b={c.n_b}), product needs {a.m}x{b.n} (n_b={nb})")
     _check_plan_handles(plan, a, b)
-    if plan.n_tasks and plan.granularity != cfg.granularity and cfg.granularity == "fine4":
-        raise ValueError("plan carries coarse16 masks; rebuild it with granularity='fine4'")
     lib = _lib.lib()
     st = _stream()
     dev = a.device
@@ -136,30 +134,25 @@ def execute_plan(plan: MultiplyPlan, a: QuadtreeMatrix, b: QuadtreeMatrix, c: Qu
     prod = None
     if run:
         va, vb = a.view(plan.depth), b.view(plan.depth)
-        vals = torch.empty((nC, 256), dtype=torch.float32, device=dev)
-        vals_t = torch.empty((nC, 256), dtype=torch.float32, device=dev)
-        sub4 = torch.empty((nC, 16), dtype=torch.float32, device=dev)
+        vals = torch.empty((nC, _lib.REC), dtype=torch.float32, device=dev)
+        vals_t = torch.empty((nC, _lib.REC), dtype=torch.float32, device=dev)
         leaf_sq = torch.empty((nC,), dtype=torch.float64, device=dev)
-        ws_bytes = lib.spamm_execute_workspace_bytes(nC)
-        ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
-        bufs = _lib.PlanBuffers(plan.c_keys.data_ptr(), plan.c_off.data_ptr(), plan.task_k.data_ptr(),
-                                plan.task_a.data_ptr(), plan.task_b.data_ptr(), plan.task_mask.data_ptr(),
-                                T, nC, None)
+        bufs = plan.buffers()
         # with an accumulator to merge, the kernel leaves alpha to the compose step
         alpha_k = 1.0 if keep_old else float(np.float32(cfg.alpha))
         gran = _lib.FINE4 if fine else _lib.COARSE16
-        _lib.check(lib.spamm_execute(C.byref(va), C.byref(vb), C.byref(bufs), T, nC, alpha_k, gran, int(cfg.exact),
-                                     vals.data_ptr(), vals_t.data_ptr(), sub4.data_ptr(), leaf_sq.data_ptr(),
-                                     counters_dev.data_ptr(), ws.data_ptr(), ws_bytes, st), "execute")
-        prod = (plan.c_keys[:nC], vals, vals_t, sub4, leaf_sq)
+        _lib.check(lib.spamm_execute(C.byref(va), C.byref(vb), C.byref(bufs), plan.n_steps, nC, float(cfg.tau), alpha_k,
+                                     gran, int(cfg.exact), vals.data_ptr(), vals_t.data_ptr(), leaf_sq.data_ptr(),
+                                     counters_dev.data_ptr(), st), "execute")
+        prod = (plan.c_keys[:nC], vals, vals_t, leaf_sq)
     # _compose (`numeric.py:268-284`)
     if not keep_old:
         if prod is None:
             if cfg.beta == 0 or c.nleaf == 0:
                 c.clear()
         else:
-            keys, vals, vals_t, sub4, leaf_sq = prod
-            c._adopt_packed(keys.clone(), vals, vals_t, sub4, leaf_sq, nC)
+            keys, vals, vals_t, leaf_sq = prod
+            c._adopt_packed(keys.clone(), vals, vals_t, leaf_sq, nC)
     else:
         _compose_with_accumulator(c, prod, cfg)
     e1.record()
@@ -198,7 +191,7 @@ def _compose_with_accumulator(c: QuadtreeMatrix, prod, cfg: MultiplyConfig) -> N
                                       scratch.data_ptr(), out_keys.data_ptr(), idx_old.data_ptr(), idx_prod.data_ptr(),
                                       nout_dev.data_ptr(), ws.data_ptr(), ws_bytes, st), "union_leaves")
     nout = int(nout_dev.item())
-    out_vals = torch.empty((nout, 256), dtype=torch.float32, device=dev)
+    out_vals = torch.empty((nout, _lib.REC), dtype=torch.float32, device=dev)
     _lib.check(lib.spamm_compose(None if pv is None else pv.data_ptr(), c.values.data_ptr(), idx_prod.data_ptr(),
                                  idx_old.data_ptr(), nout, float(np.float32(cfg.alpha)), float(np.float32(cfg.beta)),
                                  int(cfg.alpha == 1), int(cfg.beta == 1), out_vals.data_ptr(), st), "compose")
@@ -210,6 +203,6 @@ def multiply(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig | None = 
     """Symbolic plus numeric phases in one call (`numeric.py:302-313`)."""
     if cfg is None:
         cfg = MultiplyConfig()
-    plan = build_plan(a, b, cfg.tau, cfg.granularity)
+    plan = build_plan(a, b, cfg.tau)
     out, counters = execute_plan(plan, a, b, c, cfg)
     return out, plan, counters

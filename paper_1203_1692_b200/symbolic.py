@@ -1,9 +1,10 @@
 """Symbolic multiply phase on the device: ``build_plan``.
 
-Drop-in for `pkg/src/spamm/symbolic.py:151-159`.  The plan lives in HBM as the CSR task list
-the numeric kernel consumes (product leaves in Morton order, tasks in ascending k); the
-reference's host view -- ``plan.tasks`` as ``ProductTask`` objects in the reference's plan
-order, ``plan.stats`` and ``plan_dump`` -- is materialised lazily from it.
+Drop-in for `pkg/src/spamm/symbolic.py:151-159`.  The plan lives in HBM as the step records the
+numeric kernel consumes (``spamm_step`` in ``include/spamm_b200.h``: per 4x4 super-tile of
+product leaves and per k, the 16 live-task bits and the operand leaf slots).  The reference's host
+view -- ``plan.tasks`` as ``ProductTask`` objects in the reference's plan order, ``plan.stats``
+and ``plan_dump`` -- is decoded from it on demand.
 """
 
 from __future__ import annotations
@@ -33,53 +34,90 @@ class PlanStats:
     pruned: int = 0
 
 
-# capacity that worked last time for a (depth, leaves of A, leaves of B) shape
+# capacities that worked last time for a (depth, leaves of A, leaves of B, tau, rows) shape
 _capacity_hint: dict[tuple, tuple[int, int]] = {}
+
+_POS_DI = np.array([((p >> 3) & 1) << 1 | ((p >> 1) & 1) for p in range(16)], np.int64)
+_POS_DJ = np.array([((p >> 2) & 1) << 1 | (p & 1) for p in range(16)], np.int64)
 
 
 class MultiplyPlan:
     """Surviving block products for one (A, B, tau) (`symbolic.py:49-56`), device resident.
 
-    Device arrays (see ``spamm_plan_buffers``): ``c_keys[nC]``, ``c_off[nC+1]``, ``task_k/a/b[T]``,
-    ``task_mask[T]``.  ``len(plan)`` is the task count; ``plan.tasks`` builds the reference's
-    host list on demand.
+    ``len(plan)`` is the task count; ``plan.tasks`` builds the reference's host list on demand.
     """
 
-    def __init__(self, tau, granularity, depth, n_tasks, n_cleaves, buffers, a, b, row_range):
+    def __init__(self, tau, depth, n_tasks, n_cleaves, n_steps, steps, c_keys, tile_off, counts, a, b, row_range):
         self.tau = float(tau)
-        self.granularity = granularity
         self.depth = depth
         self.n_tasks = int(n_tasks)
         self.n_cleaves = int(n_cleaves)
-        self.c_keys, self.c_off, self.task_k, self.task_a, self.task_b, self.task_mask = buffers
+        self.n_steps = int(n_steps)
+        self.steps, self.c_keys, self.tile_off, self.counts = steps, c_keys, tile_off, counts
         self._a, self._b = a, b
         self._tokens = (id(a), a._rev, id(b), b._rev)
         self.row_range = row_range
         self._tasks = None
         self._stats = None
+        self._ikj = None
 
     def __len__(self) -> int:
         return self.n_tasks
 
-    # -- host views ---------------------------------------------------------------------------
-    def ikj(self) -> np.ndarray:
-        """(T, 3) int64 array of (i, k, j) leaf coordinates in device order."""
-        T, nC = self.n_tasks, self.n_cleaves
-        if T == 0:
-            return np.zeros((0, 3), np.int64)
-        keys = self.c_keys[:nC].cpu().numpy().astype(np.uint64)
-        off = self.c_off[:nC + 1].cpu().numpy().astype(np.int64)
-        ci, cj = morton.decode_array(keys)
-        rep = np.diff(off)
-        k = self.task_k[:T].cpu().numpy().astype(np.int64)
-        return np.stack([np.repeat(ci.astype(np.int64), rep), k, np.repeat(cj.astype(np.int64), rep)], axis=1)
+    def buffers(self) -> _lib.PlanBuffers:
+        return _lib.PlanBuffers(self.steps.data_ptr(), self.c_keys.data_ptr(), self.tile_off.data_ptr(),
+                                self.steps.shape[0], self.c_keys.shape[0], self.counts.data_ptr())
 
-    def masks(self) -> np.ndarray:
-        return self.task_mask[: self.n_tasks].cpu().numpy().view(np.uint64)
+    # -- host views ---------------------------------------------------------------------------
+    def step_records(self) -> np.ndarray:
+        """(n_steps, 16) uint32 host copy of the step records."""
+        return self.steps[: self.n_steps].cpu().numpy().view(np.uint32).reshape(-1, _lib.STEP_WORDS)
+
+    def ikj(self) -> np.ndarray:
+        """(T, 3) int64 array of task coordinates (i, k, j), sorted by product leaf key then k."""
+        if self._ikj is not None:
+            return self._ikj
+        if self.n_tasks == 0:
+            self._ikj = np.zeros((0, 3), np.int64)
+            return self._ikj
+        rec = self.step_records()
+        sub_shift = min(2, self.depth)               # super-tiles are 4x4 leaves (2x2, 1x1 for tiny trees)
+        k = rec[:, 0].astype(np.int64)
+        live = rec[:, 1].astype(np.int64) & 0xFFFF
+        ti, tj = morton.decode_array(rec[:, 3].astype(np.uint64))
+        bits = (live[:, None] >> np.arange(16)[None, :]) & 1
+        s_idx, pos = np.nonzero(bits)
+        i = (ti[s_idx].astype(np.int64) << sub_shift) + _POS_DI[pos]
+        j = (tj[s_idx].astype(np.int64) << sub_shift) + _POS_DJ[pos]
+        t = np.stack([i, k[s_idx], j], axis=1)
+        ck = morton.encode_array(t[:, 0], t[:, 2])
+        order = np.lexsort((t[:, 1], ck))
+        self._ikj = t[order]
+        assert self._ikj.shape[0] == self.n_tasks
+        return self._ikj
 
     def pair_keys(self) -> tuple[np.ndarray, np.ndarray]:
         t = self.ikj()
         return morton.encode_array(t[:, 0], t[:, 1]), morton.encode_array(t[:, 1], t[:, 2])
+
+    def masks(self) -> np.ndarray:
+        """fine4 live bits per task of ``ikj()`` (bit r*16 + p*4 + q, `numeric.py:232-238`),
+        evaluated on the host from the operands' sub-block norms; the device evaluates the same
+        products inside the numeric kernel."""
+        t = self.ikj()
+        out = np.zeros(t.shape[0], np.uint64)
+        if t.shape[0] == 0:
+            return out
+        ka, _, sa = self._a.packed_leaves()
+        kb, _, sb = self._b.packed_leaves()
+        an = sa[np.searchsorted(ka, morton.encode_array(t[:, 0], t[:, 1]))].astype(np.float64)
+        bn = sb[np.searchsorted(kb, morton.encode_array(t[:, 1], t[:, 2]))].astype(np.float64)
+        for r in range(4):
+            live = an[:, :, r][:, :, None] * bn[:, r, :][:, None, :] >= self.tau
+            for p in range(4):
+                for q in range(4):
+                    out |= live[:, p, q].astype(np.uint64) << np.uint64(r * 16 + p * 4 + q)
+        return out
 
     def _reference_order(self):
         """Tasks in the reference's plan order with their norm products, and the loop
@@ -97,7 +135,6 @@ class MultiplyPlan:
             tasks = (ka[order], kb[order], morton.encode_array(i, j)[order], (va * vb)[order])
         else:
             tasks = (np.zeros(0, np.uint64),) * 3 + (np.zeros(0, np.float64),)
-        # statistics: per k block, walk A entries by descending norm
         examined = pruned = 0
         rows_a, cols_b = -(-self._a.m // 16), -(-self._b.n // 16)
         r0, r1 = self.row_range
@@ -148,13 +185,12 @@ def _check_tau(tau) -> None:
         raise ValueError(f"tau must be nonnegative, got {tau}")
 
 
-def build_plan(a: QuadtreeMatrix, b: QuadtreeMatrix, tau: float, granularity: str = "fine4",
+def build_plan(a: QuadtreeMatrix, b: QuadtreeMatrix, tau: float,
                row_range: tuple[int, int] | None = None) -> MultiplyPlan:
     """Full symbolic pipeline for C = A B on the device (`symbolic.py:151-159`).
 
-    ``granularity`` only selects which fine4 masks are attached to the tasks (the task set does
-    not depend on it); ``row_range`` restricts the plan to product leaf rows [r0, r1) for the
-    row-block sharding across GPUs.
+    ``row_range`` restricts the plan to product leaf rows [r0, r1): the row-block sharding
+    across GPUs.
     """
     if a.n_b != b.n_b:
         raise ValueError(f"block sizes differ: {a.n_b} vs {b.n_b}")
@@ -167,37 +203,34 @@ def build_plan(a: QuadtreeMatrix, b: QuadtreeMatrix, tau: float, granularity: st
     L = 1 << depth
     r0, r1 = (0, L) if row_range is None else (int(row_range[0]), int(row_range[1]))
     dev = a.device
-    gran = _lib.FINE4 if granularity == "fine4" else _lib.COARSE16
     if a.nleaf == 0 or b.nleaf == 0:
-        empty = torch.empty((1,), dtype=torch.int32, device=dev)
-        return MultiplyPlan(tau, granularity, depth, 0, 0, (empty,) * 5 + (torch.empty((1,), dtype=torch.int64, device=dev),),
-                            a, b, (r0, r1))
+        z = torch.zeros((1, _lib.STEP_WORDS), dtype=torch.int32, device=dev)
+        e = torch.zeros((_lib.PLAN_COUNTS,), dtype=torch.int32, device=dev)
+        return MultiplyPlan(tau, depth, 0, 0, 0, z, e, e, e, a, b, (r0, r1))
     va, vb = a.view(depth), b.view(depth)
     hint_key = (depth, a.nleaf, b.nleaf, float(tau), r0, r1)
-    task_cap, leaf_cap = _capacity_hint.get(hint_key, (max(4096, 24 * (a.nleaf + b.nleaf)),
+    step_cap, leaf_cap = _capacity_hint.get(hint_key, (max(4096, 4 * (a.nleaf + b.nleaf)),
                                                        min(L * L, max(1024, 2 * (a.nleaf + b.nleaf)))))
-    max_tasks = min((1 << 31) - 128, L * L * L)
+    max_steps = min((1 << 31) - 128, max(1, (L * L * L) // 16 + L * L))
     while True:
-        c_keys = torch.empty((leaf_cap + 1,), dtype=torch.int32, device=dev)
-        c_off = torch.empty((leaf_cap + 2,), dtype=torch.int32, device=dev)
-        task_k = torch.empty((task_cap + 1,), dtype=torch.int32, device=dev)
-        task_a = torch.empty((task_cap + 1,), dtype=torch.int32, device=dev)
-        task_b = torch.empty((task_cap + 1,), dtype=torch.int32, device=dev)
-        task_mask = torch.empty((task_cap + 1,), dtype=torch.int64, device=dev)
-        counts = torch.empty((4,), dtype=torch.int32, device=dev)
-        ws_bytes = lib.spamm_plan_workspace_bytes(depth, task_cap, leaf_cap)
+        steps = torch.empty((step_cap, _lib.STEP_WORDS), dtype=torch.int32, device=dev)
+        c_keys = torch.empty((leaf_cap,), dtype=torch.int32, device=dev)
+        tile_off = torch.empty((leaf_cap + 1,), dtype=torch.int32, device=dev)
+        counts = torch.empty((_lib.PLAN_COUNTS,), dtype=torch.int32, device=dev)
+        ws_bytes = lib.spamm_plan_workspace_bytes(depth, step_cap, leaf_cap)
         ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
-        bufs = _lib.PlanBuffers(c_keys.data_ptr(), c_off.data_ptr(), task_k.data_ptr(), task_a.data_ptr(),
-                                task_b.data_ptr(), task_mask.data_ptr(), task_cap, leaf_cap, counts.data_ptr())
-        _lib.check(lib.spamm_plan(C.byref(va), C.byref(vb), float(tau), gran, r0, r1, C.byref(bufs), ws.data_ptr(),
+        bufs = _lib.PlanBuffers(steps.data_ptr(), c_keys.data_ptr(), tile_off.data_ptr(), step_cap, leaf_cap,
+                                counts.data_ptr())
+        _lib.check(lib.spamm_plan(C.byref(va), C.byref(vb), float(tau), r0, r1, C.byref(bufs), ws.data_ptr(),
                                   ws_bytes, _stream()), "plan")
-        n_c, n_t, overflow, max_list = counts.tolist()
+        cnt = counts.tolist()
+        n_c, overflow, max_list, n_steps = cnt[0], cnt[2], cnt[3], cnt[4]
+        n_t = (cnt[6] & 0xFFFFFFFF) | ((cnt[7] & 0xFFFFFFFF) << 32)
         if not overflow:
             break
-        if task_cap >= max_tasks and leaf_cap >= L * L:
-            raise RuntimeError("plan does not fit the 2^31 task limit")
-        task_cap = min(max_tasks, max(2 * task_cap, int(1.25 * max_list) + 1024))
-        leaf_cap = min(L * L, 4 * leaf_cap)
-    _capacity_hint[hint_key] = (task_cap, leaf_cap)
-    return MultiplyPlan(tau, granularity, depth, n_t, n_c, (c_keys, c_off, task_k, task_a, task_b, task_mask),
-                        a, b, (r0, r1))
+        if step_cap >= max_steps and leaf_cap >= L * L:
+            raise RuntimeError("plan does not fit the 2^31 step limit")
+        step_cap = min(max_steps, max(2 * step_cap, int(1.25 * max(max_list, n_steps)) + 1024))
+        leaf_cap = min(L * L, max(4 * leaf_cap, int(1.25 * n_c) + 1024))
+    _capacity_hint[hint_key] = (step_cap, leaf_cap)
+    return MultiplyPlan(tau, depth, n_t, n_c, n_steps, steps, c_keys, tile_off, counts, a, b, (r0, r1))

@@ -98,7 +98,7 @@ class QuadtreeMatrix:
     # -- storage -------------------------------------------------------------------------------
     def _set_empty(self) -> None:
         self.nleaf = 0
-        self.keys = self.values = self.values_t = self.sub4 = None
+        self.keys = self.values = self.values_t = None
         self.leaf_sq = None          # double square sum per packed leaf
         self._leaf_sq_grid = None    # the same on the leaf grid (from_dense keeps this form)
         self._grids: dict[int, _Grids] = {}
@@ -165,12 +165,11 @@ class QuadtreeMatrix:
         nleaf = int(nleaf_dev.item())
         self.nleaf = nleaf
         self.keys = keys[:nleaf].clone()
-        self.values = self._alloc((max(nleaf, 1), 256), torch.float32)
-        self.values_t = self._alloc((max(nleaf, 1), 256), torch.float32)
-        self.sub4 = self._alloc((max(nleaf, 1), 16), torch.float32)
+        self.values = self._alloc((max(nleaf, 1), _lib.REC), torch.float32)
+        self.values_t = self._alloc((max(nleaf, 1), _lib.REC), torch.float32)
         _lib.check(lib.spamm_pack_leaves(d.data_ptr(), self.m, self.n, d.stride(0), depth, self.keys.data_ptr(), nleaf,
-                                         sub4_grid.data_ptr(), self.values.data_ptr(), self.values_t.data_ptr(),
-                                         self.sub4.data_ptr(), st), "pack_leaves")
+                                         sub4_grid.data_ptr(), self.values.data_ptr(), self.values_t.data_ptr(), st),
+                   "pack_leaves")
         sq_levels = self._alloc((_lib.level_total(depth),), torch.float64)
         _lib.check(lib.spamm_build_interior(leaf_sq_grid.data_ptr(), depth, norm.data_ptr(), norm_t.data_ptr(),
                                             sq_levels.data_ptr(), 1, st), "build_interior")
@@ -179,12 +178,12 @@ class QuadtreeMatrix:
         self._grids = {depth: _Grids(depth, slot, slot_t, norm, norm_t)}
         self._rev += 1
 
-    def _adopt_packed(self, keys: torch.Tensor, values: torch.Tensor, values_t: torch.Tensor, sub4: torch.Tensor,
+    def _adopt_packed(self, keys: torch.Tensor, values: torch.Tensor, values_t: torch.Tensor,
                       leaf_sq: torch.Tensor, nleaf: int) -> None:
         """Take ownership of packed leaves whose norms are already known (a multiply result)."""
         self._pending.clear()
         self.nleaf = int(nleaf)
-        self.keys, self.values, self.values_t, self.sub4, self.leaf_sq = keys, values, values_t, sub4, leaf_sq
+        self.keys, self.values, self.values_t, self.leaf_sq = keys, values, values_t, leaf_sq
         self._leaf_sq_grid = None
         self._grids = {}
         self._index(self.depth)
@@ -237,7 +236,7 @@ class QuadtreeMatrix:
         nz = self.nleaf > 0
         return _lib.TreeView(self.m, self.n, g.depth, self.nleaf,
                              _ptr(self.keys) if nz else None, _ptr(self.values) if nz else None,
-                             _ptr(self.values_t) if nz else None, _ptr(self.sub4) if nz else None,
+                             _ptr(self.values_t) if nz else None,
                              g.slot.data_ptr(), g.slot_t.data_ptr(), g.norm.data_ptr(), g.norm_t.data_ptr())
 
     def _flush_guard(self) -> None:
@@ -264,8 +263,8 @@ class QuadtreeMatrix:
         if n == 0:
             return (np.empty(0, np.uint64), np.empty((0, 16, 16), np.float32), np.empty((0, 4, 4), np.float32))
         return (self.keys[:n].cpu().numpy().astype(np.uint64),
-                self.values[:n].cpu().numpy().reshape(n, 16, 16),
-                self.sub4[:n].cpu().numpy().reshape(n, 4, 4))
+                np.ascontiguousarray(self.values[:n, :256].cpu().numpy()).reshape(n, 16, 16),
+                np.ascontiguousarray(self.values_t[:n, 256:].cpu().numpy()).reshape(n, 4, 4))
 
     def leaf_keys(self) -> np.ndarray:
         return self.packed_leaves()[0] if self.nleaf else np.empty(0, np.uint64)
@@ -309,7 +308,7 @@ class QuadtreeMatrix:
         leaves: dict[int, np.ndarray] = {}
         if self.nleaf:
             keys = self.keys[: self.nleaf].cpu().numpy()
-            vals = self.values[: self.nleaf].cpu().numpy().reshape(-1, 16, 16)
+            vals = self.values[: self.nleaf, :256].cpu().numpy().reshape(-1, 16, 16)
             leaves.update({int(k): v for k, v in zip(keys.tolist(), vals)})
         leaves.update(self._pending)
         self._pending.clear()
@@ -319,18 +318,18 @@ class QuadtreeMatrix:
             self._rev += 1
             return
         keys_t = torch.tensor(ks, dtype=torch.int32, device=self.device)
-        vals_t = torch.from_numpy(np.stack([leaves[k] for k in ks]).reshape(-1, 256)).to(self.device)
-        self._set_packed_values(keys_t, vals_t)
+        rec = np.zeros((len(ks), _lib.REC), np.float32)
+        rec[:, :256] = np.stack([leaves[k] for k in ks]).reshape(-1, 256)
+        self._set_packed_values(keys_t, torch.from_numpy(rec).to(self.device))
 
     def _set_packed_values(self, keys: torch.Tensor, values: torch.Tensor) -> None:
-        """Leaves given by keys (ascending) and values; norms in compute_norms order."""
+        """Leaves given by keys (ascending) and (n, 272) value records; norms in compute_norms order."""
         n = int(keys.numel())
-        values_t = self._alloc((n, 256), torch.float32)
-        sub4 = self._alloc((n, 16), torch.float32)
+        values_t = self._alloc((n, _lib.REC), torch.float32)
         leaf_sq = self._alloc((n,), torch.float64)
-        _lib.check(_lib.lib().spamm_leaf_norms_packed(values.data_ptr(), n, values_t.data_ptr(), sub4.data_ptr(),
-                                                     leaf_sq.data_ptr(), _stream()), "leaf_norms_packed")
-        self._adopt_packed(keys, values, values_t, sub4, leaf_sq, n)
+        _lib.check(_lib.lib().spamm_leaf_norms_packed(values.data_ptr(), n, values_t.data_ptr(), leaf_sq.data_ptr(),
+                                                     _stream()), "leaf_norms_packed")
+        self._adopt_packed(keys, values, values_t, leaf_sq, n)
 
     def __repr__(self) -> str:
         return (f"QuadtreeMatrix({self.m}x{self.n}, n_b={self.n_b}, depth={self.depth}, "

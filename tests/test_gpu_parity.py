@@ -47,7 +47,7 @@ def test_device_matches_reference(case):
         gran = run.get("granularity", "fine4")
         alpha, beta = run.get("alpha", 1.0), run.get("beta", 0.0)
         # ---- symbolic phase
-        plan = P.build_plan(qa, qb, tau, gran)
+        plan = P.build_plan(qa, qb, tau)
         assert len(plan) == g.get(name, f"{tag}/T")
         ka, kb = plan.pair_keys()
         pairs = np.stack([ka, kb], axis=1)
