@@ -119,23 +119,27 @@ int spamm_to_dense(const spamm_tree_view *t, float *out, int64_t ld, void *strea
 
 /* ---- symbolic phase: build_plan (symbolic.py:92-159) --------------------------- */
 
-/* The compacted task list.  Product leaves are grouped in super-tiles of 4x4 leaves (16
- * consecutive Morton keys); for every super-tile (I,J) and, in ascending order, every k that
- * has at least one surviving task, the plan holds one 64-byte step record.  Bit
- * pos = morton4(di,dj) of `live` stands for the task (i,k,j) = (4I+di, k, 4J+dj); tasks of one
- * product leaf therefore appear in ascending k, the only order the numeric phase depends on
- * (numeric.py:203-217).  The records of a super-tile are contiguous, super-tiles ascend in
- * Morton order. */
-#define SPAMM_STEP_LIVE 0xFFFFu
+/* The compacted task list.  Leaves are grouped in aligned 4x4 blocks (16 consecutive Morton
+ * keys, contiguous in the packed arrays).  For every super-tile (I,J) of product leaves and,
+ * in ascending order, every block index K with at least one surviving task, the plan holds
+ * one 64-byte step record: the block product C[I,J] += A[I,K] B[K,J] restricted to its live
+ * leaf tasks.  Bit pos = morton4(di,dj) of live[kk] stands for the task
+ * (i,k,j) = (4I+di, 4K+kk, 4J+dj); tasks of one product leaf therefore appear in ascending k,
+ * the only order the numeric phase depends on (numeric.py:203-217).  The records of a
+ * super-tile are contiguous, super-tiles ascend in Morton order.  Leaf (r,c) of a block sits
+ * at packed index first + popcount(present16 & ((1 << morton4(r,c)) - 1)). */
 #define STEP_FIRST (1u << 16)   /* first record of its super-tile */
 #define STEP_LAST (1u << 17)    /* last record of its super-tile  */
 typedef struct {
-    uint32_t k;            /* contraction leaf index                                       */
-    uint32_t live_flags;   /* bits 0-15 live tasks, STEP_FIRST, STEP_LAST                  */
+    uint32_t kblock;       /* K: contraction block index, k = 4K + kk                      */
+    uint32_t flags;        /* STEP_FIRST, STEP_LAST                                        */
     uint32_t c_base;       /* packed index of the super-tile's first product leaf          */
     uint32_t tile;         /* Morton index of the super-tile (product leaf key >> 4)       */
-    uint32_t a_slot[4];    /* packed slot of leaf A(4I+di, k), valid where a task needs it */
-    uint32_t b_slot[4];    /* packed slot of leaf B(k, 4J+dj)                              */
+    uint32_t a_first;      /* packed index of the first stored leaf of block A[I,K]        */
+    uint32_t a_present;    /* its stored leaves, bit morton4(di,kk)                        */
+    uint32_t b_first;      /* packed index of the first stored leaf of block B[K,J]        */
+    uint32_t b_present;    /* its stored leaves, bit morton4(kk,dj)                        */
+    uint32_t live[4];      /* live tasks of k = 4K + kk, bit morton4(di,dj)                */
     uint32_t present;      /* product leaves of the super-tile (same bit numbering)        */
     uint32_t pad[3];
 } spamm_step;

@@ -8,27 +8,33 @@
 // single owner and a fixed summation order: results are identical run to run and, in EXACT mode
 // (separately rounded multiply and add), bit-identical to the reference.
 //
-// Work unit: a super-tile of 4x4 product leaves, described by the plan's step records (one per
-// k with a live task).  Per CTA, one producer warp streams the records (prefetched four ahead)
-// and for each stages the needed A leaves (transposed copies) and B leaves -- 1088-byte records
-// holding the values and the 4x4 sub-block norms -- with bulk copies (TMA 1-D, cp.async.bulk,
-// SASS UBLKCP) into a ring of shared-memory stages guarded by mbarriers; eight consumer warps
-// (two product leaves each) gate and multiply from shared memory.  Super-tiles are handed out
-// through an atomic counter.
+// Work unit: a super-tile of 4x4 product leaves, described by the plan's step records, one per
+// contraction block K: C[I,J] += A[I,K] B[K,J] on 4x4 blocks of leaves, with 4 x 16 live-task
+// bits.  The stored leaves of a block are contiguous in the packed arrays (Morton order), so the
+// producer warp stages each block with ONE bulk copy (TMA 1-D, cp.async.bulk, SASS UBLKCP; up to
+// 17 KB: 16 leaf records of 1088 B holding values and sub-block norms) into a ring of
+// shared-memory stages guarded by mbarriers.  Eight consumer warps (two product leaves each)
+// gate and multiply from shared memory.  Super-tiles are handed out through an atomic counter.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "plan_format.cuh"
 
-#define EX_STAGES 4
+#define EX_MAX_STAGES 6
 #define EX_CONSUMERS 8
 #define EX_THREADS (32 * (EX_CONSUMERS + 1))
 #define EX_EXIT (1u << 31)
 #define EX_PREFETCH 4
+#define EX_BLOCK_BYTES (16 * SPAMM_REC_BYTES)     // one 4x4 block of leaf records
 
 struct __align__(16) StageDesc {
-    uint32_t flags;      // live bits | STEP_FIRST | STEP_LAST | EX_EXIT
+    uint32_t flags;        // STEP_FIRST | STEP_LAST | EX_EXIT
     uint32_t c_base;
-    uint32_t present;
-    uint32_t pad;
+    uint32_t present;      // product leaves of the super-tile
+    uint32_t a_present;    // stored leaves of the staged A block, bit morton4(di,kk)
+    uint32_t b_present;    // stored leaves of the staged B block, bit morton4(kk,dj)
+    uint32_t live[4];      // live tasks per kk
+    uint32_t pad[3];
 };
 
 struct ExecArgs {
@@ -44,6 +50,8 @@ struct ExecArgs {
     float *c_values, *c_values_t;
     double *c_leaf_sq;
     unsigned long long *counters;
+    int nstages;                 // depth of the shared-memory ring
+    int dbg;                     // tuning aid (SPAMM_EX_DEBUG): 1 = no copies, 2 = no math
 };
 
 __device__ __forceinline__ double ex_row_sq(float4 v)
@@ -66,15 +74,19 @@ __device__ __forceinline__ void mac(float &acc, float a, float b)
 template <bool EXACT, bool FINE>
 __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
 {
-    __shared__ __align__(128) float sA[EX_STAGES][4][SPAMM_REC];
-    __shared__ __align__(128) float sB[EX_STAGES][4][SPAMM_REC];
-    __shared__ StageDesc desc[EX_STAGES];
-    __shared__ __align__(8) uint64_t full_bar[EX_STAGES], empty_bar[EX_STAGES];
+    // dynamic shared memory: nstages x (A block + B block), then descriptors and barriers
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int nstages = g.nstages;
+    unsigned char *sA = smem_raw;
+    unsigned char *sB = smem_raw + (size_t)nstages * EX_BLOCK_BYTES;
+    StageDesc *desc = reinterpret_cast<StageDesc *>(smem_raw + (size_t)nstages * 2 * EX_BLOCK_BYTES);
+    uint64_t *full_bar = reinterpret_cast<uint64_t *>(desc + EX_MAX_STAGES);
+    uint64_t *empty_bar = full_bar + EX_MAX_STAGES;
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
     if (threadIdx.x == 0) {
-        for (int s = 0; s < EX_STAGES; ++s) {
+        for (int s = 0; s < nstages; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], EX_CONSUMERS);
         }
@@ -85,7 +97,7 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
     uint32_t phase = 0;
 
     if (warp == EX_CONSUMERS) {
-        // ============ producer: stream step records, stage leaves with bulk copies ============
+        // ============ producer: stream step records, stage leaf blocks with bulk copies ============
         const int ntiles = g.counts[5];
         const uint32_t *words = reinterpret_cast<const uint32_t *>(g.steps);
         int tile = 0;
@@ -95,7 +107,7 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
             const int beg = g.tile_off[tile], end = g.tile_off[tile + 1];
             int next_tile = 0;
             if (lane == 0) next_tile = (int)atomicAdd(g.tile_counter, 1u);   // its latency hides behind this tile
-            // lane l < 16 holds word l of a record: 0 k, 1 flags, 2 c_base, 3 tile, 4-7 a_slot, 8-11 b_slot, 12 present
+            // lane l < 16 holds word l of a record (struct spamm_step)
             uint32_t w[EX_PREFETCH];
 #pragma unroll
             for (int x = 0; x < EX_PREFETCH; ++x)
@@ -106,33 +118,27 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
                 for (int x = 0; x + 1 < EX_PREFETCH; ++x) w[x] = w[x + 1];
                 w[EX_PREFETCH - 1] =
                     (lane < 16 && r + EX_PREFETCH < end) ? __ldg(words + (size_t)(r + EX_PREFETCH) * 16 + lane) : 0u;
-                const uint32_t flags = __shfl_sync(FULL_MASK, cur, 1);
-                const uint32_t live = flags & SPAMM_STEP_LIVE;
+                const uint32_t na = __popc(__shfl_sync(FULL_MASK, cur, 5));
+                const uint32_t nb = __popc(__shfl_sync(FULL_MASK, cur, 7));
                 mbar_wait(&empty_bar[stage], phase ^ 1u);
-                if (lane == 1) desc[stage].flags = cur;
-                if (lane == 2) desc[stage].c_base = cur;
-                if (lane == 12) desc[stage].present = cur;
-                uint32_t need = 0;
-#pragma unroll
-                for (int d = 0; d < 4; ++d) {
-                    need += (live & step_rowmask(d)) ? 1u : 0u;
-                    need += (live & step_colmask(d)) ? 1u : 0u;
-                }
+                uint32_t *d = reinterpret_cast<uint32_t *>(&desc[stage]);
+                if (lane == 1) d[0] = cur;                       // flags
+                if (lane == 2) d[1] = cur;                       // c_base
+                if (lane == 12) d[2] = cur;                      // present
+                if (lane == 5) d[3] = cur;                       // a_present
+                if (lane == 7) d[4] = cur;                       // b_present
+                if (lane >= 8 && lane < 12) d[5 + lane - 8] = cur;   // live[kk]
                 __syncwarp();
-                if (lane == 0) mbar_arrive_expect_tx(&full_bar[stage], need * SPAMM_REC_BYTES);
+                const bool copy = !(g.dbg & 1);
+                if (lane == 0) mbar_arrive_expect_tx(&full_bar[stage], copy ? (na + nb) * SPAMM_REC_BYTES : 0u);
                 __syncwarp();
-                if (lane >= 4 && lane < 8) {
-                    const int d = lane - 4;
-                    if (live & step_rowmask(d))
-                        bulk_copy_g2s(&sA[stage][d][0], g.a_values_t + (size_t)cur * SPAMM_REC, SPAMM_REC_BYTES,
-                                      &full_bar[stage]);
-                } else if (lane >= 8 && lane < 12) {
-                    const int d = lane - 8;
-                    if (live & step_colmask(d))
-                        bulk_copy_g2s(&sB[stage][d][0], g.b_values + (size_t)cur * SPAMM_REC, SPAMM_REC_BYTES,
-                                      &full_bar[stage]);
-                }
-                if (++stage == EX_STAGES) { stage = 0; phase ^= 1u; }
+                if (copy && lane == 4)
+                    bulk_copy_g2s(sA + (size_t)stage * EX_BLOCK_BYTES, g.a_values_t + (size_t)cur * SPAMM_REC,
+                                  na * SPAMM_REC_BYTES, &full_bar[stage]);
+                if (copy && lane == 6)
+                    bulk_copy_g2s(sB + (size_t)stage * EX_BLOCK_BYTES, g.b_values + (size_t)cur * SPAMM_REC,
+                                  nb * SPAMM_REC_BYTES, &full_bar[stage]);
+                if (++stage == nstages) { stage = 0; phase ^= 1u; }
             }
             tile = __shfl_sync(FULL_MASK, next_tile, 0);
         }
@@ -152,7 +158,8 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
     float acc[4][4];
     for (;;) {
         mbar_wait(&full_bar[stage], phase);
-        const uint32_t flags = desc[stage].flags;
+        const StageDesc &ds = desc[stage];
+        const uint32_t flags = ds.flags;
         if (flags & EX_EXIT) break;
         if (flags & STEP_FIRST) {
 #pragma unroll
@@ -160,16 +167,22 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
         }
-        const uint32_t live = flags & SPAMM_STEP_LIVE;
-        if ((live >> (2 * warp)) & 3u) {
+        const uint32_t a_present = ds.a_present, b_present = ds.b_present;
+        const float *Ablk = reinterpret_cast<const float *>(sA + (size_t)stage * EX_BLOCK_BYTES);
+        const float *Bblk = reinterpret_cast<const float *>(sB + (size_t)stage * EX_BLOCK_BYTES);
+#pragma unroll 1
+        for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t live = ds.live[kk];
+            if (!((live >> (2 * warp)) & 3u) || (g.dbg & 2)) continue;
             const bool mine = (live >> mypos) & 1u;
-            const float *As = &sA[stage][di][0];
-            const float *Bs = &sB[stage][dj][0];
+            // leaf (r,c) of a block sits at index popc(present & below(morton4(r,c)))
+            const float *As = Ablk + __popc(a_present & ((1u << step_pos(di, kk)) - 1u)) * SPAMM_REC;
+            const float *Bs = Bblk + __popc(b_present & ((1u << step_pos(kk, dj)) - 1u)) * SPAMM_REC;
             uint32_t on = 0;       // bit r: micro product (p,q,r) of my task runs
             if (FINE) {
-                const float4 sa = *reinterpret_cast<const float4 *>(As + 256 + 4 * p);   // subA[p][0..3]
-                const float4 sb = *reinterpret_cast<const float4 *>(Bs + 256 + 4 * q);   // subB[0..3][q]
                 if (mine) {
+                    const float4 sa = *reinterpret_cast<const float4 *>(As + 256 + 4 * p);   // subA[p][0..3]
+                    const float4 sb = *reinterpret_cast<const float4 *>(Bs + 256 + 4 * q);   // subB[0..3][q]
                     on |= (__dmul_rn((double)sa.x, (double)sb.x) >= g.tau) ? 1u : 0u;
                     on |= (__dmul_rn((double)sa.y, (double)sb.y) >= g.tau) ? 2u : 0u;
                     on |= (__dmul_rn((double)sa.z, (double)sb.z) >= g.tau) ? 4u : 0u;
@@ -183,17 +196,17 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
             for (int r = 0; r < 4; ++r) {
                 const bool go = (on >> r) & 1u;
                 if (!__any_sync(FULL_MASK, go)) continue;
-                float4 a[4], b[4];
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    a[kk] = *reinterpret_cast<const float4 *>(As + (4 * r + kk) * 16 + 4 * p);
-                    b[kk] = *reinterpret_cast<const float4 *>(Bs + (4 * r + kk) * 16 + 4 * q);
-                }
                 if (go) {
+                    float4 a[4], b[4];
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const float av[4] = {a[kk].x, a[kk].y, a[kk].z, a[kk].w};
-                        const float bv[4] = {b[kk].x, b[kk].y, b[kk].z, b[kk].w};
+                    for (int x = 0; x < 4; ++x) {
+                        a[x] = *reinterpret_cast<const float4 *>(As + (4 * r + x) * 16 + 4 * p);
+                        b[x] = *reinterpret_cast<const float4 *>(Bs + (4 * r + x) * 16 + 4 * q);
+                    }
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const float av[4] = {a[x].x, a[x].y, a[x].z, a[x].w};
+                        const float bv[4] = {b[x].x, b[x].y, b[x].z, b[x].w};
 #pragma unroll
                         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -204,12 +217,12 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
         }
         uint32_t c_base = 0, present = 0;
         if (flags & STEP_LAST) {
-            c_base = desc[stage].c_base;
-            present = desc[stage].present;
+            c_base = ds.c_base;
+            present = ds.present;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[stage]);
-        if (++stage == EX_STAGES) { stage = 0; phase ^= 1u; }
+        if (++stage == nstages) { stage = 0; phase ^= 1u; }
         if (!(flags & STEP_LAST)) continue;
 
         // epilogue of the super-tile: alpha scaling (numeric.py:273-275), both leaf layouts with
@@ -254,6 +267,19 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
     }
 }
 
+struct ExecTuning { int stages, ctas_per_sm, dbg; };
+static ExecTuning exec_tuning()
+{
+    ExecTuning t{3, 2, 0};
+    if (const char *e = getenv("SPAMM_EX_STAGES")) t.stages = atoi(e);
+    if (const char *e = getenv("SPAMM_EX_CTAS")) t.ctas_per_sm = atoi(e);
+    if (const char *e = getenv("SPAMM_EX_DEBUG")) t.dbg = atoi(e);
+    if (t.stages < 2) t.stages = 2;
+    if (t.stages > EX_MAX_STAGES) t.stages = EX_MAX_STAGES;
+    if (t.ctas_per_sm < 1) t.ctas_per_sm = 1;
+    return t;
+}
+
 extern "C" int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b, const spamm_plan_buffers *plan,
                              int64_t nsteps, int64_t nC, double tau, float alpha, int granularity, int exact,
                              float *c_values, float *c_values_t, double *c_leaf_sq, unsigned long long *counters,
@@ -278,15 +304,16 @@ extern "C" int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b,
     g.c_leaf_sq = c_leaf_sq;
     g.counters = counters;
     if (cudaMemsetAsync(plan->counts + 1, 0, sizeof(int32_t), st) != cudaSuccess) return SPAMM_ECUDA;
-    const int grid = SPAMM_NUM_SMS * 2;
+    static const ExecTuning tune = exec_tuning();
+    g.nstages = tune.stages;
+    g.dbg = tune.dbg;
+    const int grid = SPAMM_NUM_SMS * tune.ctas_per_sm;
+    const size_t smem = (size_t)tune.stages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16);
     const bool fine = granularity == SPAMM_FINE4;
-    if (exact) {
-        if (fine) execute_kernel<true, true><<<grid, EX_THREADS, 0, st>>>(g);
-        else execute_kernel<true, false><<<grid, EX_THREADS, 0, st>>>(g);
-    } else {
-        if (fine) execute_kernel<false, true><<<grid, EX_THREADS, 0, st>>>(g);
-        else execute_kernel<false, false><<<grid, EX_THREADS, 0, st>>>(g);
-    }
+    void (*kern)(ExecArgs) = exact ? (fine ? execute_kernel<true, true> : execute_kernel<true, false>)
+                                   : (fine ? execute_kernel<false, true> : execute_kernel<false, false>);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return SPAMM_ECUDA;
+    kern<<<grid, EX_THREADS, smem, st>>>(g);
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
 }

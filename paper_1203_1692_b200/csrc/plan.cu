@@ -15,8 +15,8 @@
 //
 // The walk stops two levels above the leaves: a node there is a 4x4 super-tile of product
 // leaves, the unit of work of the numeric kernel.  The last kernel tests the leaf norms of every
-// candidate k directly and emits, per super-tile and in ascending k, one 64-byte STEP record
-//   (k, 16 live bits = the tasks (4I+di, k, 4J+dj) that survive, the A and B leaf slots)
+// block product (I,K,J) directly (four k per block) and emits, per super-tile and in ascending K, one 64-byte STEP record
+//   (K, 4 x 16 live bits = the tasks (4I+di, 4K+kk, 4J+dj) that survive, where the two leaf blocks sit)
 // so the compacted task list comes out already in the order and grouping the numeric phase
 // consumes: ascending k per product leaf (numeric.py:203-217), leaves in Morton order.
 #include "common.cuh"
@@ -242,7 +242,7 @@ struct TileArgs {
     const int32_t *slot_a;    // leaf slots of A (i,k)
     const int32_t *slot_bt;   // leaf slots of B transposed (j,k)
     int L;                    // leaf grid side
-    int sub;                  // leaves per super-tile side: 4 (2 or 1 for depth 1 or 0)
+    int sub;                  // leaves per block side: 4 (2 or 1 for depth 1 or 0)
     int row0, row1;
     double tau;
     LevelBuf in;
@@ -251,31 +251,40 @@ struct TileArgs {
     uint32_t *c_keys;
     int32_t *tile_off;
     int64_t cap_steps, cap_leaves;
-    int32_t *counts;          // plan counts: [0] nC, [1] T, [2] overflow, [3] max list, [4] steps
+    int32_t *counts;          // plan counts, see spamm_b200.h
     unsigned int *tile_counter;
     volatile unsigned long long *tile_state;
 };
 
-// live bits of candidate k of super-tile (I,J): bit pos(di,dj) for every surviving leaf task
-__device__ __forceinline__ uint32_t tile_tests(const TileArgs &a, uint32_t I, uint32_t J, uint32_t k, uint32_t rowok)
+// One lane looks at one k = sub*K + kk of block product (I,K,J): the 16 leaf tests, and which
+// leaves of the A column / B row at this k are stored.
+struct LaneTests {
+    uint32_t live;       // bit morton4(di,dj): task (sub*I+di, k, sub*J+dj) survives
+    uint32_t a_here;     // bit di: leaf A(sub*I+di, k) stored
+    uint32_t b_here;     // bit dj: leaf B(k, sub*J+dj) stored
+};
+
+__device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, uint32_t I, uint32_t J, uint32_t k, uint32_t rowok)
 {
     float na[4], nb[4];
+    LaneTests t{0u, 0u, 0u};
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
         na[d] = -1.0f;
         nb[d] = -1.0f;
         if (d < a.sub) {
-            if (rowok >> d & 1u) na[d] = __ldg(a.norm_a + (int64_t)(a.sub * I + d) * a.L + k);
+            na[d] = __ldg(a.norm_a + (int64_t)(a.sub * I + d) * a.L + k);
             nb[d] = __ldg(a.norm_bt + (int64_t)(a.sub * J + d) * a.L + k);
         }
+        t.a_here |= (na[d] >= 0.0f) ? (1u << d) : 0u;
+        t.b_here |= (nb[d] >= 0.0f) ? (1u << d) : 0u;
     }
-    uint32_t live = 0;
 #pragma unroll
     for (int di = 0; di < 4; ++di)
 #pragma unroll
         for (int dj = 0; dj < 4; ++dj)
-            if (norm_test(na[di], nb[dj], a.tau)) live |= 1u << step_pos(di, dj);
-    return live;
+            if ((rowok >> di & 1u) && norm_test(na[di], nb[dj], a.tau)) t.live |= 1u << step_pos(di, dj);
+    return t;
 }
 
 __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
@@ -287,7 +296,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
     const uint32_t lane = lane_id();
     const int n_nodes = a.counts_in[0];
     const int ntiles = (n_nodes + PLAN_WARPS - 1) / PLAN_WARPS;
-    const int sub = a.sub, per = 32 / sub;       // candidates per parent entry, parent entries per warp pass
+    const int sub = a.sub, per = 32 / sub;       // lanes per block product, block products per warp pass
+    const uint32_t kk = lane % sub;              // my k inside the block
+    const uint32_t grp = (lane / sub) * sub;     // first lane of my group
     unsigned long long tasks_total = 0;
     for (;;) {
         __syncthreads();
@@ -309,13 +320,19 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
                 if (row >= a.row0 && row < a.row1) rowok |= 1u << d;
             }
         }
-        // phase 1: count steps and product leaves of this super-tile
+        // phase 1: count step records and product leaves of this super-tile
         uint32_t nsteps = 0, present = 0, ntasks = 0;
         for (int b = s; b < e; b += per) {
             const int t = b + (int)lane / sub;
             uint32_t live = 0;
-            if (t < e) live = tile_tests(a, I, J, sub * a.in.ks[t] + (lane % sub), rowok);
-            nsteps += __popc(__ballot_sync(FULL_MASK, live != 0));
+            if (t < e) live = tile_tests(a, I, J, sub * a.in.ks[t] + kk, rowok).live;
+            const uint32_t bal = __ballot_sync(FULL_MASK, live != 0);
+            // one record per group of `sub` lanes with any live task
+            uint32_t groups = bal;
+            if (sub >= 2) groups |= groups >> 1;
+            if (sub >= 4) groups |= groups >> 2;
+            groups &= (sub == 4 ? 0x11111111u : sub == 2 ? 0x55555555u : 0xFFFFFFFFu);
+            nsteps += __popc(groups);
             present |= live;
             ntasks += __popc(live);
         }
@@ -324,7 +341,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
         const uint32_t nleaves = __popc(present);
         if (lane == 0) { s_wsteps[warp] = nsteps; s_wleaves[warp] = nleaves; tasks_total += ntasks; }
         __syncthreads();
-        // phase 2: block scan + look-back over (steps, product leaves)
+        // phase 2: block scan + look-back over (records, product leaves)
         if (threadIdx.x == 0) {
             uint32_t rs = 0, rl = 0;
             for (int w = 0; w < PLAN_WARPS; ++w) {
@@ -348,7 +365,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
         __syncthreads();
         if (valid && lane == 0) a.tile_off[pidx] = (int32_t)(s_base_lo + s_wsteps[warp]);
         if (!valid || nsteps == 0) continue;
-        // phase 3: product leaf keys and step records, in ascending k
+        // phase 3: product leaf keys and step records, in ascending K
         int64_t sb = (int64_t)s_base_lo + s_wsteps[warp];
         const int64_t cb = (int64_t)s_base_hi + s_wleaves[warp];
         if (sb + nsteps > a.cap_steps || cb + nleaves > a.cap_leaves) {
@@ -359,32 +376,55 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
             a.c_keys[cb + __popc(present & ((1u << lane) - 1u))] = pm * (uint32_t)(sub * sub) + lane;
         const int64_t s_first = sb, s_last = sb + nsteps - 1;
         const uint32_t lt = lanemask_lt();
+        const uint32_t lead_mask = (sub == 4 ? 0x11111111u : sub == 2 ? 0x55555555u : 0xFFFFFFFFu);
         for (int b = s; b < e; b += per) {
             const int t = b + (int)lane / sub;
-            uint32_t live = 0, k = 0;
+            LaneTests lt4{0u, 0u, 0u};
+            uint32_t K = 0, k = 0;
             if (t < e) {
-                k = sub * a.in.ks[t] + (lane % sub);
-                live = tile_tests(a, I, J, k, rowok);
+                K = a.in.ks[t];
+                k = sub * K + kk;
+                lt4 = tile_tests(a, I, J, k, rowok);
             }
-            const uint32_t bal = __ballot_sync(FULL_MASK, live != 0);
-            if (live) {
+            // gather the group's four lanes: live per kk, stored leaves of both blocks
+            uint32_t live4[4] = {0, 0, 0, 0}, a_present = 0, b_present = 0, any = 0;
+            // first stored leaf of each block in Morton order and the lane that knows its slot
+            int a_best = 16, b_best = 16;
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const int src = (int)grp + (x < sub ? x : 0);
+                const uint32_t lv = __shfl_sync(FULL_MASK, lt4.live, src);
+                const uint32_t ah = __shfl_sync(FULL_MASK, lt4.a_here, src);
+                const uint32_t bh = __shfl_sync(FULL_MASK, lt4.b_here, src);
+                if (x < sub) {
+                    live4[x] = lv;
+                    any |= lv;
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) {
+                        if (ah >> d & 1u) { a_present |= 1u << step_pos(d, x); }     // A leaf (di=d, kk=x)
+                        if (bh >> d & 1u) { b_present |= 1u << step_pos(x, d); }     // B leaf (kk=x, dj=d)
+                    }
+                }
+            }
+            if (a_present) a_best = __ffs(a_present) - 1;
+            if (b_present) b_best = __ffs(b_present) - 1;
+            const uint32_t bal = __ballot_sync(FULL_MASK, any != 0 && lane == grp);
+            if (any != 0 && lane == grp) {
                 const int64_t x = sb + __popc(bal & lt);
-                uint32_t flags = live;
+                uint32_t flags = 0;
                 if (x == s_first) flags |= STEP_FIRST;
                 if (x == s_last) flags |= STEP_LAST;
-                uint32_t sa[4], sbb[4];
-#pragma unroll
-                for (int d = 0; d < 4; ++d) {
-                    sa[d] = (live & step_rowmask(d)) ? (uint32_t)__ldg(a.slot_a + (int64_t)(sub * I + d) * a.L + k) : 0u;
-                    sbb[d] = (live & step_colmask(d)) ? (uint32_t)__ldg(a.slot_bt + (int64_t)(sub * J + d) * a.L + k) : 0u;
-                }
+                const uint32_t a_first = (uint32_t)__ldg(
+                    a.slot_a + (int64_t)(sub * I + step_pos_di(a_best)) * a.L + (sub * K + step_pos_dj(a_best)));
+                const uint32_t b_first = (uint32_t)__ldg(
+                    a.slot_bt + (int64_t)(sub * J + step_pos_dj(b_best)) * a.L + (sub * K + step_pos_di(b_best)));
                 uint4 *rec = reinterpret_cast<uint4 *>(a.steps + x);
-                rec[0] = make_uint4(k, flags, (uint32_t)cb, pm);
-                rec[1] = make_uint4(sa[0], sa[1], sa[2], sa[3]);
-                rec[2] = make_uint4(sbb[0], sbb[1], sbb[2], sbb[3]);
+                rec[0] = make_uint4(K, flags, (uint32_t)cb, pm);
+                rec[1] = make_uint4(a_first, a_present, b_first, b_present);
+                rec[2] = make_uint4(live4[0], live4[1], live4[2], live4[3]);
                 rec[3] = make_uint4(present, 0u, 0u, 0u);
             }
-            sb += __popc(bal);
+            sb += __popc(bal & lead_mask);
         }
     }
     if (lane == 0 && tasks_total) atomicAdd(reinterpret_cast<unsigned long long *>(a.counts + 6), tasks_total);

@@ -82,14 +82,14 @@ class MultiplyPlan:
             return self._ikj
         rec = self.step_records()
         sub_shift = min(2, self.depth)               # super-tiles are 4x4 leaves (2x2, 1x1 for tiny trees)
-        k = rec[:, 0].astype(np.int64)
-        live = rec[:, 1].astype(np.int64) & 0xFFFF
+        kblock = rec[:, 0].astype(np.int64)
+        live = rec[:, 8:12].astype(np.int64) & 0xFFFF                     # (steps, kk)
         ti, tj = morton.decode_array(rec[:, 3].astype(np.uint64))
-        bits = (live[:, None] >> np.arange(16)[None, :]) & 1
-        s_idx, pos = np.nonzero(bits)
+        bits = (live[:, :, None] >> np.arange(16)[None, None, :]) & 1
+        s_idx, kk, pos = np.nonzero(bits)
         i = (ti[s_idx].astype(np.int64) << sub_shift) + _POS_DI[pos]
         j = (tj[s_idx].astype(np.int64) << sub_shift) + _POS_DJ[pos]
-        t = np.stack([i, k[s_idx], j], axis=1)
+        t = np.stack([i, (kblock[s_idx] << sub_shift) + kk, j], axis=1)
         ck = morton.encode_array(t[:, 0], t[:, 2])
         order = np.lexsort((t[:, 1], ck))
         self._ikj = t[order]
