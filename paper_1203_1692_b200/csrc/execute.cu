@@ -64,11 +64,18 @@ __device__ __forceinline__ double ex_row_sq(float4 v)
     return r;
 }
 
+// Two C elements of one column (rows 2h, 2h+1) advance together: packed FP32 (sm_100 FFMA2 with a
+// broadcast scalar operand) halves the issue slots the multiply-accumulates take.  EXACT rounds the
+// product and the sum separately (numeric.py:252-259), FMUL2 + FADD2.
 template <bool EXACT>
-__device__ __forceinline__ void mac(float &acc, float a, float b)
+__device__ __forceinline__ void mac2(float2 &acc, float2 a, float b)
 {
-    if (EXACT) acc = __fadd_rn(acc, __fmul_rn(a, b));   // numeric.py:252-259: two roundings
-    else acc = fmaf(a, b, acc);
+    if (EXACT) {   // scalar: nvcc 12.9 contracts __fmul2_rn + __fadd2_rn into one FFMA2
+        acc.x = __fadd_rn(acc.x, __fmul_rn(a.x, b));
+        acc.y = __fadd_rn(acc.y, __fmul_rn(a.y, b));
+    } else {
+        acc = __ffma2_rn(a, make_float2(b, b), acc);
+    }
 }
 
 template <bool EXACT, bool FINE>
@@ -155,7 +162,7 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
     const int mypos = 2 * warp + half;
     const int di = step_pos_di(mypos), dj = step_pos_dj(mypos);
     uint32_t executed = 0;
-    float acc[4][4];
+    float2 acc2[2][4];     // acc2[h][j] = C sub-block elements (2h, j) and (2h+1, j)
     for (;;) {
         mbar_wait(&full_bar[stage], phase);
         const StageDesc &ds = desc[stage];
@@ -163,9 +170,9 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
         if (flags & EX_EXIT) break;
         if (flags & STEP_FIRST) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+                for (int j = 0; j < 4; ++j) acc2[h][j] = make_float2(0.0f, 0.0f);
         }
         const uint32_t a_present = ds.a_present, b_present = ds.b_present;
         const float *Ablk = reinterpret_cast<const float *>(sA + (size_t)stage * EX_BLOCK_BYTES);
@@ -205,12 +212,13 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
                     }
 #pragma unroll
                     for (int x = 0; x < 4; ++x) {
-                        const float av[4] = {a[x].x, a[x].y, a[x].z, a[x].w};
+                        const float2 a01 = make_float2(a[x].x, a[x].y), a23 = make_float2(a[x].z, a[x].w);
                         const float bv[4] = {b[x].x, b[x].y, b[x].z, b[x].w};
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) mac<EXACT>(acc[i][j], av[i], bv[j]);
+                        for (int j = 0; j < 4; ++j) {
+                            mac2<EXACT>(acc2[0][j], a01, bv[j]);
+                            mac2<EXACT>(acc2[1][j], a23, bv[j]);
+                        }
                     }
                 }
             }
@@ -229,6 +237,12 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
         // their sub-norm tails, leaf square sum in compute_norms order (core.py:108-116)
         const bool exists = (present >> mypos) & 1u;
         const int64_t cslot = (int64_t)c_base + __popc(present & ((1u << mypos) - 1u));
+        float acc[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            acc[0][j] = acc2[0][j].x; acc[1][j] = acc2[0][j].y;
+            acc[2][j] = acc2[1][j].x; acc[3][j] = acc2[1][j].y;
+        }
         float4 rows[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
