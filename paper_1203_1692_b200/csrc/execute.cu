@@ -79,7 +79,10 @@ __device__ __forceinline__ void mac2(float2 &acc, float2 a, float b)
 }
 
 template <bool EXACT, bool FINE>
-__global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
+#ifndef EX_MIN_BLOCKS
+#define EX_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(ExecArgs g)
 {
     // dynamic shared memory: nstages x (A block + B block), then descriptors and barriers
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -205,7 +208,34 @@ __global__ void __launch_bounds__(EX_THREADS, 2) execute_kernel(ExecArgs g)
             } else {
                 on = mine ? 15u : 0u;
             }
+            // Fast path (the common case away from the band edge): every lane runs all four r or
+            // none, so the 16 k of the task form one branch-free block and the compiler overlaps the
+            // shared-memory reads of r+1 with the multiplies of r.
+            if (__all_sync(FULL_MASK, on == 15u || on == 0u)) {
+                if (on) {
 #pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        float4 a[4], b[4];
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) {
+                            a[x] = *reinterpret_cast<const float4 *>(As + (4 * r + x) * 16 + 4 * p);
+                            b[x] = *reinterpret_cast<const float4 *>(Bs + (4 * r + x) * 16 + 4 * q);
+                        }
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) {
+                            const float2 a01 = make_float2(a[x].x, a[x].y), a23 = make_float2(a[x].z, a[x].w);
+                            const float bv[4] = {b[x].x, b[x].y, b[x].z, b[x].w};
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                mac2<EXACT>(acc2[0][j], a01, bv[j]);
+                                mac2<EXACT>(acc2[1][j], a23, bv[j]);
+                            }
+                        }
+                    }
+                }
+                continue;
+            }
+#pragma unroll 1
             for (int r = 0; r < 4; ++r) {
                 const bool go = (on >> r) & 1u;
                 if (!__any_sync(FULL_MASK, go)) continue;
