@@ -152,6 +152,7 @@ typedef struct {
     spamm_step *steps;       /* [step_capacity]                                   */
     uint32_t *c_keys;        /* [leaf_capacity] product leaf keys, ascending      */
     int32_t *tile_off;       /* [leaf_capacity + 1] first step of each super-tile node */
+    int32_t *tile_order;     /* [leaf_capacity] super-tile nodes, most step records first */
     int64_t step_capacity;
     int64_t leaf_capacity;
     int32_t *counts;         /* [SPAMM_PLAN_COUNTS]                               */

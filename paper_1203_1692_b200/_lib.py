@@ -30,8 +30,8 @@ class TreeView(C.Structure):
 class PlanBuffers(C.Structure):
     """``spamm_plan_buffers``."""
 
-    _fields_ = [("steps", vp), ("c_keys", vp), ("tile_off", vp), ("step_capacity", i64), ("leaf_capacity", i64),
-                ("counts", vp)]
+    _fields_ = [("steps", vp), ("c_keys", vp), ("tile_off", vp), ("tile_order", vp), ("step_capacity", i64),
+                ("leaf_capacity", i64), ("counts", vp)]
 
 
 REC = 272           # floats per stored leaf record: 256 values + 16 sub-block norms

@@ -42,6 +42,7 @@ struct ExecArgs {
     const float *b_values;
     const spamm_step *steps;
     const int32_t *tile_off;     // step offset of every super-tile node, one extra entry
+    const int32_t *tile_order;   // super-tile nodes, longest first
     const int32_t *counts;       // plan counts (device): [5] = number of super-tile nodes
     unsigned int *tile_counter;
     double tau;
@@ -114,7 +115,8 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
         if (lane == 0) tile = (int)atomicAdd(g.tile_counter, 1u);
         tile = __shfl_sync(FULL_MASK, tile, 0);
         while (tile < ntiles) {
-            const int beg = g.tile_off[tile], end = g.tile_off[tile + 1];
+            const int node = g.tile_order[tile];
+            const int beg = g.tile_off[node], end = g.tile_off[node + 1];
             int next_tile = 0;
             if (lane == 0) next_tile = (int)atomicAdd(g.tile_counter, 1u);   // its latency hides behind this tile
             // lane l < 16 holds word l of a record (struct spamm_step)
@@ -345,6 +347,7 @@ extern "C" int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b,
     g.b_values = b->values;
     g.steps = plan->steps;
     g.tile_off = plan->tile_off;
+    g.tile_order = plan->tile_order;
     g.counts = plan->counts;
     g.tile_counter = reinterpret_cast<unsigned int *>(plan->counts + 1);
     g.tau = tau;

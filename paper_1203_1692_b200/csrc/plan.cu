@@ -32,9 +32,13 @@ struct LevelBuf {
     uint32_t *ks;     // contraction indices
 };
 
+#define PLAN_BINS 1024       // super-tiles are binned by their number of step records
+
 struct PlanShared {      // lives at the start of the workspace, zeroed once per plan
     unsigned int tile_counter[PLAN_MAX_LEVELS + 1];
     int32_t counts[PLAN_MAX_LEVELS + 1][2];   // (nodes, candidates) per level
+    unsigned int bins[PLAN_BINS];             // histogram of super-tile sizes
+    unsigned int cursor[PLAN_BINS];
 };
 
 // ---- start level: dense enumeration by one block ---------------------------------------
@@ -250,6 +254,7 @@ struct TileArgs {
     spamm_step *steps;
     uint32_t *c_keys;
     int32_t *tile_off;
+    unsigned int *bins;
     int64_t cap_steps, cap_leaves;
     int32_t *counts;          // plan counts, see spamm_b200.h
     unsigned int *tile_counter;
@@ -339,7 +344,10 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
         present = __reduce_or_sync(FULL_MASK, present);
         ntasks = __reduce_add_sync(FULL_MASK, ntasks);
         const uint32_t nleaves = __popc(present);
-        if (lane == 0) { s_wsteps[warp] = nsteps; s_wleaves[warp] = nleaves; tasks_total += ntasks; }
+        if (lane == 0) {
+            s_wsteps[warp] = nsteps; s_wleaves[warp] = nleaves; tasks_total += ntasks;
+            if (valid) atomicAdd(&a.bins[nsteps < PLAN_BINS ? nsteps : PLAN_BINS - 1], 1u);
+        }
         __syncthreads();
         // phase 2: block scan + look-back over (records, product leaves)
         if (threadIdx.x == 0) {
@@ -428,6 +436,48 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
         }
     }
     if (lane == 0 && tasks_total) atomicAdd(reinterpret_cast<unsigned long long *>(a.counts + 6), tasks_total);
+}
+
+// Longest-first order of the super-tiles for the numeric kernel's dynamic scheduler: a counting
+// sort by step count (any order inside a bin; the product does not depend on it).
+__global__ void __launch_bounds__(256) plan_order_kernel(const int32_t *__restrict__ tile_off, const int32_t *counts,
+                                                         const unsigned int *__restrict__ bins, unsigned int *cursor,
+                                                         int32_t *__restrict__ tile_order)
+{
+    __shared__ unsigned int s_start[PLAN_BINS];
+    __shared__ unsigned int s_part[256];
+    // exclusive scan of the bins in DESCENDING size order: 4 bins per thread
+    const int t = threadIdx.x;
+    unsigned int v[4], sum = 0;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+        v[x] = bins[PLAN_BINS - 1 - (4 * t + x)];
+        sum += v[x];
+    }
+    s_part[t] = sum;
+    __syncthreads();
+    if (t == 0) {
+        unsigned int run = 0;
+        for (int x = 0; x < 256; ++x) {
+            const unsigned int y = s_part[x];
+            s_part[x] = run;
+            run += y;
+        }
+    }
+    __syncthreads();
+    unsigned int run = s_part[t];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+        s_start[PLAN_BINS - 1 - (4 * t + x)] = run;
+        run += v[x];
+    }
+    __syncthreads();
+    const int n_nodes = counts[5];
+    for (int idx = blockIdx.x * blockDim.x + t; idx < n_nodes; idx += gridDim.x * blockDim.x) {
+        int ns = tile_off[idx + 1] - tile_off[idx];
+        if (ns >= PLAN_BINS) ns = PLAN_BINS - 1;
+        tile_order[s_start[ns] + atomicAdd(&cursor[ns], 1u)] = idx;
+    }
 }
 
 // ---- host side ---------------------------------------------------------------------------------
@@ -528,11 +578,15 @@ extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, do
     t.steps = out->steps;
     t.c_keys = out->c_keys;
     t.tile_off = out->tile_off;
+    t.bins = w.shared->bins;
     t.cap_steps = out->step_capacity; t.cap_leaves = out->leaf_capacity;
     t.counts = out->counts;
     t.tile_counter = &w.shared->tile_counter[PLAN_MAX_LEVELS];
     t.tile_state = w.tile_state[PLAN_MAX_LEVELS];
     plan_tiles_kernel<<<grid, PLAN_THREADS, 0, st>>>(t);
+    SPAMM_CHECK_LAUNCH();
+    plan_order_kernel<<<SPAMM_NUM_SMS, 256, 0, st>>>(out->tile_off, out->counts, w.shared->bins, w.shared->cursor,
+                                                     out->tile_order);
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
 }

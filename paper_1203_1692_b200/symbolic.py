@@ -47,13 +47,14 @@ class MultiplyPlan:
     ``len(plan)`` is the task count; ``plan.tasks`` builds the reference's host list on demand.
     """
 
-    def __init__(self, tau, depth, n_tasks, n_cleaves, n_steps, steps, c_keys, tile_off, counts, a, b, row_range):
+    def __init__(self, tau, depth, n_tasks, n_cleaves, n_steps, steps, c_keys, tile_off, tile_order, counts, a, b,
+                 row_range):
         self.tau = float(tau)
         self.depth = depth
         self.n_tasks = int(n_tasks)
         self.n_cleaves = int(n_cleaves)
         self.n_steps = int(n_steps)
-        self.steps, self.c_keys, self.tile_off, self.counts = steps, c_keys, tile_off, counts
+        self.steps, self.c_keys, self.tile_off, self.tile_order, self.counts = steps, c_keys, tile_off, tile_order, counts
         self._a, self._b = a, b
         self._tokens = (id(a), a._rev, id(b), b._rev)
         self.row_range = row_range
@@ -66,7 +67,8 @@ class MultiplyPlan:
 
     def buffers(self) -> _lib.PlanBuffers:
         return _lib.PlanBuffers(self.steps.data_ptr(), self.c_keys.data_ptr(), self.tile_off.data_ptr(),
-                                self.steps.shape[0], self.c_keys.shape[0], self.counts.data_ptr())
+                                self.tile_order.data_ptr(), self.steps.shape[0], self.c_keys.shape[0],
+                                self.counts.data_ptr())
 
     # -- host views ---------------------------------------------------------------------------
     def step_records(self) -> np.ndarray:
@@ -206,7 +208,7 @@ def build_plan(a: QuadtreeMatrix, b: QuadtreeMatrix, tau: float,
     if a.nleaf == 0 or b.nleaf == 0:
         z = torch.zeros((1, _lib.STEP_WORDS), dtype=torch.int32, device=dev)
         e = torch.zeros((_lib.PLAN_COUNTS,), dtype=torch.int32, device=dev)
-        return MultiplyPlan(tau, depth, 0, 0, 0, z, e, e, e, a, b, (r0, r1))
+        return MultiplyPlan(tau, depth, 0, 0, 0, z, e, e, e, e, a, b, (r0, r1))
     va, vb = a.view(depth), b.view(depth)
     hint_key = (depth, a.nleaf, b.nleaf, float(tau), r0, r1)
     step_cap, leaf_cap = _capacity_hint.get(hint_key, (max(4096, 4 * (a.nleaf + b.nleaf)),
@@ -216,11 +218,12 @@ def build_plan(a: QuadtreeMatrix, b: QuadtreeMatrix, tau: float,
         steps = torch.empty((step_cap, _lib.STEP_WORDS), dtype=torch.int32, device=dev)
         c_keys = torch.empty((leaf_cap,), dtype=torch.int32, device=dev)
         tile_off = torch.empty((leaf_cap + 1,), dtype=torch.int32, device=dev)
+        tile_order = torch.empty((leaf_cap,), dtype=torch.int32, device=dev)
         counts = torch.empty((_lib.PLAN_COUNTS,), dtype=torch.int32, device=dev)
         ws_bytes = lib.spamm_plan_workspace_bytes(depth, step_cap, leaf_cap)
         ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
-        bufs = _lib.PlanBuffers(steps.data_ptr(), c_keys.data_ptr(), tile_off.data_ptr(), step_cap, leaf_cap,
-                                counts.data_ptr())
+        bufs = _lib.PlanBuffers(steps.data_ptr(), c_keys.data_ptr(), tile_off.data_ptr(), tile_order.data_ptr(),
+                                step_cap, leaf_cap, counts.data_ptr())
         _lib.check(lib.spamm_plan(C.byref(va), C.byref(vb), float(tau), r0, r1, C.byref(bufs), ws.data_ptr(),
                                   ws_bytes, _stream()), "plan")
         cnt = counts.tolist()
@@ -233,4 +236,4 @@ def build_plan(a: QuadtreeMatrix, b: QuadtreeMatrix, tau: float,
         step_cap = min(max_steps, max(2 * step_cap, int(1.25 * max(max_list, n_steps)) + 1024))
         leaf_cap = min(L * L, max(4 * leaf_cap, int(1.25 * n_c) + 1024))
     _capacity_hint[hint_key] = (step_cap, leaf_cap)
-    return MultiplyPlan(tau, depth, n_t, n_c, n_steps, steps, c_keys, tile_off, counts, a, b, (r0, r1))
+    return MultiplyPlan(tau, depth, n_t, n_c, n_steps, steps, c_keys, tile_off, tile_order, counts, a, b, (r0, r1))
