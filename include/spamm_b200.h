@@ -193,6 +193,33 @@ int spamm_union_leaves(const int32_t *slot_old, const uint32_t *prod_keys, int64
                        int32_t *slot_prod_scratch, uint32_t *out_keys, int32_t *idx_old,
                        int32_t *idx_prod, int32_t *nout_dev, void *ws, size_t ws_bytes, void *stream);
 
+/* ---- one call: multiply (numeric.py:302-313), beta == 0 ---------------------------- */
+
+/* Storage of the product tree, sized by the plan's leaf_capacity (packed arrays) and by the
+ * depth of C (grids and level buffers, see spamm_tree_view). */
+typedef struct {
+    float *values;           /* [leaf_capacity][272] */
+    float *values_t;         /* [leaf_capacity][272] */
+    double *leaf_sq;         /* [leaf_capacity]      */
+    int32_t *slot;           /* [L*L] */
+    int32_t *slot_t;         /* [L*L] */
+    float *norm;             /* level buffer */
+    float *norm_t;           /* level buffer */
+    double *leaf_sq_grid;    /* [L*L] */
+    double *sq_levels;       /* level buffer (scratch) */
+    int32_t depth;
+} spamm_product_buffers;
+
+/* build_plan + execute_plan + compute_norms on C, enqueued back to back on `stream` with no
+ * host synchronisation: C = alpha32 * sum of the surviving leaf products.  The product leaves
+ * are plan->c_keys[0 .. counts[0]) with their records in c->values / c->values_t.  The caller
+ * reads plan->counts when it next synchronises; counts[2] != 0 means a capacity was too small
+ * (nothing was computed) and the call must be repeated with larger buffers. */
+int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
+                   int exact, float alpha, int32_t row0, int32_t row1,
+                   const spamm_plan_buffers *plan, void *plan_ws, size_t plan_ws_bytes,
+                   const spamm_product_buffers *c, unsigned long long *counters, void *stream);
+
 /* _compose with beta != 0 (numeric.py:276-284): out leaf x = (alpha32 * prod[ip]) + (old[io] * beta32)
  * with ip / io = -1 when that side has no leaf; the alpha == 1 / beta == 1 special cases keep
  * the reference's exact expressions. */

@@ -34,6 +34,13 @@ class PlanBuffers(C.Structure):
                 ("leaf_capacity", i64), ("counts", vp)]
 
 
+class ProductBuffers(C.Structure):
+    """``spamm_product_buffers``."""
+
+    _fields_ = [("values", vp), ("values_t", vp), ("leaf_sq", vp), ("slot", vp), ("slot_t", vp), ("norm", vp),
+                ("norm_t", vp), ("leaf_sq_grid", vp), ("sq_levels", vp), ("depth", i32)]
+
+
 REC = 272           # floats per stored leaf record: 256 values + 16 sub-block norms
 STEP_WORDS = 16     # uint32 words per step record (struct spamm_step)
 PLAN_COUNTS = 8
@@ -58,6 +65,8 @@ SIGNATURES = {
                              C.POINTER(PlanBuffers), vp, sz, vp]),
     "spamm_execute": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), C.POINTER(PlanBuffers), i64, i64,
                                 f64, f32, C.c_int, C.c_int, vp, vp, vp, vp, vp]),
+    "spamm_multiply": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, C.c_int, C.c_int, f32, i32, i32,
+                                 C.POINTER(PlanBuffers), vp, sz, C.POINTER(ProductBuffers), vp, vp]),
     "spamm_union_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp, sz, vp]),
     "spamm_compose": (C.c_int, [vp, vp, vp, vp, i64, f32, f32, C.c_int, C.c_int, vp, vp]),
 }

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
 
     if (warp == EX_CONSUMERS) {
         // ============ producer: stream step records, stage leaf blocks with bulk copies ============
-        const int ntiles = g.counts[5];
+        const int ntiles = g.counts[2] ? 0 : g.counts[5];      // an overflowed plan is incomplete: do nothing
         const uint32_t *words = reinterpret_cast<const uint32_t *>(g.steps);
         int tile = 0;
         if (lane == 0) tile = (int)atomicAdd(g.tile_counter, 1u);
@@ -338,9 +338,9 @@ extern "C" int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b,
                              float *c_values, float *c_values_t, double *c_leaf_sq, unsigned long long *counters,
                              void *stream)
 {
-    if (!a || !b || !plan || nsteps < 0 || nC < 0) return SPAMM_EINVAL;
+    if (!a || !b || !plan || nsteps < -1 || nC < -1) return SPAMM_EINVAL;
     if (granularity != SPAMM_FINE4 && granularity != SPAMM_COARSE16) return SPAMM_EINVAL;
-    if (nC == 0 || nsteps == 0) return SPAMM_OK;
+    if (nC == 0 || nsteps == 0) return SPAMM_OK;          // pass -1 when the counts are still on the device
     cudaStream_t st = (cudaStream_t)stream;
     ExecArgs g;
     g.a_values_t = a->values_t;

@@ -356,29 +356,30 @@ __global__ void clear_grids_kernel(int64_t cells, int32_t *slot, int32_t *slot_t
         leaf_sq_grid[x] = 0.0;
     }
 }
+// nleaf_dev (optional): the leaf count still lives on the device; nleaf is then only its upper bound
 __global__ void scatter_leaves_kernel(const uint32_t *__restrict__ keys, const double *__restrict__ leaf_sq_packed,
-                                      int64_t nleaf, int L, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t,
-                                      double *leaf_sq_grid)
+                                      int64_t nleaf, const int32_t *__restrict__ nleaf_dev, int L, int32_t *slot,
+                                      int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid)
 {
-    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= nleaf) return;
-    uint32_t i, j;
-    morton_decode(keys[s], i, j);
-    const double sq = leaf_sq_packed[s];
-    const float nv = (float)sqrt(sq);       // a stored leaf keeps norm 0 when it is all zero (core.py:336-339)
-    slot[(int64_t)i * L + j] = (int32_t)s;
-    slot_t[(int64_t)j * L + i] = (int32_t)s;
-    norm[(int64_t)i * L + j] = nv;
-    norm_t[(int64_t)j * L + i] = nv;
-    leaf_sq_grid[(int64_t)i * L + j] = sq;
+    if (nleaf_dev && (int64_t)*nleaf_dev < nleaf) nleaf = *nleaf_dev;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nleaf; s += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t i, j;
+        morton_decode(keys[s], i, j);
+        const double sq = leaf_sq_packed[s];
+        const float nv = (float)sqrt(sq);       // a stored leaf keeps norm 0 when it is all zero (core.py:336-339)
+        slot[(int64_t)i * L + j] = (int32_t)s;
+        slot_t[(int64_t)j * L + i] = (int32_t)s;
+        norm[(int64_t)i * L + j] = nv;
+        norm_t[(int64_t)j * L + i] = nv;
+        leaf_sq_grid[(int64_t)i * L + j] = sq;
+    }
 }
 
-extern "C" int spamm_index_leaves(const uint32_t *keys, const double *leaf_sq_packed, int64_t nleaf, int depth,
-                                  int32_t *slot, int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid,
-                                  void *stream)
+int spamm_index_leaves_impl(const uint32_t *keys, const double *leaf_sq_packed, int64_t nleaf, const int32_t *nleaf_dev,
+                            int depth, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid,
+                            cudaStream_t st)
 {
     if (depth < 0 || depth > 15 || nleaf < 0) return SPAMM_EINVAL;
-    cudaStream_t st = (cudaStream_t)stream;
     const int L = 1 << depth;
     const int64_t cells = (int64_t)L * L;
     const int64_t off = spamm_level_offset(depth);
@@ -387,11 +388,21 @@ extern "C" int spamm_index_leaves(const uint32_t *keys, const double *leaf_sq_pa
     clear_grids_kernel<<<blocks, 256, 0, st>>>(cells, slot, slot_t, norm + off, norm_t + off, leaf_sq_grid);
     SPAMM_CHECK_LAUNCH();
     if (nleaf > 0) {
-        scatter_leaves_kernel<<<(unsigned)((nleaf + 255) / 256), 256, 0, st>>>(keys, leaf_sq_packed, nleaf, L, slot, slot_t,
-                                                                              norm + off, norm_t + off, leaf_sq_grid);
+        int sb = (int)((nleaf + 255) / 256);
+        if (sb > SPAMM_NUM_SMS * 8) sb = SPAMM_NUM_SMS * 8;
+        scatter_leaves_kernel<<<sb, 256, 0, st>>>(keys, leaf_sq_packed, nleaf, nleaf_dev, L, slot, slot_t, norm + off,
+                                                  norm_t + off, leaf_sq_grid);
         SPAMM_CHECK_LAUNCH();
     }
     return SPAMM_OK;
+}
+
+extern "C" int spamm_index_leaves(const uint32_t *keys, const double *leaf_sq_packed, int64_t nleaf, int depth,
+                                  int32_t *slot, int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid,
+                                  void *stream)
+{
+    return spamm_index_leaves_impl(keys, leaf_sq_packed, nleaf, nullptr, depth, slot, slot_t, norm, norm_t, leaf_sq_grid,
+                                   (cudaStream_t)stream);
 }
 
 // QuadtreeMatrix.to_dense (core.py:268-276): one block per 16x16 block of the output.

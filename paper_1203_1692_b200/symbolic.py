@@ -51,9 +51,11 @@ class MultiplyPlan:
                  row_range):
         self.tau = float(tau)
         self.depth = depth
-        self.n_tasks = int(n_tasks)
-        self.n_cleaves = int(n_cleaves)
-        self.n_steps = int(n_steps)
+        # None = still on the device (asynchronous multiply): resolved on first use
+        self._n_tasks = None if n_tasks is None else int(n_tasks)
+        self._n_cleaves = None if n_cleaves is None else int(n_cleaves)
+        self._n_steps = None if n_steps is None else int(n_steps)
+        self._async = None            # set by the asynchronous multiply (numeric._AsyncProduct)
         self.steps, self.c_keys, self.tile_off, self.tile_order, self.counts = steps, c_keys, tile_off, tile_order, counts
         self._a, self._b = a, b
         self._tokens = (id(a), a._rev, id(b), b._rev)
@@ -61,6 +63,40 @@ class MultiplyPlan:
         self._tasks = None
         self._stats = None
         self._ikj = None
+
+    def _resolve(self) -> None:
+        """Read the counts back (one synchronisation); repeat the multiply if a buffer overflowed."""
+        if self._n_tasks is not None:
+            return
+        cnt = self.counts.tolist()
+        if cnt[2] and self._async is not None:
+            self._async.on_overflow(cnt)      # replaces the buffers of this plan (and of C) in place
+            cnt = self.counts.tolist()
+        if cnt[2]:
+            raise RuntimeError("plan buffers overflowed")
+        self._n_cleaves, self._n_steps = cnt[0], cnt[4]
+        self._n_tasks = (cnt[6] & 0xFFFFFFFF) | ((cnt[7] & 0xFFFFFFFF) << 32)
+        if self._async is not None:
+            self._async.on_resolved(cnt)
+            self._async = None
+
+    def _count_leaves(self) -> int:
+        return self.n_cleaves
+
+    @property
+    def n_tasks(self) -> int:
+        self._resolve()
+        return self._n_tasks
+
+    @property
+    def n_cleaves(self) -> int:
+        self._resolve()
+        return self._n_cleaves
+
+    @property
+    def n_steps(self) -> int:
+        self._resolve()
+        return self._n_steps
 
     def __len__(self) -> int:
         return self.n_tasks
@@ -210,30 +246,60 @@ def build_plan(a: QuadtreeMatrix, b: QuadtreeMatrix, tau: float,
         e = torch.zeros((_lib.PLAN_COUNTS,), dtype=torch.int32, device=dev)
         return MultiplyPlan(tau, depth, 0, 0, 0, z, e, e, e, e, a, b, (r0, r1))
     va, vb = a.view(depth), b.view(depth)
-    hint_key = (depth, a.nleaf, b.nleaf, float(tau), r0, r1)
-    step_cap, leaf_cap = _capacity_hint.get(hint_key, (max(4096, 4 * (a.nleaf + b.nleaf)),
-                                                       min(L * L, max(1024, 2 * (a.nleaf + b.nleaf)))))
-    max_steps = min((1 << 31) - 128, max(1, (L * L * L) // 16 + L * L))
+    hint_key, (step_cap, leaf_cap) = plan_capacity(a, b, tau, depth, r0, r1)
     while True:
-        steps = torch.empty((step_cap, _lib.STEP_WORDS), dtype=torch.int32, device=dev)
-        c_keys = torch.empty((leaf_cap,), dtype=torch.int32, device=dev)
-        tile_off = torch.empty((leaf_cap + 1,), dtype=torch.int32, device=dev)
-        tile_order = torch.empty((leaf_cap,), dtype=torch.int32, device=dev)
-        counts = torch.empty((_lib.PLAN_COUNTS,), dtype=torch.int32, device=dev)
-        ws_bytes = lib.spamm_plan_workspace_bytes(depth, step_cap, leaf_cap)
-        ws = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
-        bufs = _lib.PlanBuffers(steps.data_ptr(), c_keys.data_ptr(), tile_off.data_ptr(), tile_order.data_ptr(),
-                                step_cap, leaf_cap, counts.data_ptr())
-        _lib.check(lib.spamm_plan(C.byref(va), C.byref(vb), float(tau), r0, r1, C.byref(bufs), ws.data_ptr(),
-                                  ws_bytes, _stream()), "plan")
-        cnt = counts.tolist()
-        n_c, overflow, max_list, n_steps = cnt[0], cnt[2], cnt[3], cnt[4]
+        pb = PlanAlloc(dev, depth, step_cap, leaf_cap)
+        _lib.check(lib.spamm_plan(C.byref(va), C.byref(vb), float(tau), r0, r1, C.byref(pb.struct), pb.ws.data_ptr(),
+                                  pb.ws_bytes, _stream()), "plan")
+        cnt = pb.counts.tolist()
+        n_c, overflow, n_steps = cnt[0], cnt[2], cnt[4]
         n_t = (cnt[6] & 0xFFFFFFFF) | ((cnt[7] & 0xFFFFFFFF) << 32)
         if not overflow:
             break
-        if step_cap >= max_steps and leaf_cap >= L * L:
-            raise RuntimeError("plan does not fit the 2^31 step limit")
-        step_cap = min(max_steps, max(2 * step_cap, int(1.25 * max(max_list, n_steps)) + 1024))
-        leaf_cap = min(L * L, max(4 * leaf_cap, int(1.25 * n_c) + 1024))
-    _capacity_hint[hint_key] = (step_cap, leaf_cap)
-    return MultiplyPlan(tau, depth, n_t, n_c, n_steps, steps, c_keys, tile_off, tile_order, counts, a, b, (r0, r1))
+        step_cap, leaf_cap = grow_capacity(depth, step_cap, leaf_cap, cnt)
+    remember_capacity(hint_key, max(n_steps, cnt[3]), n_c, depth)
+    return MultiplyPlan(tau, depth, n_t, n_c, n_steps, pb.steps, pb.c_keys, pb.tile_off, pb.tile_order, pb.counts,
+                        a, b, (r0, r1))
+
+
+class PlanAlloc:
+    """Device buffers of one plan (``spamm_plan_buffers``) plus the planner's workspace."""
+
+    def __init__(self, dev, depth: int, step_cap: int, leaf_cap: int):
+        self.step_cap, self.leaf_cap = step_cap, leaf_cap
+        self.steps = torch.empty((step_cap, _lib.STEP_WORDS), dtype=torch.int32, device=dev)
+        self.c_keys = torch.empty((leaf_cap,), dtype=torch.int32, device=dev)
+        self.tile_off = torch.empty((leaf_cap + 1,), dtype=torch.int32, device=dev)
+        self.tile_order = torch.empty((leaf_cap,), dtype=torch.int32, device=dev)
+        self.counts = torch.empty((_lib.PLAN_COUNTS,), dtype=torch.int32, device=dev)
+        self.ws_bytes = _lib.lib().spamm_plan_workspace_bytes(depth, step_cap, leaf_cap)
+        self.ws = torch.empty((self.ws_bytes,), dtype=torch.uint8, device=dev)
+        self.struct = _lib.PlanBuffers(self.steps.data_ptr(), self.c_keys.data_ptr(), self.tile_off.data_ptr(),
+                                       self.tile_order.data_ptr(), step_cap, leaf_cap, self.counts.data_ptr())
+
+
+def plan_capacity(a: QuadtreeMatrix, b: QuadtreeMatrix, tau: float, depth: int, r0: int, r1: int):
+    """(hint key, (step capacity, leaf capacity)): what worked last time for this shape, else a guess."""
+    L = 1 << depth
+    na, nb = a._leaf_bound(), b._leaf_bound()
+    key = (depth, na, nb, float(tau), r0, r1)
+    guess = (max(4096, na + nb), min(L * L, max(1024, 2 * (na + nb))))
+    return key, _capacity_hint.get(key, guess)
+
+
+def grow_capacity(depth: int, step_cap: int, leaf_cap: int, cnt) -> tuple[int, int]:
+    L = 1 << depth
+    max_steps = min((1 << 31) - 128, max(1, (L * L * L) // 16 + L * L))
+    if step_cap >= max_steps and leaf_cap >= L * L:
+        raise RuntimeError("plan does not fit the 2^31 step limit")
+    step_cap = min(max_steps, max(2 * step_cap, int(1.25 * max(cnt[3], cnt[4])) + 1024))
+    leaf_cap = min(L * L, max(4 * leaf_cap, int(1.25 * cnt[0]) + 1024))
+    return step_cap, leaf_cap
+
+
+def remember_capacity(key, n_steps: int, n_cleaves: int, depth: int) -> None:
+    """Next time, size the buffers just above what this shape needed."""
+    L = 1 << depth
+    # (the step capacity also bounds the candidate lists of the coarser levels; the start level
+    # alone can hold 256 nodes x 16 candidates)
+    _capacity_hint[key] = (max(4608, int(1.1 * n_steps) + 256), min(L * L, max(320, int(1.1 * n_cleaves) + 64)))

@@ -96,6 +96,34 @@ class QuadtreeMatrix:
         self._set_empty()
 
     # -- storage -------------------------------------------------------------------------------
+    # The leaf count of a multiply result is produced on the device; it is read back (one
+    # synchronisation) only when something on the host first asks for it.
+    @property
+    def nleaf(self) -> int:
+        if self._nleaf is None:
+            self._nleaf = int(self._nleaf_source())
+            self._nleaf_source = None
+        return self._nleaf
+
+    @nleaf.setter
+    def nleaf(self, value: int) -> None:
+        self._nleaf = int(value)
+        self._nleaf_source = None
+
+    def _leaf_bound(self) -> int:
+        """Stored leaves, or their upper bound while the count is still on the device."""
+        return self._nleaf if self._nleaf is not None else int(self.keys.shape[0])
+
+    def _adopt_product(self, keys, values, values_t, leaf_sq, grids: "_Grids", count_source) -> None:
+        """Take over the buffers an asynchronous multiply is filling (capacity sized)."""
+        self._pending.clear()
+        self.keys, self.values, self.values_t, self.leaf_sq = keys, values, values_t, leaf_sq
+        self._leaf_sq_grid = None
+        self._grids = {grids.depth: grids}
+        self._nleaf = None
+        self._nleaf_source = count_source
+        self._rev += 1
+
     def _set_empty(self) -> None:
         self.nleaf = 0
         self.keys = self.values = self.values_t = None
@@ -233,8 +261,8 @@ class QuadtreeMatrix:
     def view(self, depth: int | None = None) -> _lib.TreeView:
         """ctypes view for the kernels, indexed at a (possibly larger) common depth."""
         g = self.grids(depth)
-        nz = self.nleaf > 0
-        return _lib.TreeView(self.m, self.n, g.depth, self.nleaf,
+        nz = self._nleaf is None or self._nleaf > 0        # do not force a pending count to the host
+        return _lib.TreeView(self.m, self.n, g.depth, self._leaf_bound() if nz else 0,
                              _ptr(self.keys) if nz else None, _ptr(self.values) if nz else None,
                              _ptr(self.values_t) if nz else None,
                              g.slot.data_ptr(), g.slot_t.data_ptr(), g.norm.data_ptr(), g.norm_t.data_ptr())
