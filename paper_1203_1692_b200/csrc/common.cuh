@@ -149,6 +149,50 @@ __device__ __forceinline__ uint32_t lb_lo(unsigned long long w) { return (uint32
 __device__ __forceinline__ uint32_t lb_hi(unsigned long long w) { return (uint32_t)((w >> 31) & 0x7FFFFFFFull); }
 __device__ __forceinline__ unsigned long long lb_status(unsigned long long w) { return w >> 62; }
 
+// Called by ONE WARP of a tile (all 32 lanes, same arguments): publishes the tile's aggregate, then
+// inspects 32 predecessors per step -- nearest first -- until one of them carries an inclusive
+// prefix.  Returns the exclusive prefix (lo, hi) in every lane and publishes the inclusive one.
+__device__ __forceinline__ void lb_exclusive_warp(volatile unsigned long long *state, int tile, uint32_t agg_lo,
+                                                  uint32_t agg_hi, uint32_t &ex_lo, uint32_t &ex_hi)
+{
+    const uint32_t lane = threadIdx.x & 31u;
+    if (tile == 0) {
+        ex_lo = ex_hi = 0;
+        if (lane == 0) {
+            __threadfence();
+            state[0] = lb_pack(LB_PREFIX, agg_lo, agg_hi);
+        }
+        return;
+    }
+    if (lane == 0) {
+        __threadfence();
+        state[tile] = lb_pack(LB_AGGREGATE, agg_lo, agg_hi);
+    }
+    uint32_t lo = 0, hi = 0;
+    for (int base = tile - 1; base >= 0; base -= 32) {
+        const int idx = base - (int)lane;                 // lane 0 looks at the nearest predecessor
+        unsigned long long w = lb_pack(LB_PREFIX, 0u, 0u);   // before tile 0: an empty prefix
+        if (idx >= 0) {
+            do {
+                w = state[idx];
+            } while (lb_status(w) == LB_INVALID);
+        }
+        const uint32_t pref = __ballot_sync(0xFFFFFFFFu, lb_status(w) == LB_PREFIX);
+        // take every lane up to and including the first one that holds a prefix
+        const uint32_t take = pref ? ((2u << (__ffs(pref) - 1)) - 1u) : 0xFFFFFFFFu;
+        const bool mine = (take >> lane) & 1u;
+        lo += __reduce_add_sync(0xFFFFFFFFu, mine ? lb_lo(w) : 0u);
+        hi += __reduce_add_sync(0xFFFFFFFFu, mine ? lb_hi(w) : 0u);
+        if (pref) break;
+    }
+    ex_lo = lo;
+    ex_hi = hi;
+    if (lane == 0) {
+        __threadfence();
+        state[tile] = lb_pack(LB_PREFIX, lo + agg_lo, hi + agg_hi);
+    }
+}
+
 // Called by ONE thread of a tile: publishes the tile's aggregate, walks back over the
 // predecessors and returns the exclusive prefix (lo, hi); then publishes the inclusive one.
 __device__ __forceinline__ void lb_exclusive(volatile unsigned long long *state, int tile, uint32_t agg_lo,

@@ -42,14 +42,17 @@ struct PlanShared {      // lives at the start of the workspace, zeroed once per
 };
 
 // ---- start level: dense enumeration by one block ---------------------------------------
-// side = 2^level <= 16, so at most 256 product nodes with at most 16 candidates each.
-__global__ void __launch_bounds__(256) plan_root_kernel(const float *__restrict__ norm_a, const float *__restrict__ norm_bt,
-                                                        int level, int shift, int row0, int row1, double tau, LevelBuf out,
-                                                        int32_t *counts_out, int64_t cap_nodes, int64_t cap_tasks,
-                                                        int32_t *overflow)
+// side = 2^level <= 32, so at most 1024 product nodes (one thread each) with at most 32 candidates.
+#define ROOT_THREADS 1024
+#define ROOT_MAX_LEVEL 5
+__global__ void __launch_bounds__(ROOT_THREADS) plan_root_kernel(const float *__restrict__ norm_a,
+                                                                 const float *__restrict__ norm_bt, int level, int shift,
+                                                                 int row0, int row1, double tau, LevelBuf out,
+                                                                 int32_t *counts_out, int64_t cap_nodes, int64_t cap_tasks,
+                                                                 int32_t *overflow)
 {
-    __shared__ uint32_t s_cnt[256], s_act[256];
-    __shared__ uint32_t s_wc[8], s_wa[8];
+    __shared__ uint32_t s_cnt[ROOT_THREADS], s_act[ROOT_THREADS];
+    __shared__ uint32_t s_wc[ROOT_THREADS / 32], s_wa[ROOT_THREADS / 32];
     const int S = 1 << level;
     const int c = threadIdx.x;
     uint32_t i = 0, j = 0, live = 0;
@@ -61,7 +64,7 @@ __global__ void __launch_bounds__(256) plan_root_kernel(const float *__restrict_
                 if (norm_test(norm_a[i * S + k], norm_bt[j * S + k], tau)) live |= 1u << k;
     }
     const uint32_t cnt = __popc(live), act = cnt > 0;
-    // block exclusive scan of (cnt, act): warp shuffles + 8 warp totals
+    // block exclusive scan of (cnt, act): warp shuffles, then the 32 warp totals by warp 0
     uint32_t ic = cnt, ia = act;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -70,14 +73,23 @@ __global__ void __launch_bounds__(256) plan_root_kernel(const float *__restrict_
     }
     if (lane_id() == 31) { s_wc[c >> 5] = ic; s_wa[c >> 5] = ia; }
     __syncthreads();
-    uint32_t bc = 0, ba = 0, tc = 0, ta = 0;
+    __shared__ uint32_t s_tot[2];
+    if (c < 32) {
+        const uint32_t vc0 = s_wc[c], va0 = s_wa[c];
+        uint32_t wc = vc0, wa = va0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) {
-        if (w < (c >> 5)) { bc += s_wc[w]; ba += s_wa[w]; }
-        tc += s_wc[w]; ta += s_wa[w];
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t xc = __shfl_up_sync(FULL_MASK, wc, d), xa = __shfl_up_sync(FULL_MASK, wa, d);
+            if (c >= d) { wc += xc; wa += xa; }
+        }
+        s_wc[c] = wc - vc0;
+        s_wa[c] = wa - va0;
+        if (c == 31) { s_tot[0] = wc; s_tot[1] = wa; }
     }
-    s_cnt[c] = bc + ic - cnt;
-    s_act[c] = ba + ia - act;
+    __syncthreads();
+    const uint32_t tc = s_tot[0], ta = s_tot[1];
+    s_cnt[c] = s_wc[c >> 5] + ic - cnt;
+    s_act[c] = s_wa[c >> 5] + ia - act;
     if (c == 0) {
         counts_out[0] = (int32_t)ta;
         counts_out[1] = (int32_t)tc;
@@ -175,18 +187,23 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_expand_kernel(ExpandArgs a)
         if (lane == 0) { s_wtasks[warp] = wtasks; s_wact[warp] = wact; }
         __syncthreads();
         // phase 2: block scan + look-back
-        if (threadIdx.x == 0) {
-            uint32_t rt = 0, ra = 0;
-            for (int w = 0; w < PLAN_WARPS; ++w) {
-                uint32_t vt = s_wtasks[w], va = s_wact[w];
-                s_wtasks[w] = rt; s_wact[w] = ra;
-                rt += vt; ra += va;
+        if (warp == 0) {
+            uint32_t vt = lane < PLAN_WARPS ? s_wtasks[lane] : 0u, va = lane < PLAN_WARPS ? s_wact[lane] : 0u;
+            uint32_t it = vt, ia = va;          // inclusive scan over the block's warps
+#pragma unroll
+            for (int d = 1; d < PLAN_WARPS; d <<= 1) {
+                const uint32_t xt = __shfl_up_sync(FULL_MASK, it, d), xa = __shfl_up_sync(FULL_MASK, ia, d);
+                if (lane >= (uint32_t)d) { it += xt; ia += xa; }
             }
+            const uint32_t rt = __shfl_sync(FULL_MASK, it, PLAN_WARPS - 1), ra = __shfl_sync(FULL_MASK, ia, PLAN_WARPS - 1);
+            if (lane < PLAN_WARPS) { s_wtasks[lane] = it - vt; s_wact[lane] = ia - va; }
             uint32_t ex_lo, ex_hi;
-            lb_exclusive(a.tile_state, tile, rt, ra, ex_lo, ex_hi);
-            s_base_lo = ex_lo;
-            s_base_hi = ex_hi;
-            if (tile == ntiles - 1) {
+            lb_exclusive_warp(a.tile_state, tile, rt, ra, ex_lo, ex_hi);
+            if (lane == 0) {
+                s_base_lo = ex_lo;
+                s_base_hi = ex_hi;
+            }
+            if (lane == 0 && tile == ntiles - 1) {
                 const int64_t tot_t = (int64_t)ex_lo + rt, tot_a = (int64_t)ex_hi + ra;
                 a.counts_out[0] = (int32_t)tot_a;
                 a.counts_out[1] = (int32_t)tot_t;
@@ -350,18 +367,23 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
         }
         __syncthreads();
         // phase 2: block scan + look-back over (records, product leaves)
-        if (threadIdx.x == 0) {
-            uint32_t rs = 0, rl = 0;
-            for (int w = 0; w < PLAN_WARPS; ++w) {
-                uint32_t vs = s_wsteps[w], vl = s_wleaves[w];
-                s_wsteps[w] = rs; s_wleaves[w] = rl;
-                rs += vs; rl += vl;
+        if (warp == 0) {
+            uint32_t vs = lane < PLAN_WARPS ? s_wsteps[lane] : 0u, vl = lane < PLAN_WARPS ? s_wleaves[lane] : 0u;
+            uint32_t is = vs, il = vl;          // inclusive scan over the block's warps
+#pragma unroll
+            for (int d = 1; d < PLAN_WARPS; d <<= 1) {
+                const uint32_t xs = __shfl_up_sync(FULL_MASK, is, d), xl = __shfl_up_sync(FULL_MASK, il, d);
+                if (lane >= (uint32_t)d) { is += xs; il += xl; }
             }
+            const uint32_t rs = __shfl_sync(FULL_MASK, is, PLAN_WARPS - 1), rl = __shfl_sync(FULL_MASK, il, PLAN_WARPS - 1);
+            if (lane < PLAN_WARPS) { s_wsteps[lane] = is - vs; s_wleaves[lane] = il - vl; }
             uint32_t ex_lo, ex_hi;
-            lb_exclusive(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
-            s_base_lo = ex_lo;
-            s_base_hi = ex_hi;
-            if (tile == ntiles - 1) {
+            lb_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
+            if (lane == 0) {
+                s_base_lo = ex_lo;
+                s_base_hi = ex_hi;
+            }
+            if (lane == 0 && tile == ntiles - 1) {
                 const int64_t tot_s = (int64_t)ex_lo + rs, tot_l = (int64_t)ex_hi + rl;
                 a.counts[0] = (int32_t)tot_l;
                 a.counts[4] = (int32_t)tot_s;
@@ -454,18 +476,16 @@ __global__ void __launch_bounds__(256) plan_order_kernel(const int32_t *__restri
         v[x] = bins[PLAN_BINS - 1 - (4 * t + x)];
         sum += v[x];
     }
-    s_part[t] = sum;
-    __syncthreads();
-    if (t == 0) {
-        unsigned int run = 0;
-        for (int x = 0; x < 256; ++x) {
-            const unsigned int y = s_part[x];
-            s_part[x] = run;
-            run += y;
-        }
+    unsigned int inc = sum;                 // block exclusive scan: warp shuffles + 8 warp totals
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned int y = __shfl_up_sync(FULL_MASK, inc, d);
+        if ((t & 31) >= d) inc += y;
     }
+    if ((t & 31) == 31) s_part[t >> 5] = inc;
     __syncthreads();
-    unsigned int run = s_part[t];
+    unsigned int run = inc - sum;
+    for (int w = 0; w < (t >> 5); ++w) run += s_part[w];
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
         s_start[PLAN_BINS - 1 - (4 * t + x)] = run;
@@ -538,10 +558,10 @@ extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, do
 
     const int depth = a->depth;
     const int tl = depth >= 2 ? depth - 2 : 0;          // super-tile level
-    const int l0 = tl < 4 ? tl : 4;                     // start level
+    const int l0 = tl < ROOT_MAX_LEVEL ? tl : ROOT_MAX_LEVEL;   // start level
     int32_t *overflow = out->counts + 2, *max_list = out->counts + 3;
     int cur = 0;
-    plan_root_kernel<<<1, 256, 0, st>>>(a->norm + spamm_level_offset(l0), b->norm_t + spamm_level_offset(l0), l0,
+    plan_root_kernel<<<1, ROOT_THREADS, 0, st>>>(a->norm + spamm_level_offset(l0), b->norm_t + spamm_level_offset(l0), l0,
                                         depth - l0, row0, row1, tau, w.buf[cur], w.shared->counts[l0],
                                         out->leaf_capacity, out->step_capacity, overflow);
     SPAMM_CHECK_LAUNCH();

@@ -49,17 +49,23 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_flags_kernel(Op op, int64_t
         }
         if (lane_id() == 31) s_warp[threadIdx.x >> 5] = inc;
         __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t run = 0;
-            for (int w = 0; w < SCAN_THREADS / 32; ++w) {
-                uint32_t v = s_warp[w];
-                s_warp[w] = run;
-                run += v;
+        if (threadIdx.x < 32) {
+            const uint32_t l = threadIdx.x;
+            const uint32_t v = l < SCAN_THREADS / 32 ? s_warp[l] : 0u;
+            uint32_t iv = v;                    // inclusive scan over the block's warps
+#pragma unroll
+            for (int d = 1; d < SCAN_THREADS / 32; d <<= 1) {
+                const uint32_t x = __shfl_up_sync(FULL_MASK, iv, d);
+                if (l >= (uint32_t)d) iv += x;
             }
+            const uint32_t run = __shfl_sync(FULL_MASK, iv, SCAN_THREADS / 32 - 1);
+            if (l < SCAN_THREADS / 32) s_warp[l] = iv - v;
             uint32_t ex, dummy;
-            lb_exclusive(tile_state, tile, run, 0u, ex, dummy);
-            s_base = ex;
-            if (tile == ntiles - 1) *total_out = (int32_t)(ex + run);
+            lb_exclusive_warp(tile_state, tile, run, 0u, ex, dummy);
+            if (l == 0) {
+                s_base = ex;
+                if (tile == ntiles - 1) *total_out = (int32_t)(ex + run);
+            }
         }
         __syncthreads();
         uint32_t pos = s_base + s_warp[threadIdx.x >> 5] + (inc - cnt);

@@ -301,5 +301,5 @@ def remember_capacity(key, n_steps: int, n_cleaves: int, depth: int) -> None:
     """Next time, size the buffers just above what this shape needed."""
     L = 1 << depth
     # (the step capacity also bounds the candidate lists of the coarser levels; the start level
-    # alone can hold 256 nodes x 16 candidates)
-    _capacity_hint[key] = (max(4608, int(1.1 * n_steps) + 256), min(L * L, max(320, int(1.1 * n_cleaves) + 64)))
+    # alone can hold 1024 nodes x 32 candidates; an overflow there just repeats the plan)
+    _capacity_hint[key] = (max(8192, int(1.1 * n_steps) + 256), min(L * L, max(320, int(1.1 * n_cleaves) + 64)))
