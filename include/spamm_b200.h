@@ -145,9 +145,10 @@ typedef struct {
 } spamm_step;
 
 /* counts[]: [0] product leaves nC, [1] scratch (the numeric kernel's tile counter),
- * [2] overflow flag, [3] largest intermediate list, [4] step records, [5] super-tile nodes,
- * [6..7] tasks T as one uint64 */
-#define SPAMM_PLAN_COUNTS 8
+ * [2] overflow flag, [3] largest intermediate list, [4] step records, [5] super-tile nodes with
+ * at least one record, [6..7] tasks T as one uint64, [8..9] executed 4x4x4 products as one uint64
+ * (spamm_multiply only), [10] scratch, [11] all super-tile nodes (tile_off has one more entry) */
+#define SPAMM_PLAN_COUNTS 12
 typedef struct {
     spamm_step *steps;       /* [step_capacity]                                   */
     uint32_t *c_keys;        /* [leaf_capacity] product leaf keys, ascending      */
@@ -212,13 +213,30 @@ typedef struct {
 
 /* build_plan + execute_plan + compute_norms on C, enqueued back to back on `stream` with no
  * host synchronisation: C = alpha32 * sum of the surviving leaf products.  The product leaves
- * are plan->c_keys[0 .. counts[0]) with their records in c->values / c->values_t.  The caller
+ * are plan->c_keys[0 .. counts[0]) with their records in c->values / c->values_t; the number of
+ * executed micro products (ExecCounters.products4) accumulates in counts[8..9].  The caller
  * reads plan->counts when it next synchronises; counts[2] != 0 means a capacity was too small
  * (nothing was computed) and the call must be repeated with larger buffers. */
 int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
                    int exact, float alpha, int32_t row0, int32_t row1,
                    const spamm_plan_buffers *plan, void *plan_ws, size_t plan_ws_bytes,
-                   const spamm_product_buffers *c, unsigned long long *counters, void *stream);
+                   const spamm_product_buffers *c, void *stream);
+
+/* The same on ONE caller-provided device allocation: spamm_multiply_arena_layout() gives the byte
+ * offset of every buffer of the plan and of the product (fields named as in spamm_plan_buffers /
+ * spamm_product_buffers) and the total size; spamm_multiply_arena() carves `arena` that way and
+ * runs spamm_multiply.  One allocation and one call per product on the host side. */
+typedef struct {
+    int64_t counts, steps, c_keys, tile_off, tile_order, plan_ws, plan_ws_bytes;
+    int64_t values, values_t, leaf_sq, slot, slot_t, norm, norm_t, leaf_sq_grid, sq_levels;
+    int64_t total;
+} spamm_arena_layout;
+int spamm_multiply_arena_layout(int depth, int c_depth, int64_t step_capacity, int64_t leaf_capacity,
+                                spamm_arena_layout *out);
+int spamm_multiply_arena(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
+                         int exact, float alpha, int32_t row0, int32_t row1, int c_depth,
+                         int64_t step_capacity, int64_t leaf_capacity, void *arena, size_t arena_bytes,
+                         void *stream);
 
 /* _compose with beta != 0 (numeric.py:276-284): out leaf x = (alpha32 * prod[ip]) + (old[io] * beta32)
  * with ip / io = -1 when that side has no leaf; the alpha == 1 / beta == 1 special cases keep

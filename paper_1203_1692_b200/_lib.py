@@ -41,9 +41,17 @@ class ProductBuffers(C.Structure):
                 ("norm_t", vp), ("leaf_sq_grid", vp), ("sq_levels", vp), ("depth", i32)]
 
 
+class ArenaLayout(C.Structure):
+    """``spamm_arena_layout`` (byte offsets into the single allocation of spamm_multiply_arena)."""
+
+    _fields_ = [(n, i64) for n in ("counts", "steps", "c_keys", "tile_off", "tile_order", "plan_ws", "plan_ws_bytes",
+                                   "values", "values_t", "leaf_sq", "slot", "slot_t", "norm", "norm_t", "leaf_sq_grid",
+                                   "sq_levels", "total")]
+
+
 REC = 272           # floats per stored leaf record: 256 values + 16 sub-block norms
 STEP_WORDS = 16     # uint32 words per step record (struct spamm_step)
-PLAN_COUNTS = 8
+PLAN_COUNTS = 12
 
 
 # every symbol include/spamm_b200.h declares: (restype, argtypes)
@@ -66,7 +74,10 @@ SIGNATURES = {
     "spamm_execute": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), C.POINTER(PlanBuffers), i64, i64,
                                 f64, f32, C.c_int, C.c_int, vp, vp, vp, vp, vp]),
     "spamm_multiply": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, C.c_int, C.c_int, f32, i32, i32,
-                                 C.POINTER(PlanBuffers), vp, sz, C.POINTER(ProductBuffers), vp, vp]),
+                                 C.POINTER(PlanBuffers), vp, sz, C.POINTER(ProductBuffers), vp]),
+    "spamm_multiply_arena_layout": (C.c_int, [C.c_int, C.c_int, i64, i64, C.POINTER(ArenaLayout)]),
+    "spamm_multiply_arena": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, C.c_int, C.c_int, f32, i32, i32,
+                                       C.c_int, i64, i64, vp, sz, vp]),
     "spamm_union_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp, sz, vp]),
     "spamm_compose": (C.c_int, [vp, vp, vp, vp, i64, f32, f32, C.c_int, C.c_int, vp, vp]),
 }

@@ -34,7 +34,8 @@ struct __align__(16) StageDesc {
     uint32_t a_present;    // stored leaves of the staged A block, bit morton4(di,kk)
     uint32_t b_present;    // stored leaves of the staged B block, bit morton4(kk,dj)
     uint32_t live[4];      // live tasks per kk
-    uint32_t pad[3];
+    uint32_t tile;         // Morton index of the super-tile
+    uint32_t pad[2];
 };
 
 struct ExecArgs {
@@ -51,6 +52,13 @@ struct ExecArgs {
     float *c_values, *c_values_t;
     double *c_leaf_sq;
     unsigned long long *counters;
+    // optional: the leaf-level grids of C (spamm_product_buffers); the epilogue then indexes the
+    // product leaves itself (slot, norm and square sum of leaf (i,j)), replacing spamm_index_leaves
+    int32_t *c_slot, *c_slot_t;
+    float *c_norm, *c_norm_t;
+    double *c_sq_grid;
+    int c_L;                     // side of C's leaf grid
+    int sub2;                    // leaves per super-tile (16; 4 or 1 for tiny trees)
     int nstages;                 // depth of the shared-memory ring
     int dbg;                     // tuning aid (SPAMM_EX_DEBUG): 1 = no copies, 2 = no math
 };
@@ -137,6 +145,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
                 if (lane == 1) d[0] = cur;                       // flags
                 if (lane == 2) d[1] = cur;                       // c_base
                 if (lane == 12) d[2] = cur;                      // present
+                if (lane == 3) d[9] = cur;                       // tile
                 if (lane == 5) d[3] = cur;                       // a_present
                 if (lane == 7) d[4] = cur;                       // b_present
                 if (lane >= 8 && lane < 12) d[5 + lane - 8] = cur;   // live[kk]
@@ -261,9 +270,10 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
                 }
             }
         }
-        uint32_t c_base = 0, present = 0;
+        uint32_t c_base = 0, present = 0, tile_id = 0;
         if (flags & STEP_LAST) {
             c_base = ds.c_base;
+            tile_id = ds.tile;
             present = ds.present;
         }
         __syncwarp();
@@ -311,7 +321,19 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
             const float sn = (float)sqrt(S);
             cv[256 + q * 4 + p] = sn;
             ct[256 + t16] = sn;
-            if (t16 == 0) g.c_leaf_sq[cslot] = tot;
+            if (t16 == 0) {
+                g.c_leaf_sq[cslot] = tot;
+                if (g.c_slot) {
+                    uint32_t ci, cj;
+                    morton_decode(tile_id * (uint32_t)g.sub2 + (uint32_t)mypos, ci, cj);
+                    const float nv = (float)sqrt(tot);
+                    g.c_slot[(int64_t)ci * g.c_L + cj] = (int32_t)cslot;
+                    g.c_slot_t[(int64_t)cj * g.c_L + ci] = (int32_t)cslot;
+                    g.c_norm[(int64_t)ci * g.c_L + cj] = nv;
+                    g.c_norm_t[(int64_t)cj * g.c_L + ci] = nv;
+                    g.c_sq_grid[(int64_t)ci * g.c_L + cj] = tot;
+                }
+            }
         }
     }
     if (FINE) {
@@ -333,10 +355,10 @@ static ExecTuning exec_tuning()
     return t;
 }
 
-extern "C" int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b, const spamm_plan_buffers *plan,
-                             int64_t nsteps, int64_t nC, double tau, float alpha, int granularity, int exact,
-                             float *c_values, float *c_values_t, double *c_leaf_sq, unsigned long long *counters,
-                             void *stream)
+int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const spamm_plan_buffers *plan,
+                       int64_t nsteps, int64_t nC, double tau, float alpha, int granularity, int exact,
+                       float *c_values, float *c_values_t, double *c_leaf_sq, unsigned long long *counters,
+                       const spamm_product_buffers *cgrid, void *stream)
 {
     if (!a || !b || !plan || nsteps < -1 || nC < -1) return SPAMM_EINVAL;
     if (granularity != SPAMM_FINE4 && granularity != SPAMM_COARSE16) return SPAMM_EINVAL;
@@ -357,6 +379,23 @@ extern "C" int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b,
     g.c_values_t = c_values_t;
     g.c_leaf_sq = c_leaf_sq;
     g.counters = counters;
+    g.c_slot = g.c_slot_t = nullptr;
+    g.c_norm = g.c_norm_t = nullptr;
+    g.c_sq_grid = nullptr;
+    g.c_L = 0;
+    {
+        const int sub = a->depth >= 2 ? 4 : (1 << a->depth);
+        g.sub2 = sub * sub;
+    }
+    if (cgrid) {
+        const int64_t off = spamm_level_offset(cgrid->depth);
+        g.c_slot = cgrid->slot;
+        g.c_slot_t = cgrid->slot_t;
+        g.c_norm = cgrid->norm + off;
+        g.c_norm_t = cgrid->norm_t + off;
+        g.c_sq_grid = cgrid->leaf_sq_grid;
+        g.c_L = 1 << cgrid->depth;
+    }
     if (cudaMemsetAsync(plan->counts + 1, 0, sizeof(int32_t), st) != cudaSuccess) return SPAMM_ECUDA;
     static const ExecTuning tune = exec_tuning();
     g.nstages = tune.stages;
@@ -370,6 +409,15 @@ extern "C" int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b,
     kern<<<grid, EX_THREADS, smem, st>>>(g);
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
+}
+
+extern "C" int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b, const spamm_plan_buffers *plan,
+                             int64_t nsteps, int64_t nC, double tau, float alpha, int granularity, int exact,
+                             float *c_values, float *c_values_t, double *c_leaf_sq, unsigned long long *counters,
+                             void *stream)
+{
+    return spamm_execute_impl(a, b, plan, nsteps, nC, tau, alpha, granularity, exact, c_values, c_values_t, c_leaf_sq,
+                              counters, nullptr, stream);
 }
 
 // ---- beta != 0: union of the old and the produced leaf sets, then _compose ----------------------

@@ -5,25 +5,100 @@
 // plan.counts[2] for the caller to check whenever it first synchronises.
 #include "common.cuh"
 
-int spamm_index_leaves_impl(const uint32_t *keys, const double *leaf_sq_packed, int64_t nleaf, const int32_t *nleaf_dev,
-                            int depth, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid,
-                            cudaStream_t st);
+int spamm_clear_leaf_grids(int depth, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid,
+                           cudaStream_t st);
+int spamm_launch_interior(const double *leaf_sq, int depth, float *norm, float *norm_t, double *sq_levels,
+                          unsigned int *ticket, cudaStream_t st);
+int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const spamm_plan_buffers *plan,
+                       int64_t nsteps, int64_t nC, double tau, float alpha, int granularity, int exact,
+                       float *c_values, float *c_values_t, double *c_leaf_sq, unsigned long long *counters,
+                       const spamm_product_buffers *cgrid, void *stream);
 
 extern "C" int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity, int exact,
                               float alpha, int32_t row0, int32_t row1, const spamm_plan_buffers *plan, void *plan_ws,
-                              size_t plan_ws_bytes, const spamm_product_buffers *c, unsigned long long *counters,
-                              void *stream)
+                              size_t plan_ws_bytes, const spamm_product_buffers *c, void *stream)
 {
-    if (!a || !b || !plan || !c || !counters) return SPAMM_EINVAL;
-    int rc = spamm_plan(a, b, tau, row0, row1, plan, plan_ws, plan_ws_bytes, stream);
+    if (!a || !b || !plan || !c) return SPAMM_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    // C's leaf grids start empty; the numeric kernel's epilogue fills in the product leaves
+    int rc = spamm_clear_leaf_grids(c->depth, c->slot, c->slot_t, c->norm, c->norm_t, c->leaf_sq_grid, st);
     if (rc != SPAMM_OK) return rc;
-    rc = spamm_execute(a, b, plan, -1, -1, tau, alpha, granularity, exact, c->values, c->values_t, c->leaf_sq, counters,
-                       stream);
+    rc = spamm_plan(a, b, tau, row0, row1, plan, plan_ws, plan_ws_bytes, stream);
     if (rc != SPAMM_OK) return rc;
-    // C's tree: leaf grids from the packed product leaves (their count is plan.counts[0]), then the
-    // interior norms -- compute_norms, numeric.py:179 / core.py:331-345
-    rc = spamm_index_leaves_impl(plan->c_keys, c->leaf_sq, plan->leaf_capacity, plan->counts, c->depth, c->slot, c->slot_t,
-                                 c->norm, c->norm_t, c->leaf_sq_grid, (cudaStream_t)stream);
+    // executed micro products are counted in plan->counts[8..9]
+    rc = spamm_execute_impl(a, b, plan, -1, -1, tau, alpha, granularity, exact, c->values, c->values_t, c->leaf_sq,
+                            reinterpret_cast<unsigned long long *>(plan->counts + 8), c, stream);
     if (rc != SPAMM_OK) return rc;
-    return spamm_build_interior(c->leaf_sq_grid, c->depth, c->norm, c->norm_t, c->sq_levels, 0, stream);
+    // interior norms of C: compute_norms, numeric.py:179 / core.py:331-345
+    return spamm_launch_interior(c->leaf_sq_grid, c->depth, c->norm, c->norm_t, c->sq_levels,
+                                 reinterpret_cast<unsigned int *>(plan->counts + 10), st);
+}
+
+// ---- the same on ONE caller-provided allocation ------------------------------------------------
+static inline int64_t arena_take(int64_t &o, int64_t bytes)
+{
+    const int64_t at = o;
+    o = (o + bytes + 255) / 256 * 256;
+    return at;
+}
+
+extern "C" int spamm_multiply_arena_layout(int depth, int c_depth, int64_t step_capacity, int64_t leaf_capacity,
+                                           spamm_arena_layout *out)
+{
+    if (!out || depth < 0 || depth > 15 || c_depth < 0 || c_depth > 15 || step_capacity < 1 || leaf_capacity < 1)
+        return SPAMM_EINVAL;
+    const int64_t cells = int64_t(1) << (2 * c_depth);
+    const int64_t total = spamm_level_offset(c_depth) + cells;
+    int64_t o = 0;
+    out->counts = arena_take(o, SPAMM_PLAN_COUNTS * 4);
+    out->steps = arena_take(o, step_capacity * (int64_t)sizeof(spamm_step));
+    out->c_keys = arena_take(o, leaf_capacity * 4);
+    out->tile_off = arena_take(o, (leaf_capacity + 1) * 4);
+    out->tile_order = arena_take(o, leaf_capacity * 4);
+    out->plan_ws_bytes = (int64_t)spamm_plan_workspace_bytes(depth, step_capacity, leaf_capacity);
+    out->plan_ws = arena_take(o, out->plan_ws_bytes);
+    out->values = arena_take(o, leaf_capacity * SPAMM_REC_BYTES);
+    out->values_t = arena_take(o, leaf_capacity * SPAMM_REC_BYTES);
+    out->leaf_sq = arena_take(o, leaf_capacity * 8);
+    out->slot = arena_take(o, cells * 4);
+    out->slot_t = arena_take(o, cells * 4);
+    out->norm = arena_take(o, total * 4);
+    out->norm_t = arena_take(o, total * 4);
+    out->leaf_sq_grid = arena_take(o, cells * 8);
+    out->sq_levels = arena_take(o, total * 8);
+    out->total = o;
+    return SPAMM_OK;
+}
+
+extern "C" int spamm_multiply_arena(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
+                                    int exact, float alpha, int32_t row0, int32_t row1, int c_depth, int64_t step_capacity,
+                                    int64_t leaf_capacity, void *arena, size_t arena_bytes, void *stream)
+{
+    if (!a || !b || !arena) return SPAMM_EINVAL;
+    spamm_arena_layout l;
+    int rc = spamm_multiply_arena_layout(a->depth, c_depth, step_capacity, leaf_capacity, &l);
+    if (rc != SPAMM_OK) return rc;
+    if ((int64_t)arena_bytes < l.total) return SPAMM_EWORKSPACE;
+    char *p = reinterpret_cast<char *>(arena);
+    spamm_plan_buffers plan;
+    plan.steps = reinterpret_cast<spamm_step *>(p + l.steps);
+    plan.c_keys = reinterpret_cast<uint32_t *>(p + l.c_keys);
+    plan.tile_off = reinterpret_cast<int32_t *>(p + l.tile_off);
+    plan.tile_order = reinterpret_cast<int32_t *>(p + l.tile_order);
+    plan.step_capacity = step_capacity;
+    plan.leaf_capacity = leaf_capacity;
+    plan.counts = reinterpret_cast<int32_t *>(p + l.counts);
+    spamm_product_buffers c;
+    c.values = reinterpret_cast<float *>(p + l.values);
+    c.values_t = reinterpret_cast<float *>(p + l.values_t);
+    c.leaf_sq = reinterpret_cast<double *>(p + l.leaf_sq);
+    c.slot = reinterpret_cast<int32_t *>(p + l.slot);
+    c.slot_t = reinterpret_cast<int32_t *>(p + l.slot_t);
+    c.norm = reinterpret_cast<float *>(p + l.norm);
+    c.norm_t = reinterpret_cast<float *>(p + l.norm_t);
+    c.leaf_sq_grid = reinterpret_cast<double *>(p + l.leaf_sq_grid);
+    c.sq_levels = reinterpret_cast<double *>(p + l.sq_levels);
+    c.depth = c_depth;
+    return spamm_multiply(a, b, tau, granularity, exact, alpha, row0, row1, &plan, p + l.plan_ws, (size_t)l.plan_ws_bytes,
+                          &c, stream);
 }

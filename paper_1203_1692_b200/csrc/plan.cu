@@ -262,6 +262,9 @@ struct TileArgs {
     const float *norm_bt;     // leaf level grid of B transposed (j,k)
     const int32_t *slot_a;    // leaf slots of A (i,k)
     const int32_t *slot_bt;   // leaf slots of B transposed (j,k)
+    const float *norm_a_t;    // super-tile level grids (dense start only)
+    const float *norm_bt_t;
+    int St;                   // side of the super-tile level
     int L;                    // leaf grid side
     int sub;                  // leaves per block side: 4 (2 or 1 for depth 1 or 0)
     int row0, row1;
@@ -309,15 +312,21 @@ __device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, uint32_t I, u
     return t;
 }
 
-__global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
+// DENSE: there is no list from a coarser level; every super-tile node of the 2^tl x 2^tl grid
+// (tl <= 6) builds its candidate list itself from the level-tl norms, into shared memory.
+#define TILE_WARPS 32          // one super-tile node per warp, 32 per block: short look-back chains
+#define TILE_THREADS (TILE_WARPS * 32)
+template <bool DENSE>
+__global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
 {
     __shared__ int s_tile;
-    __shared__ uint32_t s_wsteps[PLAN_WARPS], s_wleaves[PLAN_WARPS];
+    __shared__ uint32_t s_wsteps[TILE_WARPS], s_wleaves[TILE_WARPS];
     __shared__ uint32_t s_base_lo, s_base_hi;
+    __shared__ uint32_t s_ks[DENSE ? TILE_WARPS : 1][DENSE ? 64 : 1];
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
-    const int n_nodes = a.counts_in[0];
-    const int ntiles = (n_nodes + PLAN_WARPS - 1) / PLAN_WARPS;
+    const int n_nodes = DENSE ? (a.St * a.St) : a.counts_in[0];
+    const int ntiles = (n_nodes + TILE_WARPS - 1) / TILE_WARPS;
     const int sub = a.sub, per = 32 / sub;       // lanes per block product, block products per warp pass
     const uint32_t kk = lane % sub;              // my k inside the block
     const uint32_t grp = (lane / sub) * sub;     // first lane of my group
@@ -328,18 +337,34 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
         __syncthreads();
         const int tile = s_tile;
         if (tile >= ntiles) break;
-        const int pidx = tile * PLAN_WARPS + warp;
+        const int pidx = tile * TILE_WARPS + warp;
         const bool valid = pidx < n_nodes;
         uint32_t pm = 0, I = 0, J = 0, rowok = 0;
         int s = 0, e = 0;
+        const uint32_t *ks = DENSE ? s_ks[warp] : a.in.ks;
         if (valid) {
-            pm = a.in.node[pidx];
+            pm = DENSE ? (uint32_t)pidx : a.in.node[pidx];
             morton_decode(pm, I, J);
-            s = a.in.off[pidx];
-            e = a.in.off[pidx + 1];
             for (int d = 0; d < sub; ++d) {
                 const int row = (int)(sub * I + d);
                 if (row >= a.row0 && row < a.row1) rowok |= 1u << d;
+            }
+            if (DENSE) {
+                // candidates K of this node: the level-tl test (symbolic.py:118-125 one level up)
+                if (rowok) {
+                    for (int k0 = 0; k0 < a.St; k0 += 32) {
+                        const int K = k0 + (int)lane;
+                        const bool pass = K < a.St && norm_test(__ldg(a.norm_a_t + (int64_t)I * a.St + K),
+                                                                __ldg(a.norm_bt_t + (int64_t)J * a.St + K), a.tau);
+                        const uint32_t bal = __ballot_sync(FULL_MASK, pass);
+                        if (pass) s_ks[warp][e + __popc(bal & lanemask_lt())] = (uint32_t)K;
+                        e += __popc(bal);
+                    }
+                }
+                __syncwarp();
+            } else {
+                s = a.in.off[pidx];
+                e = a.in.off[pidx + 1];
             }
         }
         // phase 1: count step records and product leaves of this super-tile
@@ -347,7 +372,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
         for (int b = s; b < e; b += per) {
             const int t = b + (int)lane / sub;
             uint32_t live = 0;
-            if (t < e) live = tile_tests(a, I, J, sub * a.in.ks[t] + kk, rowok).live;
+            if (t < e) live = tile_tests(a, I, J, sub * ks[t] + kk, rowok).live;
             const uint32_t bal = __ballot_sync(FULL_MASK, live != 0);
             // one record per group of `sub` lanes with any live task
             uint32_t groups = bal;
@@ -368,15 +393,15 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
         __syncthreads();
         // phase 2: block scan + look-back over (records, product leaves)
         if (warp == 0) {
-            uint32_t vs = lane < PLAN_WARPS ? s_wsteps[lane] : 0u, vl = lane < PLAN_WARPS ? s_wleaves[lane] : 0u;
+            uint32_t vs = lane < TILE_WARPS ? s_wsteps[lane] : 0u, vl = lane < TILE_WARPS ? s_wleaves[lane] : 0u;
             uint32_t is = vs, il = vl;          // inclusive scan over the block's warps
 #pragma unroll
-            for (int d = 1; d < PLAN_WARPS; d <<= 1) {
+            for (int d = 1; d < TILE_WARPS; d <<= 1) {
                 const uint32_t xs = __shfl_up_sync(FULL_MASK, is, d), xl = __shfl_up_sync(FULL_MASK, il, d);
                 if (lane >= (uint32_t)d) { is += xs; il += xl; }
             }
-            const uint32_t rs = __shfl_sync(FULL_MASK, is, PLAN_WARPS - 1), rl = __shfl_sync(FULL_MASK, il, PLAN_WARPS - 1);
-            if (lane < PLAN_WARPS) { s_wsteps[lane] = is - vs; s_wleaves[lane] = il - vl; }
+            const uint32_t rs = __shfl_sync(FULL_MASK, is, TILE_WARPS - 1), rl = __shfl_sync(FULL_MASK, il, TILE_WARPS - 1);
+            if (lane < TILE_WARPS) { s_wsteps[lane] = is - vs; s_wleaves[lane] = il - vl; }
             uint32_t ex_lo, ex_hi;
             lb_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
             if (lane == 0) {
@@ -387,7 +412,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
                 const int64_t tot_s = (int64_t)ex_lo + rs, tot_l = (int64_t)ex_hi + rl;
                 a.counts[0] = (int32_t)tot_l;
                 a.counts[4] = (int32_t)tot_s;
-                a.counts[5] = n_nodes;
+                a.counts[11] = n_nodes;
                 a.tile_off[n_nodes] = (int32_t)tot_s;
                 if (tot_s > a.cap_steps || tot_l > a.cap_leaves) a.counts[2] = 1;
             }
@@ -412,7 +437,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
             LaneTests lt4{0u, 0u, 0u};
             uint32_t K = 0, k = 0;
             if (t < e) {
-                K = a.in.ks[t];
+                K = ks[t];
                 k = sub * K + kk;
                 lt4 = tile_tests(a, I, J, k, rowok);
             }
@@ -462,7 +487,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_tiles_kernel(TileArgs a)
 
 // Longest-first order of the super-tiles for the numeric kernel's dynamic scheduler: a counting
 // sort by step count (any order inside a bin; the product does not depend on it).
-__global__ void __launch_bounds__(256) plan_order_kernel(const int32_t *__restrict__ tile_off, const int32_t *counts,
+__global__ void __launch_bounds__(256) plan_order_kernel(const int32_t *__restrict__ tile_off, int32_t *counts,
                                                          const unsigned int *__restrict__ bins, unsigned int *cursor,
                                                          int32_t *__restrict__ tile_order)
 {
@@ -492,9 +517,12 @@ __global__ void __launch_bounds__(256) plan_order_kernel(const int32_t *__restri
         run += v[x];
     }
     __syncthreads();
-    const int n_nodes = counts[5];
+    const int n_nodes = counts[11];
+    // nodes without records are left out: counts[5] = nodes the numeric kernel has to visit
+    if (blockIdx.x == 0 && t == 0) counts[5] = n_nodes - (int)bins[0];
     for (int idx = blockIdx.x * blockDim.x + t; idx < n_nodes; idx += gridDim.x * blockDim.x) {
         int ns = tile_off[idx + 1] - tile_off[idx];
+        if (ns == 0) continue;
         if (ns >= PLAN_BINS) ns = PLAN_BINS - 1;
         tile_order[s_start[ns] + atomicAdd(&cursor[ns], 1u)] = idx;
     }
@@ -561,11 +589,13 @@ extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, do
     const int l0 = tl < ROOT_MAX_LEVEL ? tl : ROOT_MAX_LEVEL;   // start level
     int32_t *overflow = out->counts + 2, *max_list = out->counts + 3;
     int cur = 0;
+    const bool dense = tl <= 6 && out->leaf_capacity >= (int64_t(1) << (2 * tl));
+    const int grid = SPAMM_NUM_SMS * 4;
+    if (!dense) {
     plan_root_kernel<<<1, ROOT_THREADS, 0, st>>>(a->norm + spamm_level_offset(l0), b->norm_t + spamm_level_offset(l0), l0,
                                         depth - l0, row0, row1, tau, w.buf[cur], w.shared->counts[l0],
                                         out->leaf_capacity, out->step_capacity, overflow);
     SPAMM_CHECK_LAUNCH();
-    const int grid = SPAMM_NUM_SMS * 4;
     for (int lvl = l0; lvl < tl; ++lvl) {
         ExpandArgs x;
         x.norm_a = a->norm + spamm_level_offset(lvl + 1);
@@ -585,7 +615,11 @@ extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, do
         SPAMM_CHECK_LAUNCH();
         cur ^= 1;
     }
+    }
     TileArgs t;
+    t.norm_a_t = a->norm + spamm_level_offset(tl);
+    t.norm_bt_t = b->norm_t + spamm_level_offset(tl);
+    t.St = 1 << tl;
     t.norm_a = a->norm + spamm_level_offset(depth);
     t.norm_bt = b->norm_t + spamm_level_offset(depth);
     t.slot_a = a->slot;
@@ -603,7 +637,8 @@ extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, do
     t.counts = out->counts;
     t.tile_counter = &w.shared->tile_counter[PLAN_MAX_LEVELS];
     t.tile_state = w.tile_state[PLAN_MAX_LEVELS];
-    plan_tiles_kernel<<<grid, PLAN_THREADS, 0, st>>>(t);
+    if (dense) plan_tiles_kernel<true><<<SPAMM_NUM_SMS, TILE_THREADS, 0, st>>>(t);
+    else plan_tiles_kernel<false><<<SPAMM_NUM_SMS * 2, TILE_THREADS, 0, st>>>(t);
     SPAMM_CHECK_LAUNCH();
     plan_order_kernel<<<SPAMM_NUM_SMS, 256, 0, st>>>(out->tile_off, out->counts, w.shared->bins, w.shared->cursor,
                                                      out->tile_order);

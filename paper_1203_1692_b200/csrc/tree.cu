@@ -185,19 +185,19 @@ struct NodeSum {
     __device__ __forceinline__ double total() const { return seen == 1 ? first : __dadd_rn(first, rest); }
 };
 
-// Each block folds a 32x32 region of child level `tc` through up to five levels.
-__global__ void __launch_bounds__(256) interior_kernel(const double *__restrict__ child_sq, float *__restrict__ norm,
-                                                       float *__restrict__ norm_t, double *__restrict__ sq_levels, int tc)
+// One block folds a 32x32 region of child level `tc` (block coordinates bx, by) through up to five
+// levels: the first from global memory, the rest from shared memory.
+__device__ __forceinline__ void interior_fold(const double *__restrict__ child_sq, float *__restrict__ norm,
+                                              float *__restrict__ norm_t, double *__restrict__ sq_levels, int tc, int bx,
+                                              int by, double (*s_sq)[16][16], unsigned char (*s_pr)[16][16])
 {
-    __shared__ double s_sq[2][16][16];
-    __shared__ unsigned char s_pr[2][16][16];
     const int Sc = 1 << tc;
     const int64_t off_c = spamm_level_offset(tc);
     const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
     // level tc-1: parent (pi, pj) from four children in global memory
     {
         const int Sp = Sc >> 1;
-        const int pi = blockIdx.y * 16 + ty, pj = blockIdx.x * 16 + tx;
+        const int pi = by * 16 + ty, pj = bx * 16 + tx;
         bool present = false;
         double sq = 0.0;
         if (pi < Sp && pj < Sp) {
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(256) interior_kernel(const double *__restrict_
         const int pside = side >> 1;
         const int Sp = 1 << t;
         if (ty < pside && tx < pside) {
-            const int pi = blockIdx.y * pside + ty, pj = blockIdx.x * pside + tx;
+            const int pi = by * pside + ty, pj = bx * pside + tx;
             bool present = false;
             double sq = 0.0;
             if (pi < Sp && pj < Sp) {
@@ -252,6 +252,33 @@ __global__ void __launch_bounds__(256) interior_kernel(const double *__restrict_
     }
 }
 
+// ticket (optional, zero on entry): the last block to finish also folds the remaining levels,
+// which then fit one block (tc - 5 <= 5); it leaves the ticket at zero again.
+__global__ void __launch_bounds__(256) interior_kernel(const double *__restrict__ child_sq, float *__restrict__ norm,
+                                                       float *__restrict__ norm_t, double *__restrict__ sq_levels, int tc,
+                                                       unsigned int *ticket)
+{
+    __shared__ double s_sq[2][16][16];
+    __shared__ unsigned char s_pr[2][16][16];
+    __shared__ bool s_last;
+    interior_fold(child_sq, norm, norm_t, sq_levels, tc, blockIdx.x, blockIdx.y, s_sq, s_pr);
+    if (!ticket || tc <= 5) return;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int n = gridDim.x * gridDim.y;
+        s_last = atomicAdd(ticket, 1u) == n - 1;
+        if (s_last) *ticket = 0u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int t2 = tc - 5; t2 > 0; t2 -= 5) {
+        __syncthreads();
+        interior_fold(sq_levels + spamm_level_offset(t2), norm, norm_t, sq_levels, t2, 0, 0, s_sq, s_pr);
+    }
+}
+
 __global__ void transpose_level_kernel(const float *__restrict__ src, float *__restrict__ dst, int S)
 {
     __shared__ float tile[32][33];
@@ -265,16 +292,18 @@ __global__ void transpose_level_kernel(const float *__restrict__ src, float *__r
         if (x < S && y + r < S) dst[(int64_t)(y + r) * S + x] = tile[threadIdx.x][threadIdx.y + r];
 }
 
-static int launch_interior(const double *leaf_sq, int depth, float *norm, float *norm_t, double *sq_levels,
-                           cudaStream_t st)
+int spamm_launch_interior(const double *leaf_sq, int depth, float *norm, float *norm_t, double *sq_levels,
+                          unsigned int *ticket, cudaStream_t st)
 {
     int tc = depth;
     const double *child = leaf_sq;
     while (tc > 0) {
         const int Sp = 1 << (tc - 1);
         const int g = (Sp + 15) / 16;
-        interior_kernel<<<dim3(g, g), 256, 0, st>>>(child, norm, norm_t, sq_levels, tc);
+        const bool fuse = ticket && tc > 5 && tc - 5 <= 5;      // the rest fits one block
+        interior_kernel<<<dim3(g, g), 256, 0, st>>>(child, norm, norm_t, sq_levels, tc, fuse ? ticket : nullptr);
         SPAMM_CHECK_LAUNCH();
+        if (fuse) break;
         tc = (tc - 5 > 0) ? tc - 5 : 0;
         child = sq_levels + spamm_level_offset(tc);
     }
@@ -293,7 +322,7 @@ extern "C" int spamm_build_interior(const double *leaf_sq, int depth, float *nor
         transpose_level_kernel<<<tg, tb, 0, st>>>(norm + off, norm_t + off, L);
         SPAMM_CHECK_LAUNCH();
     }
-    return launch_interior(leaf_sq, depth, norm, norm_t, sq_levels, st);
+    return spamm_launch_interior(leaf_sq, depth, norm, norm_t, sq_levels, nullptr, st);
 }
 
 // Packed leaves -> norms in compute_norms order (core.py:108-116): sub-block sums as above,
@@ -373,6 +402,20 @@ __global__ void scatter_leaves_kernel(const uint32_t *__restrict__ keys, const d
         norm_t[(int64_t)j * L + i] = nv;
         leaf_sq_grid[(int64_t)i * L + j] = sq;
     }
+}
+
+int spamm_clear_leaf_grids(int depth, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid,
+                           cudaStream_t st)
+{
+    if (depth < 0 || depth > 15) return SPAMM_EINVAL;
+    const int L = 1 << depth;
+    const int64_t cells = (int64_t)L * L;
+    const int64_t off = spamm_level_offset(depth);
+    int blocks = (int)((cells + 255) / 256);
+    if (blocks > SPAMM_NUM_SMS * 16) blocks = SPAMM_NUM_SMS * 16;
+    clear_grids_kernel<<<blocks, 256, 0, st>>>(cells, slot, slot_t, norm + off, norm_t + off, leaf_sq_grid);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
 }
 
 int spamm_index_leaves_impl(const uint32_t *keys, const double *leaf_sq_packed, int64_t nleaf, const int32_t *nleaf_dev,

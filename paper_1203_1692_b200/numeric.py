@@ -16,7 +16,7 @@ import torch
 
 from . import _lib
 from .symbolic import MultiplyPlan, build_plan
-from .tree import QuadtreeMatrix, _stream
+from .tree import QuadtreeMatrix, _Span, _stream
 
 GRANULARITIES = ("fine4", "coarse16")
 
@@ -54,11 +54,11 @@ class ExecCounters:
         self._dev, self._total, self._fine, self._events, self._plan = _dev, _total, _fine, _events, _plan
 
     def _fetch(self):
-        if self._plan is not None:                 # asynchronous multiply: the task count arrives with the plan
+        if self._plan is not None:                 # asynchronous multiply: everything arrives with the plan counts
             plan, self._plan = self._plan, None
-            self._total = 64 * plan.n_tasks        # (resolving the plan may swap self._dev after an overflow)
-            if not self._fine:
-                self._products4, self._dev = self._total, None
+            self._total = 64 * plan.n_tasks
+            self._products4 = plan._products4 if self._fine else self._total
+            self._skipped4 = self._total - self._products4 if self._fine else 0
         if self._dev is not None:
             self._products4 = int(self._dev[0].item())
             self._skipped4 = self._total - self._products4 if self._fine else 0
@@ -227,7 +227,7 @@ def multiply(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig | None = 
 def multiply_async(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig, c: QuadtreeMatrix | None = None,
                    row_range: tuple[int, int] | None = None) -> tuple[QuadtreeMatrix, MultiplyPlan, ExecCounters]:
     """C = alpha A B through ``spamm_multiply``: one C call, no host synchronisation."""
-    from .symbolic import PlanAlloc, grow_capacity, plan_capacity, remember_capacity
+    from .symbolic import plan_capacity
     from .tree import _Grids
 
     if a.n_b != b.n_b:
@@ -250,48 +250,66 @@ def multiply_async(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig, c:
     hint_key, caps = plan_capacity(a, b, cfg.tau, depth, r0, r1)
     cd, cells, total = c.depth, 1 << (2 * c.depth), _lib.level_total(c.depth)
 
+    tl = max(depth - 2, 0)
+    i32t, f32t, f64t = torch.int32, torch.float32, torch.float64
+
     def launch(step_cap: int, leaf_cap: int):
+        """One allocation, one C call; returns the arena and its layout."""
+        if tl <= 6:     # room for every super-tile node: lets the planner start densely at that level
+            leaf_cap = max(leaf_cap, 1 << (2 * tl))
+        lay = _arena_layout(depth, cd, step_cap, leaf_cap)
+        arena = torch.empty((lay.total,), dtype=torch.uint8, device=dev)
         va, vb = a.view(depth), b.view(depth)
-        pb = PlanAlloc(dev, depth, step_cap, leaf_cap)
-        vals = torch.empty((leaf_cap, _lib.REC), dtype=torch.float32, device=dev)
-        vals_t = torch.empty((leaf_cap, _lib.REC), dtype=torch.float32, device=dev)
-        leaf_sq = torch.empty((leaf_cap,), dtype=torch.float64, device=dev)
-        grids = _Grids(cd, torch.empty((cells,), dtype=torch.int32, device=dev),
-                       torch.empty((cells,), dtype=torch.int32, device=dev),
-                       torch.empty((total,), dtype=torch.float32, device=dev),
-                       torch.empty((total,), dtype=torch.float32, device=dev))
-        sq_grid = torch.empty((cells,), dtype=torch.float64, device=dev)
-        sq_levels = torch.empty((total,), dtype=torch.float64, device=dev)
-        counters_dev = torch.zeros((2,), dtype=torch.int64, device=dev)
-        prod = _lib.ProductBuffers(vals.data_ptr(), vals_t.data_ptr(), leaf_sq.data_ptr(), grids.slot.data_ptr(),
-                                   grids.slot_t.data_ptr(), grids.norm.data_ptr(), grids.norm_t.data_ptr(),
-                                   sq_grid.data_ptr(), sq_levels.data_ptr(), cd)
-        _lib.check(lib.spamm_multiply(C.byref(va), C.byref(vb), float(cfg.tau), gran, int(cfg.exact), alpha32, r0, r1,
-                                      C.byref(pb.struct), pb.ws.data_ptr(), pb.ws_bytes, C.byref(prod),
-                                      counters_dev.data_ptr(), _stream()), "multiply")
-        return pb, vals, vals_t, leaf_sq, grids, counters_dev
+        _lib.check(lib.spamm_multiply_arena(C.byref(va), C.byref(vb), float(cfg.tau), gran, int(cfg.exact), alpha32,
+                                            r0, r1, cd, step_cap, leaf_cap, arena.data_ptr(), lay.total, _stream()),
+                   "multiply")
+        return arena, lay, step_cap, leaf_cap
+
+    def bind(plan: MultiplyPlan, c: QuadtreeMatrix, arena, lay, step_cap: int, leaf_cap: int) -> None:
+        """Point the plan and the product tree at their regions of the arena (views made on demand)."""
+        plan.steps = _Span(arena, lay.steps, (step_cap, _lib.STEP_WORDS), i32t)
+        plan.c_keys = _Span(arena, lay.c_keys, (leaf_cap,), i32t)
+        plan.tile_off = _Span(arena, lay.tile_off, (leaf_cap + 1,), i32t)
+        plan.tile_order = _Span(arena, lay.tile_order, (leaf_cap,), i32t)
+        plan.counts = _Span(arena, lay.counts, (_lib.PLAN_COUNTS,), i32t)
+        grids = _Grids(cd, _Span(arena, lay.slot, (cells,), i32t), _Span(arena, lay.slot_t, (cells,), i32t),
+                       _Span(arena, lay.norm, (total,), f32t), _Span(arena, lay.norm_t, (total,), f32t))
+        c._adopt_product(plan._c_keys, _Span(arena, lay.values, (leaf_cap, _lib.REC), f32t),
+                         _Span(arena, lay.values_t, (leaf_cap, _lib.REC), f32t),
+                         _Span(arena, lay.leaf_sq, (leaf_cap,), f64t), grids, plan._count_leaves)
 
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    pb, vals, vals_t, leaf_sq, grids, counters_dev = launch(*caps)
+    arena, lay, step_cap, leaf_cap = launch(*caps)
     e1.record()
-    plan = MultiplyPlan(cfg.tau, depth, None, None, None, pb.steps, pb.c_keys, pb.tile_off, pb.tile_order, pb.counts,
-                        a, b, (r0, r1))
-    counters = ExecCounters(_dev=counters_dev, _fine=fine, _events=(e0, e1), _plan=plan)
-    c._adopt_product(pb.c_keys, vals, vals_t, leaf_sq, grids, plan._count_leaves)
-    plan._tokens = (id(a), a._rev, id(b), b._rev)
-    plan._async = _AsyncProduct(launch, depth, hint_key, (pb.step_cap, pb.leaf_cap), plan, c, counters)
+    plan = MultiplyPlan(cfg.tau, depth, None, None, None, None, None, None, None, None, a, b, (r0, r1))
+    bind(plan, c, arena, lay, step_cap, leaf_cap)
+    counters = ExecCounters(_fine=fine, _events=(e0, e1), _plan=plan)
+    plan._async = _AsyncProduct(launch, bind, depth, hint_key, (step_cap, leaf_cap), plan, c)
     return c, plan, counters
+
+
+_layouts: dict[tuple, "_lib.ArenaLayout"] = {}
+
+
+def _arena_layout(depth: int, c_depth: int, step_cap: int, leaf_cap: int):
+    key = (depth, c_depth, step_cap, leaf_cap)
+    lay = _layouts.get(key)
+    if lay is None:
+        lay = _lib.ArenaLayout()
+        _lib.check(_lib.lib().spamm_multiply_arena_layout(depth, c_depth, step_cap, leaf_cap, C.byref(lay)), "layout")
+        _layouts[key] = lay
+    return lay
 
 
 class _AsyncProduct:
     """What a lazily resolved plan needs to repeat its multiply after a buffer overflow.  Holds the
     plan, the product tree and the counters weakly, so nothing here keeps device memory alive."""
 
-    def __init__(self, launch, depth, hint_key, caps, plan, c, counters):
+    def __init__(self, launch, bind, depth, hint_key, caps, plan, c):
         import weakref
-        self.launch, self.depth, self.hint_key, self.caps = launch, depth, hint_key, caps
-        self.plan, self.c, self.counters = weakref.ref(plan), weakref.ref(c), weakref.ref(counters)
+        self.launch, self.bind, self.depth, self.hint_key, self.caps = launch, bind, depth, hint_key, caps
+        self.plan, self.c = weakref.ref(plan), weakref.ref(c)
 
     def on_overflow(self, cnt) -> None:
         """A capacity was too small: repeat, synchronously, until the buffers fit."""
@@ -299,20 +317,16 @@ class _AsyncProduct:
         step_cap, leaf_cap = self.caps
         while True:
             step_cap, leaf_cap = grow_capacity(self.depth, step_cap, leaf_cap, cnt)
-            npb, nvals, nvals_t, nleaf_sq, ngrids, ncounters = self.launch(step_cap, leaf_cap)
-            cnt = npb.counts.tolist()
+            arena, lay, step_cap, leaf_cap = self.launch(step_cap, leaf_cap)
+            cnt = _Span(arena, lay.counts, (_lib.PLAN_COUNTS,), torch.int32).tensor().tolist()
             if not cnt[2]:
                 break
-        plan, c, counters = self.plan(), self.c(), self.counters()
+        plan, c = self.plan(), self.c()
         if plan is not None:
-            plan.steps, plan.c_keys, plan.tile_off, plan.tile_order, plan.counts = (
-                npb.steps, npb.c_keys, npb.tile_off, npb.tile_order, npb.counts)
-        if c is not None and plan is not None:
-            rev = c._rev
-            c._adopt_product(npb.c_keys, nvals, nvals_t, nleaf_sq, ngrids, plan._count_leaves)
-            c._rev = rev
-        if counters is not None:
-            counters._dev = ncounters
+            target = c if c is not None else QuadtreeMatrix(plan._a.m, plan._b.n, 16, device=plan._a.device)
+            rev = target._rev
+            self.bind(plan, target, arena, lay, step_cap, leaf_cap)
+            target._rev = rev
 
     def on_resolved(self, cnt) -> None:
         from .symbolic import remember_capacity

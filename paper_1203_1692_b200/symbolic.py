@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib, morton
-from .tree import QuadtreeMatrix, _stream
+from .tree import QuadtreeMatrix, _lazy_tensor, _ptr, _stream
 
 
 @dataclass(slots=True)
@@ -76,6 +76,7 @@ class MultiplyPlan:
             raise RuntimeError("plan buffers overflowed")
         self._n_cleaves, self._n_steps = cnt[0], cnt[4]
         self._n_tasks = (cnt[6] & 0xFFFFFFFF) | ((cnt[7] & 0xFFFFFFFF) << 32)
+        self._products4 = (cnt[8] & 0xFFFFFFFF) | ((cnt[9] & 0xFFFFFFFF) << 32)   # spamm_multiply only
         if self._async is not None:
             self._async.on_resolved(cnt)
             self._async = None
@@ -102,9 +103,15 @@ class MultiplyPlan:
         return self.n_tasks
 
     def buffers(self) -> _lib.PlanBuffers:
-        return _lib.PlanBuffers(self.steps.data_ptr(), self.c_keys.data_ptr(), self.tile_off.data_ptr(),
-                                self.tile_order.data_ptr(), self.steps.shape[0], self.c_keys.shape[0],
-                                self.counts.data_ptr())
+        return _lib.PlanBuffers(_ptr(self._steps), _ptr(self._c_keys), _ptr(self._tile_off), _ptr(self._tile_order),
+                                self._steps.shape[0], self._c_keys.shape[0], _ptr(self._counts))
+
+    # device arrays; after an asynchronous multiply they are regions of its arena (tree._Span)
+    steps = _lazy_tensor("steps")
+    c_keys = _lazy_tensor("c_keys")
+    tile_off = _lazy_tensor("tile_off")
+    tile_order = _lazy_tensor("tile_order")
+    counts = _lazy_tensor("counts")
 
     # -- host views ---------------------------------------------------------------------------
     def step_records(self) -> np.ndarray:
@@ -266,6 +273,9 @@ class PlanAlloc:
     """Device buffers of one plan (``spamm_plan_buffers``) plus the planner's workspace."""
 
     def __init__(self, dev, depth: int, step_cap: int, leaf_cap: int):
+        tl = max(depth - 2, 0)
+        if tl <= 6:     # room for every super-tile node: lets the planner start densely at that level
+            leaf_cap = max(leaf_cap, 1 << (2 * tl))
         self.step_cap, self.leaf_cap = step_cap, leaf_cap
         self.steps = torch.empty((step_cap, _lib.STEP_WORDS), dtype=torch.int32, device=dev)
         self.c_keys = torch.empty((leaf_cap,), dtype=torch.int32, device=dev)

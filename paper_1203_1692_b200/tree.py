@@ -43,8 +43,46 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
-def _ptr(t: torch.Tensor | None) -> int | None:
-    return None if t is None else t.data_ptr()
+class _Span:
+    """A typed region of one arena tensor (the single allocation of an asynchronous multiply).
+    The kernels only need its address; the tensor view is made when the host first touches it."""
+
+    __slots__ = ("arena", "off", "shape", "dtype", "_t")
+
+    def __init__(self, arena: torch.Tensor, off: int, shape: tuple, dtype: torch.dtype):
+        self.arena, self.off, self.shape, self.dtype, self._t = arena, int(off), shape, dtype, None
+
+    def ptr(self) -> int:
+        return self.arena.data_ptr() + self.off
+
+    def tensor(self) -> torch.Tensor:
+        if self._t is None:
+            n = int(np.prod(self.shape)) * torch.empty((), dtype=self.dtype).element_size()
+            self._t = self.arena[self.off:self.off + n].view(self.dtype).view(self.shape)
+        return self._t
+
+
+def _tensor(x):
+    return x.tensor() if isinstance(x, _Span) else x
+
+
+def _ptr(x) -> int | None:
+    if x is None:
+        return None
+    return x.ptr() if isinstance(x, _Span) else x.data_ptr()
+
+
+def _lazy_tensor(name: str):
+    """Attribute that may hold a tensor or a _Span; reads always give a tensor."""
+    slot = "_" + name
+
+    def get(self):
+        return _tensor(getattr(self, slot))
+
+    def put(self, value):
+        setattr(self, slot, value)
+
+    return property(get, put)
 
 
 class DenseMatrix:
@@ -74,10 +112,15 @@ class TreeNode:
 class _Grids:
     """Slot grids and norm pyramid of a tree indexed at one depth."""
 
-    __slots__ = ("depth", "slot", "slot_t", "norm", "norm_t")
+    __slots__ = ("depth", "_slot", "_slot_t", "_norm", "_norm_t")
 
     def __init__(self, depth, slot, slot_t, norm, norm_t):
-        self.depth, self.slot, self.slot_t, self.norm, self.norm_t = depth, slot, slot_t, norm, norm_t
+        self.depth, self._slot, self._slot_t, self._norm, self._norm_t = depth, slot, slot_t, norm, norm_t
+
+    slot = _lazy_tensor("slot")
+    slot_t = _lazy_tensor("slot_t")
+    norm = _lazy_tensor("norm")
+    norm_t = _lazy_tensor("norm_t")
 
 
 class QuadtreeMatrix:
@@ -110,9 +153,14 @@ class QuadtreeMatrix:
         self._nleaf = int(value)
         self._nleaf_source = None
 
+    keys = _lazy_tensor("keys")
+    values = _lazy_tensor("values")
+    values_t = _lazy_tensor("values_t")
+    leaf_sq = _lazy_tensor("leaf_sq")
+
     def _leaf_bound(self) -> int:
         """Stored leaves, or their upper bound while the count is still on the device."""
-        return self._nleaf if self._nleaf is not None else int(self.keys.shape[0])
+        return self._nleaf if self._nleaf is not None else int(self._keys.shape[0])
 
     def _adopt_product(self, keys, values, values_t, leaf_sq, grids: "_Grids", count_source) -> None:
         """Take over the buffers an asynchronous multiply is filling (capacity sized)."""
@@ -263,9 +311,9 @@ class QuadtreeMatrix:
         g = self.grids(depth)
         nz = self._nleaf is None or self._nleaf > 0        # do not force a pending count to the host
         return _lib.TreeView(self.m, self.n, g.depth, self._leaf_bound() if nz else 0,
-                             _ptr(self.keys) if nz else None, _ptr(self.values) if nz else None,
-                             _ptr(self.values_t) if nz else None,
-                             g.slot.data_ptr(), g.slot_t.data_ptr(), g.norm.data_ptr(), g.norm_t.data_ptr())
+                             _ptr(self._keys) if nz else None, _ptr(self._values) if nz else None,
+                             _ptr(self._values_t) if nz else None,
+                             _ptr(g._slot), _ptr(g._slot_t), _ptr(g._norm), _ptr(g._norm_t))
 
     def _flush_guard(self) -> None:
         if self._pending:
