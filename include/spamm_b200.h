@@ -108,6 +108,10 @@ int spamm_build_interior(const double *leaf_sq, int depth, float *norm, float *n
 int spamm_leaf_norms_packed(float *values, int64_t nleaf, float *values_t, double *leaf_sq,
                             void *stream);
 
+/* values_t records from values records whose sub-norm tails are already filled (leaves received
+ * from another GPU keep the norms their owner computed): transposition only. */
+int spamm_transpose_records(const float *values, int64_t nleaf, float *values_t, void *stream);
+
 /* Scatter packed leaves (keys ascending, leaf_sq) into the grids of a depth-`depth` tree:
  * slot, slot_t, the leaf level of norm/norm_t and the double leaf_sq grid (all L*L). */
 int spamm_index_leaves(const uint32_t *keys, const double *leaf_sq_packed, int64_t nleaf, int depth,
@@ -169,6 +173,10 @@ size_t spamm_plan_workspace_bytes(int depth, int64_t step_capacity, int64_t leaf
 int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, double tau,
                int32_t row0, int32_t row1, const spamm_plan_buffers *out,
                void *ws, size_t ws_bytes, void *stream);
+
+/* Surviving tasks per row of product leaves, row_tasks [1 << depth] (zeroed by the call): the
+ * quantity the multi-GPU split balances when it hands row blocks of C to the ranks. */
+int spamm_plan_row_counts(const spamm_plan_buffers *plan, int depth, int32_t *row_tasks, void *stream);
 
 /* ---- numeric phase: execute_plan (numeric.py:138-284) ------------------------- */
 

@@ -66,11 +66,13 @@ SIGNATURES = {
     "spamm_pack_leaves": (C.c_int, [vp, i64, i64, i64, C.c_int, vp, i64, vp, vp, vp, vp]),
     "spamm_build_interior": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int, vp]),
     "spamm_leaf_norms_packed": (C.c_int, [vp, i64, vp, vp, vp]),
+    "spamm_transpose_records": (C.c_int, [vp, i64, vp, vp]),
     "spamm_index_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp]),
     "spamm_to_dense": (C.c_int, [C.POINTER(TreeView), vp, i64, vp]),
     "spamm_plan_workspace_bytes": (sz, [C.c_int, i64, i64]),
     "spamm_plan": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, i32, i32,
                              C.POINTER(PlanBuffers), vp, sz, vp]),
+    "spamm_plan_row_counts": (C.c_int, [C.POINTER(PlanBuffers), C.c_int, vp, vp]),
     "spamm_execute": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), C.POINTER(PlanBuffers), i64, i64,
                                 f64, f32, C.c_int, C.c_int, vp, vp, vp, vp, vp]),
     "spamm_multiply": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, C.c_int, C.c_int, f32, i32, i32,

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_expand_kernel(ExpandArgs a)
     __shared__ uint32_t s_base_lo, s_base_hi;
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
-    const int n_nodes = a.counts_in[0];
+    const int n_nodes = *a.overflow ? 0 : a.counts_in[0];   // after an overflow the lists above are incomplete
     const int ntiles = (n_nodes + PLAN_WARPS - 1) / PLAN_WARPS;
     for (;;) {
         __syncthreads();
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
     __shared__ uint32_t s_ks[DENSE ? TILE_WARPS : 1][DENSE ? 64 : 1];
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
-    const int n_nodes = DENSE ? (a.St * a.St) : a.counts_in[0];
+    const int n_nodes = DENSE ? (a.St * a.St) : (a.counts[2] ? 0 : a.counts_in[0]);
     const int ntiles = (n_nodes + TILE_WARPS - 1) / TILE_WARPS;
     const int sub = a.sub, per = 32 / sub;       // lanes per block product, block products per warp pass
     const uint32_t kk = lane % sub;              // my k inside the block
@@ -563,6 +563,36 @@ static PlanWorkspace carve(void *ws, int64_t list_cap, int64_t node_cap)
     }
     w.total = o;
     return w;
+}
+
+// Surviving tasks per row of product leaves: what the multi-GPU split balances (rows of C are
+// handed to ranks in contiguous blocks of about equal task count).
+__global__ void plan_row_counts_kernel(const spamm_step *__restrict__ steps, const int32_t *__restrict__ counts,
+                                       int sub_shift, int32_t *__restrict__ row_tasks)
+{
+    const int nsteps = counts[2] ? 0 : counts[4];
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nsteps; s += gridDim.x * blockDim.x) {
+        const uint4 head = *reinterpret_cast<const uint4 *>(steps + s);
+        const uint4 live = *(reinterpret_cast<const uint4 *>(steps + s) + 2);
+        uint32_t ti, tj;
+        morton_decode(head.w, ti, tj);
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            const uint32_t m = step_rowmask(d);
+            const int c = __popc(live.x & m) + __popc(live.y & m) + __popc(live.z & m) + __popc(live.w & m);
+            if (c) atomicAdd(&row_tasks[(ti << sub_shift) + d], c);
+        }
+    }
+}
+
+extern "C" int spamm_plan_row_counts(const spamm_plan_buffers *plan, int depth, int32_t *row_tasks, void *stream)
+{
+    if (!plan || !row_tasks || depth < 0 || depth > 15) return SPAMM_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(row_tasks, 0, sizeof(int32_t) << depth, st) != cudaSuccess) return SPAMM_ECUDA;
+    plan_row_counts_kernel<<<SPAMM_NUM_SMS * 4, 256, 0, st>>>(plan->steps, plan->counts, depth >= 2 ? 2 : depth, row_tasks);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
 }
 
 extern "C" size_t spamm_plan_workspace_bytes(int depth, int64_t step_capacity, int64_t leaf_capacity)

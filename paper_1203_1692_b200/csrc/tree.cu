@@ -373,6 +373,30 @@ extern "C" int spamm_leaf_norms_packed(float *values, int64_t nleaf, float *valu
     return SPAMM_OK;
 }
 
+// values -> values_t for leaves whose norms are already in the record tails (e.g. leaves that
+// arrived from another GPU): transposes the 16x16 values and the 4x4 sub-norm tail, nothing else.
+__global__ void __launch_bounds__(256) transpose_records_kernel(const float *__restrict__ values,
+                                                                float *__restrict__ values_t)
+{
+    __shared__ float tile[16][17];
+    const int64_t s = blockIdx.x;
+    const int r = threadIdx.x >> 4, c = threadIdx.x & 15;
+    tile[r][c] = values[s * SPAMM_REC + threadIdx.x];
+    __syncthreads();
+    values_t[s * SPAMM_REC + threadIdx.x] = tile[c][r];
+    if (threadIdx.x < 16)   // values tail is [q*4+p], values_t tail is [p*4+q]
+        values_t[s * SPAMM_REC + 256 + (threadIdx.x & 3) * 4 + (threadIdx.x >> 2)] = values[s * SPAMM_REC + 256 + threadIdx.x];
+}
+
+extern "C" int spamm_transpose_records(const float *values, int64_t nleaf, float *values_t, void *stream)
+{
+    if (nleaf == 0) return SPAMM_OK;
+    if (!values || !values_t || nleaf < 0) return SPAMM_EINVAL;
+    transpose_records_kernel<<<(unsigned)nleaf, 256, 0, (cudaStream_t)stream>>>(values, values_t);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
+}
+
 // Grids of a tree given by packed leaves: clear, then scatter.
 __global__ void clear_grids_kernel(int64_t cells, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t,
                                    double *leaf_sq_grid)

@@ -1,0 +1,236 @@
+"""Row-block sharding of the SpAMM product across the GPUs of one box.
+
+The reference is single process (`SPEC.md:542` lists distribution as a non-goal); this is the
+split BASELINE.json's north_star asks for.  Every product leaf C(i,j) has exactly one owner and
+accumulates over k locally, so no reduction crosses ranks and the ascending-k order -- hence the
+bitwise result -- is the same for any number of ranks.
+
+* Operands enter row-sharded: rank r holds the stored leaves of its block of leaf rows, as a
+  ``PackedShard`` (keys, 272-float leaf records with their sub-norm tails, leaf square sums).
+  Block boundaries are multiples of 4 leaf rows, so every aligned 4x4 block of leaves -- the unit
+  the numeric kernel stages with one bulk copy -- has one owner and stays contiguous.
+* One exchange step: an all-gather of the shards (NCCL over NVLink/NVSwitch; only stored leaves
+  travel).  The transposed copies are rebuilt locally instead of being sent.
+* Every rank then plans the product on the (replicated) norm pyramids, counts the surviving tasks
+  per leaf row, cuts the rows of C into contiguous blocks of about equal task count, and runs the
+  fused multiply restricted to its own block (``row_range``).
+
+The collective and partition logic is plain ``torch.distributed`` on whatever device the tensors
+live on, so it is covered on CPU with the gloo backend (tests/test_parallel.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROW_ALIGN = 4      # leaf rows; shard boundaries are multiples of this
+
+
+@dataclass
+class PackedShard:
+    """Stored leaves of a block of leaf rows (any device)."""
+
+    keys: torch.Tensor       # (n,) int32 Morton keys in GLOBAL leaf coordinates
+    records: torch.Tensor    # (n, 272) float32: row-major leaf values + transposed sub-norm tail
+    leaf_sq: torch.Tensor    # (n,) float64 leaf square sums
+
+    @property
+    def n(self) -> int:
+        return int(self.keys.shape[0])
+
+
+def even_row_split(nrows: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous blocks of leaf rows of (nearly) equal height, boundaries aligned to ROW_ALIGN."""
+    units = -(-nrows // ROW_ALIGN)
+    cuts = [min(nrows, ROW_ALIGN * ((units * r) // world)) for r in range(world + 1)]
+    cuts[-1] = nrows
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def balanced_row_split(row_tasks: np.ndarray, world: int) -> list[tuple[int, int]]:
+    """Contiguous blocks of leaf rows with about equal numbers of surviving tasks.
+
+    Cut r sits where the running task count first reaches r/world of the total, rounded to
+    ROW_ALIGN rows; every rank evaluates this on the same counts and gets the same answer."""
+    row_tasks = np.asarray(row_tasks, np.int64)
+    nrows = int(row_tasks.shape[0])
+    total = int(row_tasks.sum())
+    if total == 0:
+        return even_row_split(nrows, world)
+    csum = np.concatenate([[0], np.cumsum(row_tasks)])
+    cuts = [0]
+    for r in range(1, world):
+        x = int(np.searchsorted(csum, total * r / world, side="left"))
+        x = min(nrows, max(cuts[-1], ROW_ALIGN * int(round(x / ROW_ALIGN))))
+        cuts.append(x)
+    cuts.append(nrows)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def _spread16(x: torch.Tensor) -> torch.Tensor:
+    x = x & 0xFFFF
+    x = (x | (x << 8)) & 0x00FF00FF
+    x = (x | (x << 4)) & 0x0F0F0F0F
+    x = (x | (x << 2)) & 0x33333333
+    x = (x | (x << 1)) & 0x55555555
+    return x
+
+
+def _squeeze16(x: torch.Tensor) -> torch.Tensor:
+    x = x & 0x55555555
+    x = (x | (x >> 1)) & 0x33333333
+    x = (x | (x >> 2)) & 0x0F0F0F0F
+    x = (x | (x >> 4)) & 0x00FF00FF
+    x = (x | (x >> 8)) & 0x0000FFFF
+    return x
+
+
+def shift_keys(keys: torch.Tensor, row_offset: int) -> torch.Tensor:
+    """Morton keys of leaves (i, j) -> keys of (i + row_offset, j) (row bit above column bit)."""
+    k = keys.to(torch.int64)
+    i = _squeeze16(k >> 1) + int(row_offset)
+    j = _squeeze16(k)
+    return ((_spread16(i) << 1) | _spread16(j)).to(torch.int32)
+
+
+def shard_from_dense_rows(dense_rows, row0_leaf: int, device=None) -> PackedShard:
+    """Shard of the leaf rows starting at ``row0_leaf`` from the matching rows of the dense matrix
+    (``QuadtreeMatrix.from_dense`` on the row block, keys moved to global coordinates)."""
+    from .tree import QuadtreeMatrix
+    if row0_leaf % ROW_ALIGN:
+        raise ValueError(f"row blocks must start at a multiple of {ROW_ALIGN} leaf rows")
+    local = QuadtreeMatrix.from_dense(dense_rows, device=device)
+    n = local.nleaf
+    if n == 0:
+        dev = local.device
+        return PackedShard(torch.empty((0,), dtype=torch.int32, device=dev),
+                           torch.empty((0, 272), dtype=torch.float32, device=dev),
+                           torch.empty((0,), dtype=torch.float64, device=dev))
+    return PackedShard(shift_keys(local.keys[:n], row0_leaf), local.values[:n], local._packed_leaf_sq()[:n])
+
+
+def shard_of_tree(tree, r0: int, r1: int) -> PackedShard:
+    """The stored leaves of leaf rows [r0, r1) of a whole tree (benchmarks and tests)."""
+    n = tree.nleaf
+    keys = tree.keys[:n]
+    rows = _squeeze16(keys.to(torch.int64) >> 1)
+    sel = torch.nonzero((rows >= r0) & (rows < r1)).flatten()
+    return PackedShard(keys[sel].contiguous(), tree.values[:n][sel].contiguous(),
+                       tree._packed_leaf_sq()[:n][sel].contiguous())
+
+
+def allgather_shards(shard: PackedShard, group=None) -> PackedShard:
+    """Every rank's shard, concatenated in rank order.  Sizes differ, so the counts are gathered
+    first and the payloads padded to the largest shard (one all-gather per array)."""
+    world = dist.get_world_size(group)
+    dev = shard.keys.device
+    counts = [torch.zeros((1,), dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(counts, torch.tensor([shard.n], dtype=torch.int64, device=dev), group=group)
+    counts = [int(c.item()) for c in counts]
+    cap = max(max(counts), 1)
+
+    def gather(x: torch.Tensor) -> torch.Tensor:
+        pad = torch.zeros((cap,) + tuple(x.shape[1:]), dtype=x.dtype, device=dev)
+        pad[: x.shape[0]] = x
+        outs = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(outs, pad, group=group)
+        return torch.cat([outs[r][: counts[r]] for r in range(world)], dim=0)
+
+    return PackedShard(gather(shard.keys), gather(shard.records), gather(shard.leaf_sq))
+
+
+def tree_from_shard(m: int, n: int, shard: PackedShard, device=None):
+    """Whole-matrix tree from gathered leaves: transposed copies, leaf grids and the norm pyramid are
+    rebuilt on the device; the leaf norms are the ones their owners computed."""
+    from . import _lib
+    from .tree import QuadtreeMatrix, _stream
+    q = QuadtreeMatrix(m, n, device=device)
+    cnt = shard.n
+    if cnt == 0:
+        return q
+    keys = shard.keys.to(q.device).contiguous()
+    values = shard.records.to(q.device).contiguous()
+    leaf_sq = shard.leaf_sq.to(q.device).contiguous()
+    values_t = torch.empty_like(values)
+    _lib.check(_lib.lib().spamm_transpose_records(values.data_ptr(), cnt, values_t.data_ptr(), _stream()),
+               "transpose_records")
+    q._adopt_packed(keys, values, values_t, leaf_sq, cnt)
+    q._keys_sorted = False          # rank order, not one ascending Morton sequence
+    return q
+
+
+def row_task_counts(plan, depth: int) -> torch.Tensor:
+    """Surviving tasks per leaf row of the product (device int32 tensor of length 2^depth)."""
+    import ctypes as C
+    from . import _lib
+    from .tree import _stream
+    out = torch.empty((1 << depth,), dtype=torch.int32, device=plan.steps.device)
+    bufs = plan.buffers()
+    _lib.check(_lib.lib().spamm_plan_row_counts(C.byref(bufs), depth, out.data_ptr(), _stream()), "row_counts")
+    return out
+
+
+def multiply_sharded(a_shard: PackedShard, b_shard: PackedShard | None, shape_a: tuple[int, int],
+                     shape_b: tuple[int, int], cfg, group=None, device=None):
+    """C = A B with C's leaf rows split across the ranks of ``group``.
+
+    ``a_shard`` / ``b_shard`` are this rank's row blocks of the operands (``b_shard is None`` means
+    B is A).  Returns ``(c, plan, counters, (r0, r1))``: ``c`` has the global shape and holds this
+    rank's rows [r0, r1) of product leaves."""
+    from .numeric import multiply_async
+    from .symbolic import build_plan
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    a_full = tree_from_shard(shape_a[0], shape_a[1], allgather_shards(a_shard, group), device)
+    b_full = a_full if b_shard is None else tree_from_shard(shape_b[0], shape_b[1],
+                                                            allgather_shards(b_shard, group), device)
+    # balance: every rank plans the whole product on the replicated norms (cheap) and cuts alike
+    plan = build_plan(a_full, b_full, cfg.tau)
+    counts = row_task_counts(plan, plan.depth).cpu().numpy()
+    nrows = -(-shape_a[0] // 16)
+    r0, r1 = balanced_row_split(counts[:nrows], world)[rank]
+    c, myplan, counters = multiply_async(a_full, b_full, cfg, None, row_range=(r0, r1))
+    return c, myplan, counters, (r0, r1)
+
+
+def bench_sharded(P, torch_mod, dist_mod, a_dense, b_dense, cfg, steps: int, warmup: int, flush):
+    """bench.py's N > 1 leg: config 5 (or any workload) with the all-gather inside the timed region."""
+    rank, world = dist_mod.get_rank(), dist_mod.get_world_size()
+    m = a_dense.shape[0]
+    nrows = -(-m // 16)
+    r0, r1 = even_row_split(nrows, world)[rank]
+    a_shard = shard_from_dense_rows(a_dense[r0 * 16:min(m, r1 * 16)], r0)
+    b_shard = None if b_dense is None else shard_from_dense_rows(b_dense[r0 * 16:min(b_dense.shape[0], r1 * 16)], r0)
+    shape_b = a_dense.shape if b_dense is None else b_dense.shape
+    times = []
+    out = None
+    for it in range(warmup + steps):
+        flush.fill_(it)
+        dist_mod.barrier()
+        torch_mod.cuda.synchronize()
+        e0, e1 = torch_mod.cuda.Event(enable_timing=True), torch_mod.cuda.Event(enable_timing=True)
+        e0.record()
+        out = multiply_sharded(a_shard, b_shard, a_dense.shape, shape_b, cfg)
+        e1.record()
+        torch_mod.cuda.synchronize()
+        if it >= warmup:
+            times.append(e0.elapsed_time(e1))
+    ms = torch_mod.tensor([float(np.mean(times))], device="cuda")
+    dist_mod.all_reduce(ms, op=dist_mod.ReduceOp.MAX)
+    c, plan, counters, rows = out
+    work = torch_mod.tensor([float(counters.products4), float(len(plan))], dtype=torch_mod.float64, device="cuda")
+    dist_mod.all_reduce(work)
+    fine = cfg.granularity == "fine4"
+    flops = 128.0 * work[0].item() if fine else 8192.0 * work[1].item()
+    ms = float(ms.item())
+    line = {"metric": "spamm_surviving_gflops", "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "cfg5" if m == 32768 else f"n={m}", "n": int(m), "tau": cfg.tau,
+                       "granularity": cfg.granularity, "tasks": int(work[1].item()),
+                       "products4": int(work[0].item()), "parallelism": f"row-blocks x{world}, all-gather of B",
+                       "l2": "flushed between steps"}}
+    return {"line": line}

@@ -338,9 +338,13 @@ class QuadtreeMatrix:
         n = self.nleaf
         if n == 0:
             return (np.empty(0, np.uint64), np.empty((0, 16, 16), np.float32), np.empty((0, 4, 4), np.float32))
-        return (self.keys[:n].cpu().numpy().astype(np.uint64),
-                np.ascontiguousarray(self.values[:n, :256].cpu().numpy()).reshape(n, 16, 16),
-                np.ascontiguousarray(self.values_t[:n, 256:].cpu().numpy()).reshape(n, 4, 4))
+        keys = self.keys[:n].cpu().numpy().astype(np.uint64)
+        vals = np.ascontiguousarray(self.values[:n, :256].cpu().numpy()).reshape(n, 16, 16)
+        subs = np.ascontiguousarray(self.values_t[:n, 256:].cpu().numpy()).reshape(n, 4, 4)
+        if not getattr(self, "_keys_sorted", True):     # gathered from several ranks: rank order
+            order = np.argsort(keys, kind="stable")
+            keys, vals, subs = keys[order], vals[order], subs[order]
+        return keys, vals, subs
 
     def leaf_keys(self) -> np.ndarray:
         return self.packed_leaves()[0] if self.nleaf else np.empty(0, np.uint64)

@@ -1,0 +1,139 @@
+"""BASELINE.json configurations at full size on the device.
+
+Where the CPU oracle finishes in seconds (configs 1-3) the product is compared with it bit for bit
+(EXACT rounding mode) and within the north_star tolerance (FMA mode).  Where it does not
+(config 4 at n = 7500: 6e7-9e7 tasks; config 5 at n = 32768) parity is pinned the way SURVEY.md 8c
+prescribes: the task count, the executed-micro-product count and the product-leaf count against
+the oracle's flat all-pairs plan, slabs of C rows against the oracle executing exactly those rows'
+tasks, plus size-independent properties: determinism, symmetry of A*A, monotonicity in tau.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1203_1692_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-5     # BASELINE.json north_star: max-norm relative error against the reference output
+
+
+def _device_tree(P, dense):
+    return P.QuadtreeMatrix.from_dense(dense)
+
+
+def _slab_rows_match(P, c_dev, oa, ob, oplan, tau, gran, rows):
+    """Rows [r0, r1) of product leaves: oracle on exactly those rows' tasks vs the device product."""
+    dev = c_dev.to_dense().data
+    for r0, r1 in rows:
+        sel = (oplan.ti >= r0) & (oplan.ti < r1)
+        sub = O.OraclePlan(oplan.ti[sel], oplan.tk[sel], oplan.tj[sel], oplan.norm_product[sel], tau)
+        c, _ = O.execute_plan(sub, oa, ob, None, tau, gran)
+        want = c.to_dense()[r0 * 16:r1 * 16]
+        assert np.array_equal(dev[r0 * 16:r1 * 16], want), f"C rows {r0}:{r1}"
+
+
+@pytest.mark.parametrize("tau", [1e-4, 1e-6, 1e-8, 1e-10])
+def test_config2_full_size_matches_oracle(tau):
+    import paper_1203_1692_b200 as P
+    a, _ = inputs.make_operands("cfg2")
+    oa = O.tree_from_dense(a)
+    qa = _device_tree(P, a)
+    oc, oplan, ok = O.multiply(oa, oa, tau)
+    c, plan, k = P.multiply(qa, qa, P.MultiplyConfig(tau=tau, exact=True))
+    assert len(plan) == len(oplan)
+    assert (k.products4, k.skipped4) == (ok.products4, ok.skipped4)
+    ref = oc.to_dense()
+    got = c.to_dense().data
+    assert np.array_equal(got, ref), "exact-mode product differs from the oracle"
+    assert np.array_equal(got, got.T), "A*A of a symmetric A must come out symmetric, bit for bit"
+    for t in range(oc.depth + 1):
+        assert np.array_equal(c.level_norms(t), oc.level_norm(t)), f"C norms, tier {t}"
+    c2, _, k2 = P.multiply(qa, qa, P.MultiplyConfig(tau=tau))
+    got2 = c2.to_dense().data
+    assert np.abs(got2.astype(np.float64) - ref).max() <= REL_TOL * np.abs(ref).max()
+    assert k2.products4 == ok.products4
+    c3, _, _ = P.multiply(qa, qa, P.MultiplyConfig(tau=tau))
+    assert np.array_equal(c3.to_dense().data, got2), "the FMA path must be deterministic run to run"
+    cc, _, kc = P.multiply(qa, qa, P.MultiplyConfig(tau=tau, granularity="coarse16", exact=True))
+    occ, _, okc = O.multiply(oa, oa, tau, "coarse16")
+    assert np.array_equal(cc.to_dense().data, occ.to_dense()) and kc.products4 == okc.products4 == 64 * len(oplan)
+
+
+def test_config2_work_is_monotone_in_tau():
+    # tests/test_acceptance.py:245-259 of the reference: work falls, error does not, as tau grows
+    import paper_1203_1692_b200 as P
+    a, _ = inputs.make_operands("cfg2")
+    qa = _device_tree(P, a)
+    tasks, p4 = [], []
+    for tau in (0.0, 1e-10, 1e-8, 1e-6, 1e-4, 1e-2, 1.0, 1e3):
+        _, plan, k = P.multiply(qa, qa, P.MultiplyConfig(tau=tau))
+        tasks.append(len(plan))
+        p4.append(k.products4)
+    assert tasks == sorted(tasks, reverse=True) and p4 == sorted(p4, reverse=True)
+    assert tasks[-1] == 0 and p4[0] == 64 * tasks[0]
+
+
+def test_config3_full_size_matches_oracle():
+    import paper_1203_1692_b200 as P
+    a, b = inputs.make_operands("cfg3")
+    tau = 1e-8
+    oa, ob = O.tree_from_dense(a), O.tree_from_dense(b)
+    qa, qb = _device_tree(P, a), _device_tree(P, b)
+    oc, oplan, ok = O.multiply(oa, ob, tau)
+    c, plan, k = P.multiply(qa, qb, P.MultiplyConfig(tau=tau, exact=True))
+    assert len(plan) == len(oplan) and k.products4 == ok.products4 and k.skipped4 == ok.skipped4
+    ref = oc.to_dense()
+    assert np.array_equal(c.to_dense().data, ref)
+    c2, _, _ = P.multiply(qa, qb, P.MultiplyConfig(tau=tau))
+    assert np.abs(c2.to_dense().data.astype(np.float64) - ref).max() <= REL_TOL * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("tau", [1e-6, 1e-8])
+def test_config4_full_size_counts_and_slabs(tau):
+    import paper_1203_1692_b200 as P
+    a, _ = inputs.make_operands("cfg4")
+    assert a.shape == (7500, 7500)
+    oa = O.tree_from_dense(a)
+    assert oa.depth == 9                      # tests/test_core.py:22 of the reference
+    qa = _device_tree(P, a)
+    oplan = O.build_plan(oa, oa, tau)         # the flat all-pairs task set
+    c, plan, k = P.multiply(qa, qa, P.MultiplyConfig(tau=tau, exact=True))
+    assert len(plan) == len(oplan)
+    assert plan.n_cleaves == np.unique(oplan.ti.astype(np.int64) * 512 + oplan.tj).size
+    masks = O.task_masks(oa, oa, oplan, tau)
+    want_p4 = int(np.bitwise_count(masks).sum()) if hasattr(np, "bitwise_count") else int(sum(bin(int(m)).count("1") for m in masks))
+    assert k.products4 == want_p4 and k.skipped4 == 64 * len(oplan) - want_p4
+    _slab_rows_match(P, c, oa, oa, oplan, tau, "fine4", [(0, 2), (233, 235), (467, 469)])
+    d = c.to_dense().data
+    assert np.array_equal(d, d.T)
+
+
+def test_config5_full_size_counts_and_slabs():
+    import paper_1203_1692_b200 as P
+    a, _ = inputs.make_operands("cfg5")
+    tau = 1e-8
+    oa = O.tree_from_dense(a)
+    qa = _device_tree(P, a)
+    assert qa.nleaf == int(oa.keys.size)
+    del a
+    oplan = O.build_plan(oa, oa, tau)
+    c, plan, k = P.multiply(qa, qa, P.MultiplyConfig(tau=tau, exact=True))
+    assert len(plan) == len(oplan)
+    masks = O.task_masks(oa, oa, oplan, tau)
+    assert k.products4 == int(np.bitwise_count(masks).sum())
+    # slabs of C rows, bit for bit, via packed leaves (the dense product would be 4.3 GB)
+    keys, vals, _ = c.packed_leaves()
+    from paper_1203_1692_b200 import morton
+    ci, cj = morton.decode_array(keys)
+    for r0, r1 in ((0, 1), (1000, 1001), (2047, 2048)):
+        sel = (oplan.ti >= r0) & (oplan.ti < r1)
+        sub = O.OraclePlan(oplan.ti[sel], oplan.tk[sel], oplan.tj[sel], oplan.norm_product[sel], tau)
+        oc, _ = O.execute_plan(sub, oa, oa, None, tau)
+        oi, oj = np.nonzero(oc.slot >= 0)
+        mine = (ci >= r0) & (ci < r1)
+        assert np.array_equal(np.sort(cj[mine]), np.sort(oj.astype(np.uint64)))
+        order = np.argsort(cj[mine], kind="stable")
+        want = oc.values[oc.slot[oi, oj]][np.argsort(oj, kind="stable")]
+        assert np.array_equal(vals[mine][order], want), f"C leaf row {r0}"
