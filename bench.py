@@ -5,10 +5,11 @@
 One "step" is one SpAMM multiply (symbolic phase + numeric phase + C norms, the reference's timed
 region `pkg/src/spamm/bench.py:135-145`) of the workload, operands already resident in HBM as
 quadtrees.  N = 1 runs config 2 of BASELINE.json (exponential decay, n = 4096) at tau = 1e-8 with
-the reference's default fine4 gating and reports the tau sweep beside it; N > 1 runs config 5
-(n = 32768) with C sharded by row blocks and B all-gathered.  `value` is surviving GFLOP/s
-(128 flop per executed 4x4x4 product, `numeric.py:28-29`, `:63-65`).  Inputs are seeded synthetic
-matrices of the BASELINE.json laws (paper_1203_1692_b200/inputs.py).
+the reference's default fine4 gating and reports the tau sweep and the other configs beside it;
+N > 1 (under torchrun) runs config 5 (n = 32768) with C sharded by row blocks and the operand
+shards all-gathered inside the timed region.  `value` is surviving GFLOP/s (128 flop per executed
+4x4x4 product, `numeric.py:28-29`, `:63-65`).  Inputs are seeded synthetic matrices of the
+BASELINE.json laws (paper_1203_1692_b200/inputs.py).
 """
 
 from __future__ import annotations
@@ -28,6 +29,7 @@ sys.path.insert(0, ROOT)
 
 HEADLINE_TAU = 1e-8
 L2_FLUSH_BYTES = 256 << 20
+NUM_SMS = 148
 
 
 def peaks():
@@ -39,25 +41,76 @@ def peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback"}
 
 
+def recorded_traffic(workload: str, granularity: str):
+    """dram bytes per launch of execute_kernel from the committed `ncu --set full` capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(f"{workload}:{granularity}")
+    except (OSError, ValueError):
+        return None
+
+
 class ClockSampler:
-    """Samples nvidia-smi clocks and throttle reasons while the timed region runs."""
+    """Samples SM clocks and throttle reasons while the timed region runs (NVML, every 2 ms;
+    `nvidia-smi --query-gpu` as the fallback)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int = 0):
-        self.index, self.samples, self._stop, self._t = index, [], threading.Event(), None
+        self.index, self.mhz, self.max_mhz, self.reasons = index, [], None, set()
+        self._stop, self._t, self._nvml, self._h = threading.Event(), None, None, None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self._physical_index(index))
+            self.max_mhz = int(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self._nvml = None
+
+    @staticmethod
+    def _physical_index(index: int) -> int:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            ids = [v.strip() for v in vis.split(",") if v.strip()]
+            if index < len(ids) and ids[index].isdigit():
+                return int(ids[index])
+        return index
+
+    def _sample_nvml(self):
+        n = self._nvml
+        self.mhz.append(int(n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)))
+        r = int(n.nvmlDeviceGetCurrentClocksEventReasons(self._h)) if hasattr(n, "nvmlDeviceGetCurrentClocksEventReasons") \
+            else int(n.nvmlDeviceGetCurrentClocksThrottleReasons(self._h))
+        for name, bit in (("hw_slowdown", 0x8), ("sw_power_cap", 0x4), ("sw_thermal_slowdown", 0x20),
+                          ("hw_thermal_slowdown", 0x40)):
+            if r & bit:
+                self.reasons.add(name)
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-i",
+                              str(self.index)], capture_output=True, text=True, timeout=5).stdout.strip()
+        s = [x.strip() for x in out.split(",")]
+        if len(s) >= 6 and s[0].isdigit():
+            self.mhz.append(int(s[0]))
+            if s[1].isdigit():
+                self.max_mhz = max(self.max_mhz or 0, int(s[1]))
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), s[2:6]):
+                if v.lower() == "active":
+                    self.reasons.add(name)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                      "-i", str(self.index)], capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                if self._nvml is not None:
+                    self._sample_nvml()
+                else:
+                    self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.002 if self._nvml is not None else 0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -69,18 +122,10 @@ class ClockSampler:
         self._t.join(timeout=6)
 
     def summary(self):
-        mhz = sorted(int(s[0]) for s in self.samples if s and s[0].isdigit())
-        mx = [int(s[1]) for s in self.samples if len(s) > 1 and s[1].isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:6]) if v.strip().lower() == "active"})
-        return {"sm_mhz": mhz[len(mhz) // 2] if mhz else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
-
-
-def workload_operands(name: str):
-    from paper_1203_1692_b200 import inputs
-    a, b = inputs.make_operands(name)
-    return a, b
+        mhz = sorted(self.mhz)
+        return {"sm_mhz": mhz[len(mhz) // 2] if mhz else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(mhz),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -95,11 +140,13 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     from oracle import oracle as O
+    from paper_1203_1692_b200 import inputs
     name = args.workload or ("cfg2" if args.gpus == 1 else "cfg5")
     n_override = None
+    sample = f"whole {name} multiply"
     if name == "cfg5":
         n_override = 8192      # largest size of the law whose step stays in the seconds range on a CPU
-    from paper_1203_1692_b200 import inputs
+        sample = "cfg5 law at n=8192 (n=32768 does not fit the time bound on a CPU)"
     a_d, b_d = inputs.make_operands(name, n_override)
     ta = O.tree_from_dense(a_d)
     tb = ta if b_d is None else O.tree_from_dense(b_d)
@@ -113,7 +160,7 @@ def run_reference(args) -> None:
         if it >= args.warmup:
             times.append(dt)
     sec = float(np.mean(times))
-    flops = 128 * counters.products4
+    flops = 128 * counters.products4 if args.granularity == "fine4" else 8192 * len(plan)
     val = flops / sec / 1e9
     cores = O.num_threads()
     line = {
@@ -124,13 +171,13 @@ def run_reference(args) -> None:
         "config": {"workload": name, "n": int(a_d.shape[0]), "tau": tau, "granularity": args.granularity,
                    "tasks": len(plan), "products4": counters.products4},
         "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"whole {name} multiply (n={a_d.shape[0]}), C oracle with OpenMP"},
+                         "sample": f"{sample}; C port of the reference algorithm, OpenMP over product leaves"},
         "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
 
-# --------------------------------------------------------------------------- own arm
+# --------------------------------------------------------------------------- own arm, one GPU
 
 def timed_multiply(P, torch, qa, qb, cfg, steps, warmup, flush):
     """Per-step CUDA-event times of multiply(); L2 is flushed between steps, outside the events."""
@@ -176,36 +223,31 @@ def kernel_time_execute(P, torch, plan, qa, qb, cfg, reps, flush):
     return float(np.mean(times))
 
 
-def run_own(args) -> None:
-    import torch
-    import torch.distributed as dist
+def measure_case(P, torch, qa, qb, tau, gran, flush, fp32_peak, ref64=None, steps=5):
+    cf = P.MultiplyConfig(tau=tau, granularity=gran)
+    ts, (cs, pl, ks) = timed_multiply(P, torch, qa, qb, cf, steps, 3, flush)
+    fl = 128 * ks.products4 if gran == "fine4" else 8192 * len(pl)
+    kt = kernel_time_execute(P, torch, pl, qa, qb, cf, steps, flush)
+    err = None
+    if ref64 is not None:
+        err = float((cs.to_dense_tensor().double() - ref64).abs().max().item())
+    L = 1 << pl.depth
+    med = float(np.median(ts))
+    return {"tau": tau, "granularity": gran, "ms": med, "tasks": len(pl), "task_fraction": len(pl) / float(L) ** 3,
+            "products4": ks.products4, "gflops": fl / (med * 1e-3) / 1e9, "kernel_ms": kt,
+            "kernel_tflops": fl / (kt * 1e-3) / 1e12, "kernel_frac_fp32_peak": fl / (kt * 1e-3) / 1e12 / fp32_peak,
+            "max_abs_err_vs_fp64": err}
 
-    import paper_1203_1692_b200 as P
-    from paper_1203_1692_b200 import _lib
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    name = args.workload or ("cfg2" if world == 1 else "cfg5")
+def run_single(args, torch, P, local: int) -> None:
+    from paper_1203_1692_b200 import _lib, inputs
+    name = args.workload or "cfg2"
     pk = peaks()
-    fp32_peak_tflops = 2 * 128 * 148 * pk["sm_max_mhz"] * 1e6 / 1e12
-    a_d, b_d = workload_operands(name)
+    fp32_peak = 2 * 128 * NUM_SMS * pk["sm_max_mhz"] * 1e6 / 1e12
+    a_d, b_d = inputs.make_operands(name)
     n = a_d.shape[0]
     flush = torch.empty((L2_FLUSH_BYTES,), dtype=torch.uint8, device="cuda")
     cfg = P.MultiplyConfig(tau=args.tau, granularity=args.granularity)
-
-    if world > 1:
-        from paper_1203_1692_b200 import parallel
-        result = parallel.bench_sharded(P, torch, dist, a_d, b_d, cfg, args.steps, args.warmup, flush)
-        if rank == 0:
-            result["line"].update({"n_gpus": world, "steps": args.steps, "warmup": args.warmup})
-            print(json.dumps(result["line"]))
-        dist.destroy_process_group()
-        return
-
     qa = P.QuadtreeMatrix.from_dense(a_d)
     qb = qa if b_d is None else P.QuadtreeMatrix.from_dense(b_d)
     torch.cuda.synchronize()
@@ -221,18 +263,19 @@ def run_own(args) -> None:
     value = flops / (ms * 1e-3) / 1e9
 
     # ---- the dominant kernel alone, for the roofline
-    k3_ms = kernel_time_execute(P, torch, plan, qa, qb, cfg, max(5, args.steps), flush)
+    k3_ms = kernel_time_execute(P, torch, plan, qa, qb, cfg, max(5, min(args.steps, 50)), flush)
     k3_tflops = flops / (k3_ms * 1e-3) / 1e12
     # compulsory traffic of the kernel: every stored A leaf (transposed copy) and B leaf once, C leaves
-    # written in both layouts, task records
+    # written in both layouts, step records
     alg_bytes = 1088 * (qa.nleaf + qb.nleaf + 2 * plan.n_cleaves) + 64 * plan.n_steps
+    n_tasks, n_cleaves = len(plan), plan.n_cleaves
 
     # ---- end to end through the public API with host buffers
     host_a = torch.from_numpy(a_d).pin_memory()
     host_b = host_a if b_d is None else torch.from_numpy(b_d).pin_memory()
     host_c = torch.empty((a_d.shape[0], (b_d if b_d is not None else a_d).shape[1]), dtype=torch.float32).pin_memory()
     e2e_times = []
-    for it in range(2 + max(3, args.steps // 2)):
+    for it in range(2 + max(3, min(args.steps, 20) // 2)):
         flush.fill_(it)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -247,33 +290,18 @@ def run_own(args) -> None:
     e2e_ms = float(np.mean(e2e_times))
     h2d = a_d.nbytes * (1 if b_d is None else 2)
 
-    # ---- tau sweep (config 2 of BASELINE.json), both granularities
+    # ---- tau sweep of the headline workload (config 2 of BASELINE.json), both granularities
     sweep = []
     if not args.no_sweep:
-        from paper_1203_1692_b200 import inputs
-        taus = inputs.WORKLOADS[name].taus
         ref64 = None
         if n <= 8192:
             ad = torch.from_numpy(a_d).cuda().double()
             bd = ad if b_d is None else torch.from_numpy(b_d).cuda().double()
             ref64 = ad @ bd
             del ad, bd
-        for tau in taus:
+        for tau in inputs.WORKLOADS[name].taus:
             for gran in ("fine4", "coarse16"):
-                cf = P.MultiplyConfig(tau=tau, granularity=gran)
-                ts, (cs, pl, ks) = timed_multiply(P, torch, qa, qb, cf, 5, 2, flush)
-                fl = 128 * ks.products4 if gran == "fine4" else 8192 * len(pl)
-                kt = kernel_time_execute(P, torch, pl, qa, qb, cf, 5, flush)
-                err = None
-                if ref64 is not None:
-                    err = float((cs.to_dense_tensor().double() - ref64).abs().max().item())
-                L = 1 << pl.depth
-                sweep.append({"tau": tau, "granularity": gran, "ms": float(np.median(ts)), "tasks": len(pl),
-                              "task_fraction": len(pl) / float(L) ** 3, "products4": ks.products4,
-                              "gflops": fl / (np.median(ts) * 1e-3) / 1e9, "kernel_ms": kt,
-                              "kernel_tflops": fl / (kt * 1e-3) / 1e12,
-                              "kernel_frac_fp32_peak": fl / (kt * 1e-3) / 1e12 / fp32_peak_tflops,
-                              "max_abs_err_vs_fp64": err})
+                sweep.append(measure_case(P, torch, qa, qb, tau, gran, flush, fp32_peak, ref64))
         del ref64
 
     # ---- CPU baseline beside it: the oracle port on the host cores
@@ -282,25 +310,50 @@ def run_own(args) -> None:
         from oracle import oracle as O
         ta_o = O.tree_from_dense(a_d)
         tb_o = ta_o if b_d is None else O.tree_from_dense(b_d)
-        t0 = time.perf_counter()
-        opl = O.build_plan(ta_o, tb_o, args.tau)
-        _, ocnt = O.execute_plan(opl, ta_o, tb_o, None, args.tau, args.granularity)
-        dt = time.perf_counter() - t0
-        cpu = {"value": 128 * ocnt.products4 / dt / 1e9, "unit": "GFLOP/s", "cores": O.num_threads(), "kind": "port",
-               "sample": f"one whole {name} multiply, {dt:.2f} s (C oracle port of the reference, OpenMP)"}
+        reps, t0 = 0, time.perf_counter()
+        while reps < 3 or (time.perf_counter() - t0 < 10.0 and reps < 200):
+            opl = O.build_plan(ta_o, tb_o, args.tau)
+            _, ocnt = O.execute_plan(opl, ta_o, tb_o, None, args.tau, args.granularity)
+            reps += 1
+        dt = (time.perf_counter() - t0) / reps
+        oflops = 128 * ocnt.products4 if args.granularity == "fine4" else 8192 * len(opl)
+        cpu = {"value": oflops / dt / 1e9, "unit": "GFLOP/s", "cores": O.num_threads(), "kind": "port",
+               "sample": f"{reps} whole {name} multiplies, {dt * 1e3:.1f} ms each (C port of the reference "
+                         f"algorithm, OpenMP over product leaves)"}
+        del ta_o, tb_o
+
+    # ---- the other BASELINE.json configs on this GPU (time per multiply, GFLOP/s, K3 fraction)
+    others = []
+    if not args.no_configs and args.workload is None:
+        del qa, qb, c, plan
+        for wl in ("cfg1", "cfg3", "cfg4", "cfg5"):
+            xa, xb = inputs.make_operands(wl)
+            ta = P.QuadtreeMatrix.from_dense(xa)
+            tb = ta if xb is None else P.QuadtreeMatrix.from_dense(xb)
+            nn = int(xa.shape[0])
+            del xa, xb
+            for tau in inputs.WORKLOADS[wl].taus:
+                for gran in ("fine4", "coarse16"):
+                    r = measure_case(P, torch, ta, tb, tau, gran, flush, fp32_peak, None, steps=3)
+                    r.update({"workload": wl, "n": nn})
+                    others.append(r)
+            del ta, tb
+            torch.cuda.empty_cache()
 
     line = {
         "metric": "spamm_surviving_gflops", "value": value, "unit": "GFLOP/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": name, "n": int(n), "tau": args.tau, "granularity": args.granularity,
-                   "tasks": len(plan), "product_leaves": plan.n_cleaves, "products4": p4,
+                   "tasks": n_tasks, "product_leaves": n_cleaves, "products4": p4,
                    "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write)",
                    "effective_gflops_2n3": 2.0 * n ** 3 / (ms * 1e-3) / 1e9},
-        "roofline": {"bound": "fp32", "kernel": "execute_kernel", "achieved": k3_tflops, "peak": fp32_peak_tflops,
-                     "unit": "TFLOP/s", "frac": k3_tflops / fp32_peak_tflops,
-                     "peak_source": f"2*128 lanes*148 SMs*{pk['sm_max_mhz']:.0f} MHz ({pk['source']} clock)",
-                     "kernel_ms": k3_ms, "traffic": None,
+        "roofline": {"bound": "fp32", "kernel": "execute_kernel", "achieved": k3_tflops, "peak": fp32_peak,
+                     "unit": "TFLOP/s", "frac": k3_tflops / fp32_peak,
+                     "peak_source": f"2*128 lanes*{NUM_SMS} SMs*{pk['sm_max_mhz']:.0f} MHz ({pk['source']} max clock); "
+                                    "MEASURED_PEAKS.json has no FP32 FMA figure",
+                     "kernel_ms": k3_ms, "traffic": recorded_traffic(name, args.granularity),
+                     "algorithmic_bytes": int(alg_bytes),
                      "hbm_frac_of_measured": alg_bytes / (k3_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
         "cpu_baseline": cpu,
         "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
@@ -308,14 +361,143 @@ def run_own(args) -> None:
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "sweep": sweep,
+        "configs": others,
     }
     print(json.dumps(line))
+
+
+# --------------------------------------------------------------------------- own arm, N GPUs
+
+def run_sharded(args, torch, dist, P, local: int) -> None:
+    """Config 5 with C's leaf rows split across the ranks.  Timed region of one step, per rank:
+    all-gather of the operand shards -> whole-matrix tree (transposed copies, grids, pyramid) ->
+    plan on the replicated norms -> task-balanced row cut -> fused multiply of the own row block."""
+    from paper_1203_1692_b200 import _lib, inputs, parallel
+    rank, world = dist.get_rank(), dist.get_world_size()
+    name = args.workload or "cfg5"
+    cfg = P.MultiplyConfig(tau=args.tau, granularity=args.granularity)
+    flush = torch.empty((L2_FLUSH_BYTES,), dtype=torch.uint8, device="cuda")
+
+    # rank 0 draws the matrix and builds the tree; the packed leaves are broadcast (set-up, untimed)
+    meta = torch.zeros((4,), dtype=torch.int64, device="cuda")
+    if rank == 0:
+        a_d, b_d = inputs.make_operands(name)
+        if b_d is not None:
+            raise SystemExit("the sharded bench runs C = A*A workloads (cfg2, cfg4, cfg5)")
+        q0 = P.QuadtreeMatrix.from_dense(a_d)
+        meta[:] = torch.tensor([a_d.shape[0], a_d.shape[1], q0.nleaf, 0])
+        del a_d
+    dist.broadcast(meta, 0)
+    m, n, nleaf = int(meta[0]), int(meta[1]), int(meta[2])
+    if rank == 0:
+        whole = parallel.shard_of_tree(q0, 0, 1 << 30)
+        del q0
+    else:
+        whole = parallel.PackedShard(torch.empty((nleaf,), dtype=torch.int32, device="cuda"),
+                                     torch.empty((nleaf, 272), dtype=torch.float32, device="cuda"),
+                                     torch.empty((nleaf,), dtype=torch.float64, device="cuda"))
+    for t in (whole.keys, whole.records, whole.leaf_sq):
+        dist.broadcast(t, 0)
+    full = parallel.tree_from_shard(m, n, whole)
+    nrows = -(-m // 16)
+    r0, r1 = parallel.even_row_split(nrows, world)[rank]
+    mine = parallel.shard_of_tree(full, r0, r1)
+    host_rows = full.to_dense_tensor()[r0 * 16:min(m, r1 * 16)].cpu().pin_memory()
+    del full, whole
+    torch.cuda.empty_cache()
+
+    def step_resident():
+        return parallel.multiply_sharded(mine, None, (m, n), (m, n), cfg)
+
+    host_out = {}
+
+    def step_e2e():
+        shard = parallel.shard_from_dense_rows(host_rows, r0)
+        c, plan, counters, rows = parallel.multiply_sharded(shard, None, (m, n), (m, n), cfg)
+        block = c.to_dense_tensor()[rows[0] * 16:min(m, rows[1] * 16)]
+        if host_out.get("buf") is None or host_out["buf"].shape != block.shape:
+            host_out["buf"] = torch.empty(block.shape, dtype=torch.float32).pin_memory()
+        host_out["buf"].copy_(block, non_blocking=True)
+        return c, plan, counters, rows
+
+    def timed(fn, steps, warmup):
+        times, out = [], None
+        for it in range(warmup + steps):
+            flush.fill_(it)
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = fn()
+            e1.record()
+            torch.cuda.synchronize()
+            if it >= warmup:
+                times.append(e0.elapsed_time(e1))
+        t = torch.tensor([float(np.mean(times))], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), out
+
+    l0 = _lib.launch_count()
+    with ClockSampler(local) as clocks:
+        ms, (c, plan, counters, rows) = timed(step_resident, args.steps, args.warmup)
+    launches = (_lib.launch_count() - l0) * args.steps // (args.steps + args.warmup)
+    work = torch.tensor([float(counters.products4), float(len(plan)), float(r1 - r0), float(rows[1] - rows[0])],
+                        dtype=torch.float64, device="cuda")
+    per_rank = [torch.zeros_like(work) for _ in range(world)]
+    dist.all_gather(per_rank, work)
+    tot_p4 = sum(float(w[0]) for w in per_rank)
+    tot_tasks = sum(float(w[1]) for w in per_rank)
+    flops = 128.0 * tot_p4 if cfg.granularity == "fine4" else 8192.0 * tot_tasks
+    e2e_ms, _ = timed(step_e2e, max(2, min(args.steps, 5)), 2)
+    d2h = 0 if host_out.get("buf") is None else host_out["buf"].numel() * 4
+    io = torch.tensor([float(host_rows.numel() * 4), float(d2h)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(io)
+    if rank == 0:
+        line = {
+            "metric": "spamm_surviving_gflops", "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": name, "n": m, "tau": args.tau, "granularity": args.granularity,
+                       "tasks": int(tot_tasks), "products4": int(tot_p4),
+                       "parallelism": f"C row blocks x{world} balanced by task count, operand shards all-gathered (NCCL) "
+                                      "inside the timed region",
+                       "tasks_per_rank": [int(w[1]) for w in per_rank],
+                       "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write)"},
+            "roofline": None, "cpu_baseline": None,
+            "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": int(io[0].item()), "d2h_bytes_per_step": int(io[1].item())},
+            "gpu_launches": int(launches), "clocks": clocks.summary(),
+        }
+        print(json.dumps(line))
+
+
+def run_own(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import paper_1203_1692_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    sharded = world > 1 or os.environ.get("SPAMM_BENCH_SHARDED") == "1"
+    if sharded:
+        if not dist.is_initialized():
+            if "MASTER_ADDR" not in os.environ:
+                os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": "29531", "RANK": "0", "WORLD_SIZE": "1"})
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        try:
+            run_sharded(args, torch, dist, P, local)
+        finally:
+            dist.destroy_process_group()
+    else:
+        run_single(args, torch, P, local)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="own", choices=("own", "reference"))
     ap.add_argument("--workload", default=None)
@@ -323,6 +505,7 @@ def main():
     ap.add_argument("--granularity", default="fine4", choices=("fine4", "coarse16"))
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

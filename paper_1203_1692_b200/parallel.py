@@ -194,43 +194,3 @@ def multiply_sharded(a_shard: PackedShard, b_shard: PackedShard | None, shape_a:
     r0, r1 = balanced_row_split(counts[:nrows], world)[rank]
     c, myplan, counters = multiply_async(a_full, b_full, cfg, None, row_range=(r0, r1))
     return c, myplan, counters, (r0, r1)
-
-
-def bench_sharded(P, torch_mod, dist_mod, a_dense, b_dense, cfg, steps: int, warmup: int, flush):
-    """bench.py's N > 1 leg: config 5 (or any workload) with the all-gather inside the timed region."""
-    rank, world = dist_mod.get_rank(), dist_mod.get_world_size()
-    m = a_dense.shape[0]
-    nrows = -(-m // 16)
-    r0, r1 = even_row_split(nrows, world)[rank]
-    a_shard = shard_from_dense_rows(a_dense[r0 * 16:min(m, r1 * 16)], r0)
-    b_shard = None if b_dense is None else shard_from_dense_rows(b_dense[r0 * 16:min(b_dense.shape[0], r1 * 16)], r0)
-    shape_b = a_dense.shape if b_dense is None else b_dense.shape
-    times = []
-    out = None
-    for it in range(warmup + steps):
-        flush.fill_(it)
-        dist_mod.barrier()
-        torch_mod.cuda.synchronize()
-        e0, e1 = torch_mod.cuda.Event(enable_timing=True), torch_mod.cuda.Event(enable_timing=True)
-        e0.record()
-        out = multiply_sharded(a_shard, b_shard, a_dense.shape, shape_b, cfg)
-        e1.record()
-        torch_mod.cuda.synchronize()
-        if it >= warmup:
-            times.append(e0.elapsed_time(e1))
-    ms = torch_mod.tensor([float(np.mean(times))], device="cuda")
-    dist_mod.all_reduce(ms, op=dist_mod.ReduceOp.MAX)
-    c, plan, counters, rows = out
-    work = torch_mod.tensor([float(counters.products4), float(len(plan))], dtype=torch_mod.float64, device="cuda")
-    dist_mod.all_reduce(work)
-    fine = cfg.granularity == "fine4"
-    flops = 128.0 * work[0].item() if fine else 8192.0 * work[1].item()
-    ms = float(ms.item())
-    line = {"metric": "spamm_surviving_gflops", "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": "cfg5" if m == 32768 else f"n={m}", "n": int(m), "tau": cfg.tau,
-                       "granularity": cfg.granularity, "tasks": int(work[1].item()),
-                       "products4": int(work[0].item()), "parallelism": f"row-blocks x{world}, all-gather of B",
-                       "l2": "flushed between steps"}}
-    return {"line": line}
