@@ -134,6 +134,16 @@ int spamm_to_dense(const spamm_tree_view *t, float *out, int64_t ld, void *strea
  * at packed index first + popcount(present16 & ((1 << morton4(r,c)) - 1)). */
 #define STEP_FIRST (1u << 16)   /* first record of its super-tile */
 #define STEP_LAST (1u << 17)    /* last record of its super-tile  */
+/* Work units of the numeric phase.  A unit is a run of consecutive step records of one super-tile.
+ * With many more super-tiles than CTAs every tile is one unit (counts[12] == 0, unit = node).
+ * Otherwise the planner cuts the tiles that are handed out last into segments of about counts[12]
+ * records, so that the persistent CTAs of the numeric kernel finish together: unit =
+ * node | segment << 20 | segments << 26, segment s of nseg covering records
+ * [s * ns / nseg, (s + 1) * ns / nseg) of a tile with ns records.  The accumulators of a tile pass
+ * from one segment to the next through C's own value records (chain[] holds, per product leaf, the
+ * number of finished segments), which keeps the ascending-k summation order.  A unit's
+ * predecessor always comes earlier in tile_order. */
+#define SPAMM_UNIT_EXTRA 8192   /* room in tile_order beyond one unit per super-tile */
 typedef struct {
     uint32_t kblock;       /* K: contraction block index, k = 4K + kk                      */
     uint32_t flags;        /* STEP_FIRST, STEP_LAST                                        */
@@ -148,16 +158,19 @@ typedef struct {
     uint32_t pad[3];
 } spamm_step;
 
-/* counts[]: [0] product leaves nC, [1] scratch (the numeric kernel's tile counter),
- * [2] overflow flag, [3] largest intermediate list, [4] step records, [5] super-tile nodes with
- * at least one record, [6..7] tasks T as one uint64, [8..9] executed 4x4x4 products as one uint64
- * (spamm_multiply only), [10] scratch, [11] all super-tile nodes (tile_off has one more entry) */
-#define SPAMM_PLAN_COUNTS 12
+/* counts[]: [0] product leaves nC, [1] unused,
+ * [2] overflow flag, [3] largest intermediate list, [4] step records, [5] work units in
+ * tile_order, [6..7] tasks T as one uint64, [8..9] executed 4x4x4 products as one uint64
+ * (spamm_multiply only), [10] scratch, [11] all super-tile nodes (tile_off has one more entry),
+ * [12] records per segment (0: every unit is a whole super-tile), [13..14] the numeric kernel's
+ * hand-out and exit counters (zero between launches), [15] reserved */
+#define SPAMM_PLAN_COUNTS 16
 typedef struct {
     spamm_step *steps;       /* [step_capacity]                                   */
     uint32_t *c_keys;        /* [leaf_capacity] product leaf keys, ascending      */
     int32_t *tile_off;       /* [leaf_capacity + 1] first step of each super-tile node */
-    int32_t *tile_order;     /* [leaf_capacity] super-tile nodes, most step records first */
+    int32_t *tile_order;     /* [leaf_capacity + SPAMM_UNIT_EXTRA] work units in hand-out order */
+    int32_t *chain;          /* [leaf_capacity] finished segments per product leaf (numeric phase scratch) */
     int64_t step_capacity;
     int64_t leaf_capacity;
     int32_t *counts;         /* [SPAMM_PLAN_COUNTS]                               */
@@ -235,7 +248,7 @@ int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b, double ta
  * spamm_product_buffers) and the total size; spamm_multiply_arena() carves `arena` that way and
  * runs spamm_multiply.  One allocation and one call per product on the host side. */
 typedef struct {
-    int64_t counts, steps, c_keys, tile_off, tile_order, plan_ws, plan_ws_bytes;
+    int64_t counts, steps, c_keys, tile_off, tile_order, chain, plan_ws, plan_ws_bytes;
     int64_t values, values_t, leaf_sq, slot, slot_t, norm, norm_t, leaf_sq_grid, sq_levels;
     int64_t total;
 } spamm_arena_layout;

@@ -30,7 +30,8 @@ class TreeView(C.Structure):
 class PlanBuffers(C.Structure):
     """``spamm_plan_buffers``."""
 
-    _fields_ = [("steps", vp), ("c_keys", vp), ("tile_off", vp), ("tile_order", vp), ("step_capacity", i64),
+    _fields_ = [("steps", vp), ("c_keys", vp), ("tile_off", vp), ("tile_order", vp), ("chain", vp),
+                ("step_capacity", i64),
                 ("leaf_capacity", i64), ("counts", vp)]
 
 
@@ -44,14 +45,16 @@ class ProductBuffers(C.Structure):
 class ArenaLayout(C.Structure):
     """``spamm_arena_layout`` (byte offsets into the single allocation of spamm_multiply_arena)."""
 
-    _fields_ = [(n, i64) for n in ("counts", "steps", "c_keys", "tile_off", "tile_order", "plan_ws", "plan_ws_bytes",
+    _fields_ = [(n, i64) for n in ("counts", "steps", "c_keys", "tile_off", "tile_order", "chain", "plan_ws",
+                                   "plan_ws_bytes",
                                    "values", "values_t", "leaf_sq", "slot", "slot_t", "norm", "norm_t", "leaf_sq_grid",
                                    "sq_levels", "total")]
 
 
 REC = 272           # floats per stored leaf record: 256 values + 16 sub-block norms
 STEP_WORDS = 16     # uint32 words per step record (struct spamm_step)
-PLAN_COUNTS = 12
+PLAN_COUNTS = 16
+UNIT_EXTRA = 8192   # SPAMM_UNIT_EXTRA: tile_order holds leaf_capacity + UNIT_EXTRA units, then the chain flags
 
 
 # every symbol include/spamm_b200.h declares: (restype, argtypes)

@@ -15,6 +15,7 @@
 // 17 KB: 16 leaf records of 1088 B holding values and sub-block norms) into a ring of
 // shared-memory stages guarded by mbarriers.  Eight consumer warps (two product leaves each)
 // gate and multiply from shared memory.  Super-tiles are handed out through an atomic counter.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -24,6 +25,8 @@
 #define EX_CONSUMERS 8
 #define EX_THREADS (32 * (EX_CONSUMERS + 1))
 #define EX_EXIT (1u << 31)
+#define EX_CHAIN_IN (1u << 30)    // first step of a later segment: accumulators come from C's records
+#define EX_CHAIN_OUT (1u << 29)   // last step of a segment that is not the tile's last: hand them on
 #define EX_PREFETCH 4
 #define EX_BLOCK_BYTES (16 * SPAMM_REC_BYTES)     // one 4x4 block of leaf records
 
@@ -35,7 +38,8 @@ struct __align__(16) StageDesc {
     uint32_t b_present;    // stored leaves of the staged B block, bit morton4(kk,dj)
     uint32_t live[4];      // live tasks per kk
     uint32_t tile;         // Morton index of the super-tile
-    uint32_t pad[2];
+    uint32_t seg;          // segment of the tile this step belongs to
+    uint32_t pad;
 };
 
 struct ExecArgs {
@@ -43,8 +47,9 @@ struct ExecArgs {
     const float *b_values;
     const spamm_step *steps;
     const int32_t *tile_off;     // step offset of every super-tile node, one extra entry
-    const int32_t *tile_order;   // super-tile nodes, longest first
-    const int32_t *counts;       // plan counts (device): [5] = number of super-tile nodes
+    const int32_t *tile_order;   // work units (node | segment << 24) in hand-out order
+    const int32_t *counts;       // plan counts (device): [5] = number of units, [12] = records per segment
+    int32_t *chain;              // finished segments per product leaf (zeroed before the launch)
     unsigned int *tile_counter;
     double tau;
     float alpha;
@@ -61,7 +66,15 @@ struct ExecArgs {
     int sub2;                    // leaves per super-tile (16; 4 or 1 for tiny trees)
     int nstages;                 // depth of the shared-memory ring
     int dbg;                     // tuning aid (SPAMM_EX_DEBUG): 1 = no copies, 2 = no math
+    unsigned long long *trace;   // tuning aid (SPAMM_EX_TRACE): per CTA start / first data / end / units
 };
+
+__device__ __forceinline__ unsigned long long global_timer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ double ex_row_sq(float4 v)
 {
@@ -75,7 +88,7 @@ __device__ __forceinline__ double ex_row_sq(float4 v)
 
 // Two C elements of one column (rows 2h, 2h+1) advance together: packed FP32 (sm_100 FFMA2 with a
 // broadcast scalar operand) halves the issue slots the multiply-accumulates take.  EXACT rounds the
-// product and the sum separately (numeric.py:252-259), FMUL2 + FADD2.
+// product and the sum separately (numeric.py:252-259) with scalar FMUL + FADD.
 template <bool EXACT>
 __device__ __forceinline__ void mac2(float2 &acc, float2 a, float b)
 {
@@ -114,25 +127,45 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
     __syncthreads();
     int stage = 0;
     uint32_t phase = 0;
+    if (g.trace && threadIdx.x == 0) g.trace[blockIdx.x * 4] = global_timer();
 
     if (warp == EX_CONSUMERS) {
         // ============ producer: stream step records, stage leaf blocks with bulk copies ============
         const int ntiles = g.counts[2] ? 0 : g.counts[5];      // an overflowed plan is incomplete: do nothing
+        const int seg_len = g.counts[12];
+        const bool claim_late = ntiles < 16 * (int)gridDim.x;
         const uint32_t *words = reinterpret_cast<const uint32_t *>(g.steps);
-        int tile = 0;
+        int tile = 0, units_done = 0;
         if (lane == 0) tile = (int)atomicAdd(g.tile_counter, 1u);
         tile = __shfl_sync(FULL_MASK, tile, 0);
         while (tile < ntiles) {
-            const int node = g.tile_order[tile];
-            const int beg = g.tile_off[node], end = g.tile_off[node + 1];
+            ++units_done;
+            const uint32_t unit = (uint32_t)g.tile_order[tile];
+            const int node = seg_len ? (int)(unit & ((1u << UNIT_NODE_BITS) - 1u)) : (int)unit;
+            const int seg = seg_len ? (int)((unit >> UNIT_NODE_BITS) & 63u) : 0;
+            int beg = g.tile_off[node], end = g.tile_off[node + 1];
+            bool chain_in = false, chain_out = false;
+            if (seg_len) {      // this unit is one segment of the tile
+                const int ns = end - beg, nseg = (int)(unit >> 26);
+                end = beg + unit_begin(ns, nseg, seg + 1);
+                beg = beg + unit_begin(ns, nseg, seg);
+                chain_in = seg > 0;
+                chain_out = seg + 1 < nseg;
+            }
+            // With few units per CTA the next unit is claimed late, two records before the
+            // end of this one: its latency still hides behind the staged records, and a CTA never sits
+            // on a whole unit it has not started while others run dry.  With many whole tiles it is
+            // claimed right away.
             int next_tile = 0;
-            if (lane == 0) next_tile = (int)atomicAdd(g.tile_counter, 1u);   // its latency hides behind this tile
+            if (lane == 0 && !claim_late) next_tile = (int)atomicAdd(g.tile_counter, 1u);
             // lane l < 16 holds word l of a record (struct spamm_step)
             uint32_t w[EX_PREFETCH];
 #pragma unroll
             for (int x = 0; x < EX_PREFETCH; ++x)
                 w[x] = (lane < 16 && beg + x < end) ? __ldg(words + (size_t)(beg + x) * 16 + lane) : 0u;
             for (int r = beg; r < end; ++r) {
+                if (lane == 0 && claim_late && (r + 2 == end || (r == beg && r + 2 > end)))
+                    next_tile = (int)atomicAdd(g.tile_counter, 1u);
                 const uint32_t cur = w[0];
 #pragma unroll
                 for (int x = 0; x + 1 < EX_PREFETCH; ++x) w[x] = w[x + 1];
@@ -142,7 +175,9 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
                 const uint32_t nb = __popc(__shfl_sync(FULL_MASK, cur, 7));
                 mbar_wait(&empty_bar[stage], phase ^ 1u);
                 uint32_t *d = reinterpret_cast<uint32_t *>(&desc[stage]);
-                if (lane == 1) d[0] = cur;                       // flags
+                if (lane == 1)                                   // flags
+                    d[0] = cur | (chain_in && r == beg ? EX_CHAIN_IN : 0u) | (chain_out && r + 1 == end ? EX_CHAIN_OUT : 0u);
+                if (lane == 13) d[10] = (uint32_t)seg;
                 if (lane == 2) d[1] = cur;                       // c_base
                 if (lane == 12) d[2] = cur;                      // present
                 if (lane == 3) d[9] = cur;                       // tile
@@ -167,6 +202,12 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
         if (lane == 0) {
             desc[stage].flags = EX_EXIT;
             mbar_arrive(&full_bar[stage]);
+            if (g.trace) g.trace[blockIdx.x * 4 + 3] = (unsigned long long)units_done;
+            // the last CTA to run out of units leaves both counters at zero for the next launch
+            if (atomicAdd(g.tile_counter + 1, 1u) == gridDim.x - 1) {
+                g.tile_counter[0] = 0u;
+                g.tile_counter[1] = 0u;
+            }
         }
         return;
     }
@@ -183,16 +224,40 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
     const int di = step_pos_di(mypos), dj = step_pos_dj(mypos);
     uint32_t executed = 0;
     float2 acc2[2][4];     // acc2[h][j] = C sub-block elements (2h, j) and (2h+1, j)
+    bool traced = false;
     for (;;) {
         mbar_wait(&full_bar[stage], phase);
         const StageDesc &ds = desc[stage];
         const uint32_t flags = ds.flags;
+        if (g.trace && threadIdx.x == 0 && !traced) {
+            g.trace[blockIdx.x * 4 + 1] = global_timer();
+            traced = true;
+        }
         if (flags & EX_EXIT) break;
         if (flags & STEP_FIRST) {
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc2[h][j] = make_float2(0.0f, 0.0f);
+        } else if (flags & EX_CHAIN_IN) {
+            // continue a tile another CTA started: wait for its segment, then take the partial sums
+            // from C's value record (written below under EX_CHAIN_OUT); L1 is bypassed
+            const uint32_t present_in = ds.present;
+            if ((present_in >> mypos) & 1u) {
+                const int64_t cs = (int64_t)ds.c_base + __popc(present_in & ((1u << mypos) - 1u));
+                const int want = (int)ds.seg;
+                while (ld_acquire_gpu(g.chain + cs) < want) __nanosleep(40);
+                // thread t16 keeps its 16 partial sums in registers order at floats [16 t16, 16 t16 + 16)
+                const float4 *cv = reinterpret_cast<const float4 *>(g.c_values + cs * SPAMM_REC + 16 * t16);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float4 u = __ldcg(cv + 2 * h), v = __ldcg(cv + 2 * h + 1);
+                    acc2[h][0] = make_float2(u.x, u.y);
+                    acc2[h][1] = make_float2(u.z, u.w);
+                    acc2[h][2] = make_float2(v.x, v.y);
+                    acc2[h][3] = make_float2(v.z, v.w);
+                }
+            }
         }
         const uint32_t a_present = ds.a_present, b_present = ds.b_present;
         const float *Ablk = reinterpret_cast<const float *>(sA + (size_t)stage * EX_BLOCK_BYTES);
@@ -270,15 +335,34 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
                 }
             }
         }
-        uint32_t c_base = 0, present = 0, tile_id = 0;
-        if (flags & STEP_LAST) {
+        uint32_t c_base = 0, present = 0, tile_id = 0, seg_done = 0;
+        if (flags & (STEP_LAST | EX_CHAIN_OUT)) {
             c_base = ds.c_base;
             tile_id = ds.tile;
             present = ds.present;
+            seg_done = ds.seg + 1u;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[stage]);
         if (++stage == nstages) { stage = 0; phase ^= 1u; }
+        if (flags & EX_CHAIN_OUT) {
+            // hand the partial sums to the CTA that runs the next segment of this tile
+            if ((present >> mypos) & 1u) {
+                const int64_t cs = (int64_t)c_base + __popc(present & ((1u << mypos) - 1u));
+                float4 *cv = reinterpret_cast<float4 *>(g.c_values + cs * SPAMM_REC + 16 * t16);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    __stcg(cv + 2 * h, make_float4(acc2[h][0].x, acc2[h][0].y, acc2[h][1].x, acc2[h][1].y));
+                    __stcg(cv + 2 * h + 1, make_float4(acc2[h][2].x, acc2[h][2].y, acc2[h][3].x, acc2[h][3].y));
+                }
+            }
+            __syncwarp();      // the 16 lanes' stores happen before the release below
+            if (t16 == 0 && ((present >> mypos) & 1u)) {
+                const int64_t cs = (int64_t)c_base + __popc(present & ((1u << mypos) - 1u));
+                st_release_gpu(g.chain + cs, (int)seg_done);
+            }
+            continue;
+        }
         if (!(flags & STEP_LAST)) continue;
 
         // epilogue of the super-tile: alpha scaling (numeric.py:273-275), both leaf layouts with
@@ -322,6 +406,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
             cv[256 + q * 4 + p] = sn;
             ct[256 + t16] = sn;
             if (t16 == 0) {
+                if (seg_done > 1u) g.chain[cslot] = 0;      // last reader of the flag: leave it clear
                 g.c_leaf_sq[cslot] = tot;
                 if (g.c_slot) {
                     uint32_t ci, cj;
@@ -336,6 +421,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
             }
         }
     }
+    if (g.trace && threadIdx.x == 0) g.trace[blockIdx.x * 4 + 2] = global_timer();
     if (FINE) {
         executed = __reduce_add_sync(FULL_MASK, executed);
         if (lane == 0 && executed) atomicAdd(g.counters, (unsigned long long)executed);
@@ -343,6 +429,12 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
 }
 
 struct ExecTuning { int stages, ctas_per_sm, dbg; };
+static ExecTuning exec_tuning();
+int spamm_execute_grid()
+{
+    static const ExecTuning tune = exec_tuning();
+    return SPAMM_NUM_SMS * tune.ctas_per_sm;
+}
 static ExecTuning exec_tuning()
 {
     ExecTuning t{3, 2, 0};
@@ -371,7 +463,8 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     g.tile_off = plan->tile_off;
     g.tile_order = plan->tile_order;
     g.counts = plan->counts;
-    g.tile_counter = reinterpret_cast<unsigned int *>(plan->counts + 1);
+    g.tile_counter = reinterpret_cast<unsigned int *>(plan->counts + 13);   // [13] hand-out, [14] exited CTAs
+    g.chain = plan->chain;
     g.tau = tau;
     g.alpha = alpha;
     g.alpha_is_one = (alpha == 1.0f);
@@ -396,7 +489,8 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
         g.c_sq_grid = cgrid->leaf_sq_grid;
         g.c_L = 1 << cgrid->depth;
     }
-    if (cudaMemsetAsync(plan->counts + 1, 0, sizeof(int32_t), st) != cudaSuccess) return SPAMM_ECUDA;
+    // counts[13..14] and the chain flags are zero here: spamm_plan clears them and every launch of
+    // the kernel leaves them clear again
     static const ExecTuning tune = exec_tuning();
     g.nstages = tune.stages;
     g.dbg = tune.dbg;
@@ -406,8 +500,24 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     void (*kern)(ExecArgs) = exact ? (fine ? execute_kernel<true, true> : execute_kernel<true, false>)
                                    : (fine ? execute_kernel<false, true> : execute_kernel<false, false>);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return SPAMM_ECUDA;
+    g.trace = nullptr;
+    static const char *trace_path = getenv("SPAMM_EX_TRACE");     // tuning aid: allocates and synchronises
+    if (trace_path && cudaMalloc(&g.trace, sizeof(unsigned long long) * 4 * grid) != cudaSuccess) g.trace = nullptr;
+    if (g.trace) cudaMemsetAsync(g.trace, 0, sizeof(unsigned long long) * 4 * grid, st);
     kern<<<grid, EX_THREADS, smem, st>>>(g);
     SPAMM_CHECK_LAUNCH();
+    if (g.trace) {
+        unsigned long long *h = (unsigned long long *)malloc(sizeof(unsigned long long) * 4 * grid);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, g.trace, sizeof(unsigned long long) * 4 * grid, cudaMemcpyDeviceToHost);
+        if (FILE *f = fopen(trace_path, "w")) {
+            for (int x = 0; x < grid; ++x)
+                fprintf(f, "%d %llu %llu %llu %llu\n", x, h[4 * x], h[4 * x + 1], h[4 * x + 2], h[4 * x + 3]);
+            fclose(f);
+        }
+        free(h);
+        cudaFree(g.trace);
+    }
     return SPAMM_OK;
 }
 

@@ -54,7 +54,8 @@ extern "C" int spamm_multiply_arena_layout(int depth, int c_depth, int64_t step_
     out->steps = arena_take(o, step_capacity * (int64_t)sizeof(spamm_step));
     out->c_keys = arena_take(o, leaf_capacity * 4);
     out->tile_off = arena_take(o, (leaf_capacity + 1) * 4);
-    out->tile_order = arena_take(o, leaf_capacity * 4);
+    out->tile_order = arena_take(o, (2 * leaf_capacity + SPAMM_UNIT_EXTRA) * 4);   // units, then the chain flags
+    out->chain = out->tile_order + (leaf_capacity + SPAMM_UNIT_EXTRA) * 4;
     out->plan_ws_bytes = (int64_t)spamm_plan_workspace_bytes(depth, step_capacity, leaf_capacity);
     out->plan_ws = arena_take(o, out->plan_ws_bytes);
     out->values = arena_take(o, leaf_capacity * SPAMM_REC_BYTES);
@@ -85,6 +86,7 @@ extern "C" int spamm_multiply_arena(const spamm_tree_view *a, const spamm_tree_v
     plan.c_keys = reinterpret_cast<uint32_t *>(p + l.c_keys);
     plan.tile_off = reinterpret_cast<int32_t *>(p + l.tile_off);
     plan.tile_order = reinterpret_cast<int32_t *>(p + l.tile_order);
+    plan.chain = reinterpret_cast<int32_t *>(p + l.chain);
     plan.step_capacity = step_capacity;
     plan.leaf_capacity = leaf_capacity;
     plan.counts = reinterpret_cast<int32_t *>(p + l.counts);

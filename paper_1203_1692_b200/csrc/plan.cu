@@ -19,6 +19,8 @@
 //   (K, 4 x 16 live bits = the tasks (4I+di, 4K+kk, 4J+dj) that survive, where the two leaf blocks sit)
 // so the compacted task list comes out already in the order and grouping the numeric phase
 // consumes: ascending k per product leaf (numeric.py:203-217), leaves in Morton order.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "plan_format.cuh"
 
@@ -489,9 +491,15 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
 // sort by step count (any order inside a bin; the product does not depend on it).
 __global__ void __launch_bounds__(256) plan_order_kernel(const int32_t *__restrict__ tile_off, int32_t *counts,
                                                          const unsigned int *__restrict__ bins, unsigned int *cursor,
-                                                         int32_t *__restrict__ tile_order)
+                                                         int32_t *__restrict__ tile_order, int unit_target, int min_seg,
+                                                         int grid_ctas, int32_t *__restrict__ chain,
+                                                         int64_t leaf_capacity)
 {
+    // the numeric kernel's per-leaf hand-over flags start clear
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < leaf_capacity; x += (int64_t)gridDim.x * blockDim.x)
+        chain[x] = 0;
     __shared__ unsigned int s_start[PLAN_BINS];
+    __shared__ unsigned int s_base[256];
     __shared__ unsigned int s_part[256];
     // exclusive scan of the bins in DESCENDING size order: 4 bins per thread
     const int t = threadIdx.x;
@@ -517,18 +525,69 @@ __global__ void __launch_bounds__(256) plan_order_kernel(const int32_t *__restri
         run += v[x];
     }
     __syncthreads();
+    // Work units.  With many more super-tiles than CTAs every tile is one unit.  Otherwise the tiles
+    // handed out last (the shortest ones, ranks >= whole) are cut into segments of about seg_len
+    // records so that the CTAs of the numeric kernel run dry together; the longer tiles, handed out
+    // first, stay whole (a hand-over costs about a third of a record).  Segment s >= 1 of the cut
+    // tiles follows segment s - 1 of all of them, so unit (tile, s) sits at s_base[s] + rank - whole.
     const int n_nodes = counts[11];
-    // nodes without records are left out: counts[5] = nodes the numeric kernel has to visit
-    if (blockIdx.x == 0 && t == 0) counts[5] = n_nodes - (int)bins[0];
+    const int n_tiles = n_nodes - (int)bins[0];
+    const int total_steps = counts[4];
+    int seg_len = 0, whole = 0;
+    if (unit_target > 0 && n_tiles > grid_ctas && n_tiles < unit_target && n_nodes <= (1 << UNIT_NODE_BITS)) {
+        seg_len = (total_steps + unit_target - 1) / unit_target;
+        if (seg_len < min_seg) seg_len = min_seg;
+        whole = grid_ctas * (n_tiles / grid_ctas - 1);
+    }
+    unsigned int cnt = 0;                   // cut tiles with more than t segments (t = 0: all tiles)
+    if (t == 0) cnt = (unsigned int)n_tiles;
+    else if (seg_len && t < UNIT_MAX_SEGMENTS && (long long)t * seg_len < PLAN_BINS) {
+        const int longer = (int)s_start[t * seg_len];          // tiles with more than t * seg_len records
+        cnt = longer > whole ? (unsigned int)(longer - whole) : 0u;
+    }
+    __syncthreads();                        // s_part is reused
+    unsigned int inc2 = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned int y = __shfl_up_sync(FULL_MASK, inc2, d);
+        if ((t & 31) >= d) inc2 += y;
+    }
+    if ((t & 31) == 31) s_part[t >> 5] = inc2;
+    __syncthreads();
+    unsigned int base = inc2 - cnt;
+    for (int w = 0; w < (t >> 5); ++w) base += s_part[w];
+    s_base[t] = base;
+    if (blockIdx.x == 0 && t == 255) {
+        counts[5] = (int)(base + cnt);      // work units the numeric kernel hands out
+        counts[12] = seg_len;
+    }
+    __syncthreads();
     for (int idx = blockIdx.x * blockDim.x + t; idx < n_nodes; idx += gridDim.x * blockDim.x) {
-        int ns = tile_off[idx + 1] - tile_off[idx];
+        const int ns = tile_off[idx + 1] - tile_off[idx];
         if (ns == 0) continue;
-        if (ns >= PLAN_BINS) ns = PLAN_BINS - 1;
-        tile_order[s_start[ns] + atomicAdd(&cursor[ns], 1u)] = idx;
+        const int bin = ns < PLAN_BINS ? ns : PLAN_BINS - 1;
+        const int rank = (int)(s_start[bin] + atomicAdd(&cursor[bin], 1u));
+        if (!seg_len) {
+            tile_order[rank] = idx;
+            continue;
+        }
+        // hand-out order: first segments of the cut tiles, the whole tiles, then the later segments
+        // (whose predecessors are then long finished)
+        const int nseg = rank >= whole ? unit_segments(ns, seg_len) : 1;
+        tile_order[rank >= whole ? rank - whole : n_tiles - whole + rank] = (int32_t)unit_pack(idx, 0, nseg);
+        for (int sgm = 1; sgm < nseg; ++sgm) tile_order[s_base[sgm] + rank - whole] = (int32_t)unit_pack(idx, sgm, nseg);
     }
 }
 
 // ---- host side ---------------------------------------------------------------------------------
+int spamm_execute_grid();     // CTAs of the numeric kernel (execute.cu)
+
+static int plan_env(const char *name, int dflt, int lo, int hi)
+{
+    int v = dflt;
+    if (const char *e = getenv(name)) v = atoi(e);
+    return v < lo ? lo : (v > hi ? hi : v);
+}
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct PlanWorkspace {
@@ -670,8 +729,11 @@ extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, do
     if (dense) plan_tiles_kernel<true><<<SPAMM_NUM_SMS, TILE_THREADS, 0, st>>>(t);
     else plan_tiles_kernel<false><<<SPAMM_NUM_SMS * 2, TILE_THREADS, 0, st>>>(t);
     SPAMM_CHECK_LAUNCH();
+    static const int unit_target = plan_env("SPAMM_UNIT_TARGET", 6 * 2 * SPAMM_NUM_SMS, 0, SPAMM_UNIT_EXTRA);
+    static const int min_seg = plan_env("SPAMM_UNIT_MIN_SEG", 2, 1, 1024);
     plan_order_kernel<<<SPAMM_NUM_SMS, 256, 0, st>>>(out->tile_off, out->counts, w.shared->bins, w.shared->cursor,
-                                                     out->tile_order);
+                                                     out->tile_order, unit_target, min_seg, spamm_execute_grid(),
+                                                     out->chain, out->leaf_capacity);
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
 }

@@ -10,6 +10,27 @@ __host__ __device__ __forceinline__ int step_pos(int di, int dj)
 }
 __host__ __device__ __forceinline__ int step_pos_di(int pos) { return ((pos >> 3) & 1) << 1 | ((pos >> 1) & 1); }
 __host__ __device__ __forceinline__ int step_pos_dj(int pos) { return ((pos >> 2) & 1) << 1 | (pos & 1); }
+// Work units (spamm_b200.h).  When the planner cuts tiles (counts[12] = seg_len != 0) a unit is
+// node | segment << 20 | segments << 26, otherwise just the node.
+#define UNIT_NODE_BITS 20
+#define UNIT_MAX_SEGMENTS 63
+#define UNIT_SIZE_CLAMP 1023     // = PLAN_BINS - 1: tiles are ranked by min(ns, 1023)
+__host__ __device__ __forceinline__ uint32_t unit_pack(int node, int seg, int nseg)
+{
+    return (uint32_t)node | ((uint32_t)seg << UNIT_NODE_BITS) | ((uint32_t)nseg << 26);
+}
+__host__ __device__ __forceinline__ int unit_segments(int ns, int seg_len)
+{
+    if (seg_len <= 0) return 1;
+    const int c = ns < UNIT_SIZE_CLAMP ? ns : UNIT_SIZE_CLAMP;
+    const int n = (c + seg_len - 1) / seg_len;
+    return n < UNIT_MAX_SEGMENTS ? (n > 0 ? n : 1) : UNIT_MAX_SEGMENTS;
+}
+// first record (relative to the tile) of segment s of nseg
+__host__ __device__ __forceinline__ int unit_begin(int ns, int nseg, int s)
+{
+    return (int)(((long long)s * ns) / nseg);
+}
 // positions that share leaf row di / leaf column dj
 __host__ __device__ __forceinline__ uint32_t step_rowmask(int di)
 {

@@ -270,7 +270,8 @@ def multiply_async(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig, c:
         plan.steps = _Span(arena, lay.steps, (step_cap, _lib.STEP_WORDS), i32t)
         plan.c_keys = _Span(arena, lay.c_keys, (leaf_cap,), i32t)
         plan.tile_off = _Span(arena, lay.tile_off, (leaf_cap + 1,), i32t)
-        plan.tile_order = _Span(arena, lay.tile_order, (leaf_cap,), i32t)
+        # units followed by the chain flags, as in symbolic.PlanAlloc (the arena keeps them adjacent)
+        plan.tile_order = _Span(arena, lay.tile_order, (2 * leaf_cap + _lib.UNIT_EXTRA,), i32t)
         plan.counts = _Span(arena, lay.counts, (_lib.PLAN_COUNTS,), i32t)
         grids = _Grids(cd, _Span(arena, lay.slot, (cells,), i32t), _Span(arena, lay.slot_t, (cells,), i32t),
                        _Span(arena, lay.norm, (total,), f32t), _Span(arena, lay.norm_t, (total,), f32t))

@@ -103,8 +103,11 @@ class MultiplyPlan:
         return self.n_tasks
 
     def buffers(self) -> _lib.PlanBuffers:
-        return _lib.PlanBuffers(_ptr(self._steps), _ptr(self._c_keys), _ptr(self._tile_off), _ptr(self._tile_order),
-                                self._steps.shape[0], self._c_keys.shape[0], _ptr(self._counts))
+        leaf_cap = self._c_keys.shape[0]       # tile_order tensor: units, then the chain flags
+        order = _ptr(self._tile_order)
+        return _lib.PlanBuffers(_ptr(self._steps), _ptr(self._c_keys), _ptr(self._tile_off), order,
+                                order + 4 * (leaf_cap + _lib.UNIT_EXTRA), self._steps.shape[0], leaf_cap,
+                                _ptr(self._counts))
 
     # device arrays; after an asynchronous multiply they are regions of its arena (tree._Span)
     steps = _lazy_tensor("steps")
@@ -280,12 +283,14 @@ class PlanAlloc:
         self.steps = torch.empty((step_cap, _lib.STEP_WORDS), dtype=torch.int32, device=dev)
         self.c_keys = torch.empty((leaf_cap,), dtype=torch.int32, device=dev)
         self.tile_off = torch.empty((leaf_cap + 1,), dtype=torch.int32, device=dev)
-        self.tile_order = torch.empty((leaf_cap,), dtype=torch.int32, device=dev)
+        self.tile_order = torch.empty((2 * leaf_cap + _lib.UNIT_EXTRA,), dtype=torch.int32, device=dev)
         self.counts = torch.empty((_lib.PLAN_COUNTS,), dtype=torch.int32, device=dev)
         self.ws_bytes = _lib.lib().spamm_plan_workspace_bytes(depth, step_cap, leaf_cap)
         self.ws = torch.empty((self.ws_bytes,), dtype=torch.uint8, device=dev)
         self.struct = _lib.PlanBuffers(self.steps.data_ptr(), self.c_keys.data_ptr(), self.tile_off.data_ptr(),
-                                       self.tile_order.data_ptr(), step_cap, leaf_cap, self.counts.data_ptr())
+                                       self.tile_order.data_ptr(),
+                                       self.tile_order.data_ptr() + 4 * (leaf_cap + _lib.UNIT_EXTRA), step_cap, leaf_cap,
+                                       self.counts.data_ptr())
 
 
 def plan_capacity(a: QuadtreeMatrix, b: QuadtreeMatrix, tau: float, depth: int, r0: int, r1: int):
