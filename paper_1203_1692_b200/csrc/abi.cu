@@ -1,4 +1,6 @@
 // Library-level entry points of the C ABI (include/spamm_b200.h).
+#include <stdlib.h>
+
 #include <atomic>
 
 #include "common.cuh"
@@ -6,6 +8,15 @@
 static std::atomic<int64_t> g_launches{0};
 
 void spamm_note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+bool spamm_pdl_enabled()
+{
+    static const bool on = [] {
+        const char *e = getenv("SPAMM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 extern "C" int64_t spamm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 

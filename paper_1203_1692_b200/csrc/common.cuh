@@ -25,6 +25,35 @@ void spamm_note_launch(int n = 1);
         }                                                         \
     } while (0)
 
+// ---- programmatic dependent launch ------------------------------------------------------------------
+// The kernels of one multiply run back to back on one stream.  Launched with the programmatic
+// stream serialization attribute, a kernel's CTAs may become resident while its predecessor is
+// still running; every such kernel first waits for the predecessor's completion (and memory
+// flush) with pdl_enter(), which also lets ITS successor start launching.  Only the launch latency
+// and the prologue overlap; no kernel touches memory before its predecessor has finished.
+__device__ __forceinline__ void pdl_enter()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool spamm_pdl_enabled();      // SPAMM_PDL=0 turns the attribute off (abi.cu)
+template <typename... Params, typename... Args>
+inline cudaError_t spamm_launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                    Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = spamm_pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, Params(args)...);
+}
+
 // Level t of a level buffer starts at element spamm_level_offset(t): levels are packed root
 // first, each start rounded to 4 elements so rows can be read with vector loads.
 __host__ __device__ static inline int64_t spamm_level_offset(int t)

@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
+    pdl_enter();
     if (threadIdx.x == 0) {
         for (int s = 0; s < nstages; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -504,7 +505,7 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     static const char *trace_path = getenv("SPAMM_EX_TRACE");     // tuning aid: allocates and synchronises
     if (trace_path && cudaMalloc(&g.trace, sizeof(unsigned long long) * 4 * grid) != cudaSuccess) g.trace = nullptr;
     if (g.trace) cudaMemsetAsync(g.trace, 0, sizeof(unsigned long long) * 4 * grid, st);
-    kern<<<grid, EX_THREADS, smem, st>>>(g);
+    if (spamm_launch_pdl(kern, dim3(grid), dim3(EX_THREADS), smem, st, g) != cudaSuccess) return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
     if (g.trace) {
         unsigned long long *h = (unsigned long long *)malloc(sizeof(unsigned long long) * 4 * grid);

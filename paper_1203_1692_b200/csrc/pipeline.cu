@@ -3,10 +3,15 @@
 // beta == 0 case).  Every count the later kernels need (product leaves, step records, super-tile
 // nodes) stays in device memory; buffers are sized by capacities and an overflow is flagged in
 // plan.counts[2] for the caller to check whenever it first synchronises.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 int spamm_clear_leaf_grids(int depth, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid,
-                           cudaStream_t st);
+                           void *zero0, size_t zero0_bytes, void *zero1, size_t zero1_bytes, cudaStream_t st);
+size_t spamm_plan_zero_bytes(int64_t step_capacity, int64_t leaf_capacity);
+int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
+                    const spamm_plan_buffers *out, void *ws, size_t ws_bytes, bool prezeroed, void *stream);
 int spamm_launch_interior(const double *leaf_sq, int depth, float *norm, float *norm_t, double *sq_levels,
                           unsigned int *ticket, cudaStream_t st);
 int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const spamm_plan_buffers *plan,
@@ -20,15 +25,21 @@ extern "C" int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b
 {
     if (!a || !b || !plan || !c) return SPAMM_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    // C's leaf grids start empty; the numeric kernel's epilogue fills in the product leaves
-    int rc = spamm_clear_leaf_grids(c->depth, c->slot, c->slot_t, c->norm, c->norm_t, c->leaf_sq_grid, st);
+    // C's leaf grids start empty (the numeric kernel's epilogue fills in the product leaves); the same
+    // kernel clears the planner's look-back state and the plan counts
+    const size_t zero_ws = spamm_plan_zero_bytes(plan->step_capacity, plan->leaf_capacity);
+    if (!plan_ws || plan_ws_bytes < zero_ws) return SPAMM_EWORKSPACE;
+    int rc = spamm_clear_leaf_grids(c->depth, c->slot, c->slot_t, c->norm, c->norm_t, c->leaf_sq_grid, plan_ws, zero_ws,
+                                    plan->counts, SPAMM_PLAN_COUNTS * sizeof(int32_t), st);
     if (rc != SPAMM_OK) return rc;
-    rc = spamm_plan(a, b, tau, row0, row1, plan, plan_ws, plan_ws_bytes, stream);
-    if (rc != SPAMM_OK) return rc;
+    static const int stop = getenv("SPAMM_PIPE_STOP") ? atoi(getenv("SPAMM_PIPE_STOP")) : 0;   // tuning aid: truncate
+    if (stop == 1) return SPAMM_OK;
+    rc = spamm_plan_impl(a, b, tau, row0, row1, plan, plan_ws, plan_ws_bytes, true, stream);
+    if (rc != SPAMM_OK || stop == 2) return rc;
     // executed micro products are counted in plan->counts[8..9]
     rc = spamm_execute_impl(a, b, plan, -1, -1, tau, alpha, granularity, exact, c->values, c->values_t, c->leaf_sq,
                             reinterpret_cast<unsigned long long *>(plan->counts + 8), c, stream);
-    if (rc != SPAMM_OK) return rc;
+    if (rc != SPAMM_OK || stop == 3) return rc;
     // interior norms of C: compute_norms, numeric.py:179 / core.py:331-345
     return spamm_launch_interior(c->leaf_sq_grid, c->depth, c->norm, c->norm_t, c->sq_levels,
                                  reinterpret_cast<unsigned int *>(plan->counts + 10), st);

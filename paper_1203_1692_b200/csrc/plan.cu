@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(ROOT_THREADS) plan_root_kernel(const float *__
                                                                  int32_t *counts_out, int64_t cap_nodes, int64_t cap_tasks,
                                                                  int32_t *overflow)
 {
+    pdl_enter();
     __shared__ uint32_t s_cnt[ROOT_THREADS], s_act[ROOT_THREADS];
     __shared__ uint32_t s_wc[ROOT_THREADS / 32], s_wa[ROOT_THREADS / 32];
     const int S = 1 << level;
@@ -147,6 +148,7 @@ __device__ __forceinline__ uint32_t child_tests(const ExpandArgs &a, uint32_t pi
 
 __global__ void __launch_bounds__(PLAN_THREADS) plan_expand_kernel(ExpandArgs a)
 {
+    pdl_enter();
     __shared__ int s_tile;
     __shared__ uint32_t s_wtasks[PLAN_WARPS], s_wact[PLAN_WARPS];
     __shared__ uint32_t s_base_lo, s_base_hi;
@@ -321,6 +323,7 @@ __device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, uint32_t I, u
 template <bool DENSE>
 __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
 {
+    pdl_enter();
     __shared__ int s_tile;
     __shared__ uint32_t s_wsteps[TILE_WARPS], s_wleaves[TILE_WARPS];
     __shared__ uint32_t s_base_lo, s_base_hi;
@@ -495,6 +498,7 @@ __global__ void __launch_bounds__(256) plan_order_kernel(const int32_t *__restri
                                                          int grid_ctas, int32_t *__restrict__ chain,
                                                          int64_t leaf_capacity)
 {
+    pdl_enter();
     // the numeric kernel's per-leaf hand-over flags start clear
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < leaf_capacity; x += (int64_t)gridDim.x * blockDim.x)
         chain[x] = 0;
@@ -660,8 +664,15 @@ extern "C" size_t spamm_plan_workspace_bytes(int depth, int64_t step_capacity, i
     return carve(nullptr, step_capacity, leaf_capacity).total;
 }
 
-extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
-                          const spamm_plan_buffers *out, void *ws, size_t ws_bytes, void *stream)
+// bytes at the start of the workspace that must be zero when the planner starts
+size_t spamm_plan_zero_bytes(int64_t step_capacity, int64_t leaf_capacity)
+{
+    return carve(nullptr, step_capacity, leaf_capacity).zero_bytes;
+}
+
+// prezeroed: the caller has already cleared that region and out->counts on the stream
+int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
+                    const spamm_plan_buffers *out, void *ws, size_t ws_bytes, bool prezeroed, void *stream)
 {
     if (!a || !b || !out || !ws) return SPAMM_EINVAL;
     if (!(tau >= 0.0)) return SPAMM_EINVAL;                       // NaN or negative (symbolic.py:99-100)
@@ -670,8 +681,10 @@ extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, do
     cudaStream_t st = (cudaStream_t)stream;
     PlanWorkspace w = carve(ws, out->step_capacity, out->leaf_capacity);
     if (ws_bytes < w.total) return SPAMM_EWORKSPACE;
-    if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return SPAMM_ECUDA;
-    if (cudaMemsetAsync(out->counts, 0, SPAMM_PLAN_COUNTS * sizeof(int32_t), st) != cudaSuccess) return SPAMM_ECUDA;
+    if (!prezeroed) {
+        if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return SPAMM_ECUDA;
+        if (cudaMemsetAsync(out->counts, 0, SPAMM_PLAN_COUNTS * sizeof(int32_t), st) != cudaSuccess) return SPAMM_ECUDA;
+    }
 
     const int depth = a->depth;
     const int tl = depth >= 2 ? depth - 2 : 0;          // super-tile level
@@ -681,9 +694,10 @@ extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, do
     const bool dense = tl <= 6 && out->leaf_capacity >= (int64_t(1) << (2 * tl));
     const int grid = SPAMM_NUM_SMS * 4;
     if (!dense) {
-    plan_root_kernel<<<1, ROOT_THREADS, 0, st>>>(a->norm + spamm_level_offset(l0), b->norm_t + spamm_level_offset(l0), l0,
-                                        depth - l0, row0, row1, tau, w.buf[cur], w.shared->counts[l0],
-                                        out->leaf_capacity, out->step_capacity, overflow);
+    if (spamm_launch_pdl(plan_root_kernel, dim3(1), dim3(ROOT_THREADS), 0, st, a->norm + spamm_level_offset(l0),
+                         b->norm_t + spamm_level_offset(l0), l0, depth - l0, row0, row1, tau, w.buf[cur],
+                         w.shared->counts[l0], out->leaf_capacity, out->step_capacity, overflow) != cudaSuccess)
+        return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
     for (int lvl = l0; lvl < tl; ++lvl) {
         ExpandArgs x;
@@ -700,7 +714,7 @@ extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, do
         x.overflow = overflow; x.max_list = max_list;
         x.tile_counter = &w.shared->tile_counter[lvl];
         x.tile_state = w.tile_state[lvl];
-        plan_expand_kernel<<<grid, PLAN_THREADS, 0, st>>>(x);
+        if (spamm_launch_pdl(plan_expand_kernel, dim3(grid), dim3(PLAN_THREADS), 0, st, x) != cudaSuccess) return SPAMM_ECUDA;
         SPAMM_CHECK_LAUNCH();
         cur ^= 1;
     }
@@ -726,14 +740,22 @@ extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, do
     t.counts = out->counts;
     t.tile_counter = &w.shared->tile_counter[PLAN_MAX_LEVELS];
     t.tile_state = w.tile_state[PLAN_MAX_LEVELS];
-    if (dense) plan_tiles_kernel<true><<<SPAMM_NUM_SMS, TILE_THREADS, 0, st>>>(t);
-    else plan_tiles_kernel<false><<<SPAMM_NUM_SMS * 2, TILE_THREADS, 0, st>>>(t);
+    if (spamm_launch_pdl(dense ? plan_tiles_kernel<true> : plan_tiles_kernel<false>,
+                         dim3(dense ? SPAMM_NUM_SMS : SPAMM_NUM_SMS * 2), dim3(TILE_THREADS), 0, st, t) != cudaSuccess)
+        return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
     static const int unit_target = plan_env("SPAMM_UNIT_TARGET", 6 * 2 * SPAMM_NUM_SMS, 0, SPAMM_UNIT_EXTRA);
     static const int min_seg = plan_env("SPAMM_UNIT_MIN_SEG", 2, 1, 1024);
-    plan_order_kernel<<<SPAMM_NUM_SMS, 256, 0, st>>>(out->tile_off, out->counts, w.shared->bins, w.shared->cursor,
-                                                     out->tile_order, unit_target, min_seg, spamm_execute_grid(),
-                                                     out->chain, out->leaf_capacity);
+    if (spamm_launch_pdl(plan_order_kernel, dim3(SPAMM_NUM_SMS), dim3(256), 0, st, out->tile_off, out->counts,
+                         w.shared->bins, w.shared->cursor, out->tile_order, unit_target, min_seg, spamm_execute_grid(),
+                         out->chain, out->leaf_capacity) != cudaSuccess)
+        return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
+}
+
+extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
+                          const spamm_plan_buffers *out, void *ws, size_t ws_bytes, void *stream)
+{
+    return spamm_plan_impl(a, b, tau, row0, row1, out, ws, ws_bytes, false, stream);
 }

@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(256) interior_kernel(const double *__restrict_
     __shared__ double s_sq[2][16][16];
     __shared__ unsigned char s_pr[2][16][16];
     __shared__ bool s_last;
+    pdl_enter();
     interior_fold(child_sq, norm, norm_t, sq_levels, tc, blockIdx.x, blockIdx.y, s_sq, s_pr);
     if (!ticket || tc <= 5) return;
     __threadfence();
@@ -301,7 +302,9 @@ int spamm_launch_interior(const double *leaf_sq, int depth, float *norm, float *
         const int Sp = 1 << (tc - 1);
         const int g = (Sp + 15) / 16;
         const bool fuse = ticket && tc > 5 && tc - 5 <= 5;      // the rest fits one block
-        interior_kernel<<<dim3(g, g), 256, 0, st>>>(child, norm, norm_t, sq_levels, tc, fuse ? ticket : nullptr);
+        if (spamm_launch_pdl(interior_kernel, dim3(g, g), dim3(256), 0, st, child, norm, norm_t, sq_levels, tc,
+                             fuse ? ticket : (unsigned int *)nullptr) != cudaSuccess)
+            return SPAMM_ECUDA;
         SPAMM_CHECK_LAUNCH();
         if (fuse) break;
         tc = (tc - 5 > 0) ? tc - 5 : 0;
@@ -398,9 +401,16 @@ extern "C" int spamm_transpose_records(const float *values, int64_t nleaf, float
 }
 
 // Grids of a tree given by packed leaves: clear, then scatter.
+// zero / nzero: optionally a region of 32-bit words to clear as well (the planner's workspace and
+// counts when the multiply pipeline runs this kernel first)
 __global__ void clear_grids_kernel(int64_t cells, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t,
-                                   double *leaf_sq_grid)
+                                   double *leaf_sq_grid, uint32_t *zero0, int64_t nzero0, uint32_t *zero1, int64_t nzero1)
 {
+    pdl_enter();
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nzero0; x += (int64_t)gridDim.x * blockDim.x)
+        zero0[x] = 0u;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nzero1; x += (int64_t)gridDim.x * blockDim.x)
+        zero1[x] = 0u;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < cells; x += (int64_t)gridDim.x * blockDim.x) {
         slot[x] = -1;
         slot_t[x] = -1;
@@ -429,7 +439,7 @@ __global__ void scatter_leaves_kernel(const uint32_t *__restrict__ keys, const d
 }
 
 int spamm_clear_leaf_grids(int depth, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid,
-                           cudaStream_t st)
+                           void *zero0, size_t zero0_bytes, void *zero1, size_t zero1_bytes, cudaStream_t st)
 {
     if (depth < 0 || depth > 15) return SPAMM_EINVAL;
     const int L = 1 << depth;
@@ -437,7 +447,10 @@ int spamm_clear_leaf_grids(int depth, int32_t *slot, int32_t *slot_t, float *nor
     const int64_t off = spamm_level_offset(depth);
     int blocks = (int)((cells + 255) / 256);
     if (blocks > SPAMM_NUM_SMS * 16) blocks = SPAMM_NUM_SMS * 16;
-    clear_grids_kernel<<<blocks, 256, 0, st>>>(cells, slot, slot_t, norm + off, norm_t + off, leaf_sq_grid);
+    if (spamm_launch_pdl(clear_grids_kernel, dim3(blocks), dim3(256), 0, st, cells, slot, slot_t, norm + off, norm_t + off,
+                         leaf_sq_grid, reinterpret_cast<uint32_t *>(zero0), (int64_t)(zero0_bytes / 4),
+                         reinterpret_cast<uint32_t *>(zero1), (int64_t)(zero1_bytes / 4)) != cudaSuccess)
+        return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
 }
@@ -452,7 +465,8 @@ int spamm_index_leaves_impl(const uint32_t *keys, const double *leaf_sq_packed, 
     const int64_t off = spamm_level_offset(depth);
     int blocks = (int)((cells + 255) / 256);
     if (blocks > SPAMM_NUM_SMS * 16) blocks = SPAMM_NUM_SMS * 16;
-    clear_grids_kernel<<<blocks, 256, 0, st>>>(cells, slot, slot_t, norm + off, norm_t + off, leaf_sq_grid);
+    clear_grids_kernel<<<blocks, 256, 0, st>>>(cells, slot, slot_t, norm + off, norm_t + off, leaf_sq_grid, nullptr, 0,
+                                               nullptr, 0);
     SPAMM_CHECK_LAUNCH();
     if (nleaf > 0) {
         int sb = (int)((nleaf + 255) / 256);
