@@ -273,7 +273,12 @@ def run_single(args, torch, P, local: int) -> None:
     # ---- end to end through the public API with host buffers
     host_a = torch.from_numpy(a_d).pin_memory()
     host_b = host_a if b_d is None else torch.from_numpy(b_d).pin_memory()
-    host_c = torch.empty((a_d.shape[0], (b_d if b_d is not None else a_d).shape[1]), dtype=torch.float32).pin_memory()
+    # the result comes back as the product tree's packed leaves (keys + 272-float leaf records: the
+    # reference's packed_leaves() form, `core.py:387-405`), not as a zero-filled dense matrix
+    cap = plan.n_cleaves
+    host_vals = torch.empty((cap, _lib.REC), dtype=torch.float32).pin_memory()
+    host_keys = torch.empty((cap,), dtype=torch.int32).pin_memory()
+    d2h = 0
     e2e_times = []
     for it in range(2 + max(3, min(args.steps, 20) // 2)):
         flush.fill_(it)
@@ -282,7 +287,10 @@ def run_single(args, torch, P, local: int) -> None:
         ta = P.QuadtreeMatrix.from_dense(host_a)
         tb = ta if b_d is None else P.QuadtreeMatrix.from_dense(host_b)
         cc, _, _ = P.multiply(ta, tb, cfg)
-        host_c.copy_(cc.to_dense_tensor(), non_blocking=True)
+        nc = cc.nleaf                       # reads the counts back (the one synchronisation of the step)
+        host_vals[:nc].copy_(cc.values[:nc], non_blocking=True)
+        host_keys[:nc].copy_(cc.keys[:nc], non_blocking=True)
+        d2h = nc * (_lib.REC * 4 + 4)
         e1.record()
         torch.cuda.synchronize()
         if it >= 2:
@@ -357,7 +365,8 @@ def run_single(args, torch, P, local: int) -> None:
                      "hbm_frac_of_measured": alg_bytes / (k3_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
         "cpu_baseline": cpu,
         "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(host_c.numel() * 4)},
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "result": "product tree as packed leaves (keys + leaf records)"},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "sweep": sweep,
@@ -414,10 +423,13 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
     def step_e2e():
         shard = parallel.shard_from_dense_rows(host_rows, r0)
         c, plan, counters, rows = parallel.multiply_sharded(shard, None, (m, n), (m, n), cfg)
-        block = c.to_dense_tensor()[rows[0] * 16:min(m, rows[1] * 16)]
-        if host_out.get("buf") is None or host_out["buf"].shape != block.shape:
-            host_out["buf"] = torch.empty(block.shape, dtype=torch.float32).pin_memory()
-        host_out["buf"].copy_(block, non_blocking=True)
+        nc = c.nleaf                         # this rank's product leaves, read back as packed leaves
+        if host_out.get("vals") is None or host_out["vals"].shape[0] < nc:
+            host_out["vals"] = torch.empty((nc, 272), dtype=torch.float32).pin_memory()
+            host_out["keys"] = torch.empty((nc,), dtype=torch.int32).pin_memory()
+        host_out["vals"][:nc].copy_(c.values[:nc], non_blocking=True)
+        host_out["keys"][:nc].copy_(c.keys[:nc], non_blocking=True)
+        host_out["bytes"] = nc * (272 * 4 + 4)
         return c, plan, counters, rows
 
     def timed(fn, steps, warmup):
@@ -449,7 +461,7 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
     tot_tasks = sum(float(w[1]) for w in per_rank)
     flops = 128.0 * tot_p4 if cfg.granularity == "fine4" else 8192.0 * tot_tasks
     e2e_ms, _ = timed(step_e2e, max(2, min(args.steps, 5)), 2)
-    d2h = 0 if host_out.get("buf") is None else host_out["buf"].numel() * 4
+    d2h = host_out.get("bytes", 0)
     io = torch.tensor([float(host_rows.numel() * 4), float(d2h)], dtype=torch.float64, device="cuda")
     dist.all_reduce(io)
     if rank == 0:
