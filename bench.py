@@ -201,7 +201,7 @@ def kernel_time_execute(P, torch, plan, qa, qb, cfg, reps, flush):
     lib = _lib.lib()
     dev = qa.device
     nC = plan.n_cleaves
-    va, vb = qa.view(plan.depth), qb.view(plan.depth)
+    va, vb = qa.view(plan.depth), qb.view(plan.depth, left=False)
     vals = torch.empty((nC, _lib.REC), dtype=torch.float32, device=dev)
     vals_t = torch.empty_like(vals)
     leaf_sq = torch.empty((nC,), dtype=torch.float64, device=dev)
@@ -379,8 +379,9 @@ def run_single(args, torch, P, local: int) -> None:
 
 def run_sharded(args, torch, dist, P, local: int) -> None:
     """Config 5 with C's leaf rows split across the ranks.  Timed region of one step, per rank:
-    all-gather of the operand shards -> whole-matrix tree (transposed copies, grids, pyramid) ->
-    plan on the replicated norms -> task-balanced row cut -> fused multiply of the own row block."""
+    tree of the own rows of A (transposed copies, grids, pyramid) -> all-gather of the packed leaves
+    (B = A) -> tree of B (grids and pyramid only) -> fused multiply, which yields the own rows of C.
+    The row blocks are cut by surviving-task count once, at set-up."""
     from paper_1203_1692_b200 import _lib, inputs, parallel
     rank, world = dist.get_rank(), dist.get_world_size()
     name = args.workload or "cfg5"
@@ -409,7 +410,12 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
         dist.broadcast(t, 0)
     full = parallel.tree_from_shard(m, n, whole)
     nrows = -(-m // 16)
-    r0, r1 = parallel.even_row_split(nrows, world)[rank]
+    # the partition of A's rows is the partition of the work: cut by surviving-task count (set-up, untimed)
+    from paper_1203_1692_b200.symbolic import build_plan
+    probe = build_plan(full, full, cfg.tau)
+    counts = parallel.row_task_counts(probe, probe.depth).cpu().numpy()
+    r0, r1 = parallel.balanced_row_split(counts[:nrows], world)[rank]
+    del probe
     mine = parallel.shard_of_tree(full, r0, r1)
     host_rows = full.to_dense_tensor()[r0 * 16:min(m, r1 * 16)].cpu().pin_memory()
     del full, whole
@@ -422,7 +428,7 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
 
     def step_e2e():
         shard = parallel.shard_from_dense_rows(host_rows, r0)
-        c, plan, counters, rows = parallel.multiply_sharded(shard, None, (m, n), (m, n), cfg)
+        c, plan, counters = parallel.multiply_sharded(shard, None, (m, n), (m, n), cfg)
         nc = c.nleaf                         # this rank's product leaves, read back as packed leaves
         if host_out.get("vals") is None or host_out["vals"].shape[0] < nc:
             host_out["vals"] = torch.empty((nc, 272), dtype=torch.float32).pin_memory()
@@ -430,7 +436,7 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
         host_out["vals"][:nc].copy_(c.values[:nc], non_blocking=True)
         host_out["keys"][:nc].copy_(c.keys[:nc], non_blocking=True)
         host_out["bytes"] = nc * (272 * 4 + 4)
-        return c, plan, counters, rows
+        return c, plan, counters
 
     def timed(fn, steps, warmup):
         times, out = [], None
@@ -451,9 +457,9 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
 
     l0 = _lib.launch_count()
     with ClockSampler(local) as clocks:
-        ms, (c, plan, counters, rows) = timed(step_resident, args.steps, args.warmup)
+        ms, (c, plan, counters) = timed(step_resident, args.steps, args.warmup)
     launches = (_lib.launch_count() - l0) * args.steps // (args.steps + args.warmup)
-    work = torch.tensor([float(counters.products4), float(len(plan)), float(r1 - r0), float(rows[1] - rows[0])],
+    work = torch.tensor([float(counters.products4), float(len(plan)), float(r1 - r0), float(c.nleaf)],
                         dtype=torch.float64, device="cuda")
     per_rank = [torch.zeros_like(work) for _ in range(world)]
     dist.all_gather(per_rank, work)
@@ -471,8 +477,8 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": name, "n": m, "tau": args.tau, "granularity": args.granularity,
                        "tasks": int(tot_tasks), "products4": int(tot_p4),
-                       "parallelism": f"C row blocks x{world} balanced by task count, operand shards all-gathered (NCCL) "
-                                      "inside the timed region",
+                       "parallelism": f"row blocks of A and C x{world} cut by task count, B all-gathered (NCCL) inside "
+                                      "the timed region",
                        "tasks_per_rank": [int(w[1]) for w in per_rank],
                        "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write)"},
             "roofline": None, "cpu_baseline": None,

@@ -112,7 +112,8 @@ int spamm_leaf_norms_packed(float *values, int64_t nleaf, float *values_t, doubl
  * from another GPU keep the norms their owner computed): transposition only. */
 int spamm_transpose_records(const float *values, int64_t nleaf, float *values_t, void *stream);
 
-/* Scatter packed leaves (keys ascending, leaf_sq) into the grids of a depth-`depth` tree:
+/* Scatter packed leaves (keys, leaf_sq; a key of 0xFFFFFFFF marks an unused slot and is skipped,
+ * as in a shard gathered from several GPUs) into the grids of a depth-`depth` tree:
  * slot, slot_t, the leaf level of norm/norm_t and the double leaf_sq grid (all L*L). */
 int spamm_index_leaves(const uint32_t *keys, const double *leaf_sq_packed, int64_t nleaf, int depth,
                        int32_t *slot, int32_t *slot_t, float *norm, float *norm_t,

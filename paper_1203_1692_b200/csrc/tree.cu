@@ -379,23 +379,42 @@ extern "C" int spamm_leaf_norms_packed(float *values, int64_t nleaf, float *valu
 // values -> values_t for leaves whose norms are already in the record tails (e.g. leaves that
 // arrived from another GPU): transposes the 16x16 values and the 4x4 sub-norm tail, nothing else.
 __global__ void __launch_bounds__(256) transpose_records_kernel(const float *__restrict__ values,
-                                                                float *__restrict__ values_t)
+                                                                float *__restrict__ values_t, int64_t nleaf)
 {
-    __shared__ float tile[16][17];
-    const int64_t s = blockIdx.x;
-    const int r = threadIdx.x >> 4, c = threadIdx.x & 15;
-    tile[r][c] = values[s * SPAMM_REC + threadIdx.x];
-    __syncthreads();
-    values_t[s * SPAMM_REC + threadIdx.x] = tile[c][r];
-    if (threadIdx.x < 16)   // values tail is [q*4+p], values_t tail is [p*4+q]
-        values_t[s * SPAMM_REC + 256 + (threadIdx.x & 3) * 4 + (threadIdx.x >> 2)] = values[s * SPAMM_REC + 256 + threadIdx.x];
+    // one warp per leaf and pass, 16-byte loads and stores, transposition through shared memory
+    __shared__ float tile[8][16][17];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float(*t)[17] = tile[warp];
+    for (int64_t s = (int64_t)blockIdx.x * 8 + warp; s < nleaf; s += (int64_t)gridDim.x * 8) {
+        const float4 *src = reinterpret_cast<const float4 *>(values + s * SPAMM_REC);
+        float4 *dst = reinterpret_cast<float4 *>(values_t + s * SPAMM_REC);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = lane + 32 * h, r = e >> 2, c = (e & 3) * 4;
+            const float4 v = src[e];
+            t[r][c] = v.x; t[r][c + 1] = v.y; t[r][c + 2] = v.z; t[r][c + 3] = v.w;
+        }
+        float tail = 0.0f;
+        if (lane < 16) tail = values[s * SPAMM_REC + 256 + lane];
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = lane + 32 * h, r = e >> 2, c = (e & 3) * 4;
+            dst[e] = make_float4(t[c][r], t[c + 1][r], t[c + 2][r], t[c + 3][r]);
+        }
+        // values tail is [q*4+p], values_t tail is [p*4+q]
+        if (lane < 16) values_t[s * SPAMM_REC + 256 + (lane & 3) * 4 + (lane >> 2)] = tail;
+        __syncwarp();
+    }
 }
 
 extern "C" int spamm_transpose_records(const float *values, int64_t nleaf, float *values_t, void *stream)
 {
     if (nleaf == 0) return SPAMM_OK;
     if (!values || !values_t || nleaf < 0) return SPAMM_EINVAL;
-    transpose_records_kernel<<<(unsigned)nleaf, 256, 0, (cudaStream_t)stream>>>(values, values_t);
+    int64_t blocks = (nleaf + 7) / 8;
+    if (blocks > SPAMM_NUM_SMS * 16) blocks = SPAMM_NUM_SMS * 16;
+    transpose_records_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(values, values_t, nleaf);
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
 }
@@ -427,6 +446,7 @@ __global__ void scatter_leaves_kernel(const uint32_t *__restrict__ keys, const d
     if (nleaf_dev && (int64_t)*nleaf_dev < nleaf) nleaf = *nleaf_dev;
     for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nleaf; s += (int64_t)gridDim.x * blockDim.x) {
         uint32_t i, j;
+        if (keys[s] == 0xFFFFFFFFu) continue;     // unused slot of a gathered shard
         morton_decode(keys[s], i, j);
         const double sq = leaf_sq_packed[s];
         const float nv = (float)sqrt(sq);       // a stored leaf keeps norm 0 when it is all zero (core.py:336-339)

@@ -138,7 +138,7 @@ def execute_plan(plan: MultiplyPlan, a: QuadtreeMatrix, b: QuadtreeMatrix, c: Qu
     keep_old = cfg.beta != 0 and c.nleaf > 0
     prod = None
     if run:
-        va, vb = a.view(plan.depth), b.view(plan.depth)
+        va, vb = a.view(plan.depth), b.view(plan.depth, left=False)
         vals = torch.empty((nC, _lib.REC), dtype=torch.float32, device=dev)
         vals_t = torch.empty((nC, _lib.REC), dtype=torch.float32, device=dev)
         leaf_sq = torch.empty((nC,), dtype=torch.float64, device=dev)
@@ -259,7 +259,7 @@ def multiply_async(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig, c:
             leaf_cap = max(leaf_cap, 1 << (2 * tl))
         lay = _arena_layout(depth, cd, step_cap, leaf_cap)
         arena = torch.empty((lay.total,), dtype=torch.uint8, device=dev)
-        va, vb = a.view(depth), b.view(depth)
+        va, vb = a.view(depth), b.view(depth, left=False)
         _lib.check(lib.spamm_multiply_arena(C.byref(va), C.byref(vb), float(cfg.tau), gran, int(cfg.exact), alpha32,
                                             r0, r1, cd, step_cap, leaf_cap, arena.data_ptr(), lay.total, _stream()),
                    "multiply")

@@ -123,29 +123,51 @@ def shard_of_tree(tree, r0: int, r1: int) -> PackedShard:
                        tree._packed_leaf_sq()[:n][sel].contiguous())
 
 
+HOLE = -1          # key of an unused slot in a gathered shard (0xFFFFFFFF on the device)
+
+
 def allgather_shards(shard: PackedShard, group=None) -> PackedShard:
-    """Every rank's shard, concatenated in rank order.  Sizes differ, so the counts are gathered
-    first and the payloads padded to the largest shard (one all-gather per array)."""
+    """Every rank's shard in rank order, gathered straight into its final buffers.
+
+    Shard sizes differ, so each rank's part occupies ``cap`` = the largest shard size slots of the
+    result; the unused slots at the end of a part carry the key ``HOLE`` and are never indexed
+    (`spamm_index_leaves` skips them).  One collective per array, no staging copy of the payload
+    beyond padding the rank's own shard; with a single rank nothing is copied at all."""
     world = dist.get_world_size(group)
+    if world == 1:
+        return shard
     dev = shard.keys.device
-    counts = [torch.zeros((1,), dtype=torch.int64, device=dev) for _ in range(world)]
-    dist.all_gather(counts, torch.tensor([shard.n], dtype=torch.int64, device=dev), group=group)
-    counts = [int(c.item()) for c in counts]
-    cap = max(max(counts), 1)
+    sizes = [torch.zeros((1,), dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([shard.n], dtype=torch.int64, device=dev), group=group)
+    cap = max(max(int(c.item()) for c in sizes), 1)
 
-    def gather(x: torch.Tensor) -> torch.Tensor:
-        pad = torch.zeros((cap,) + tuple(x.shape[1:]), dtype=x.dtype, device=dev)
+    def gather(x: torch.Tensor, fill) -> torch.Tensor:
+        pad = torch.empty((cap,) + tuple(x.shape[1:]), dtype=x.dtype, device=dev)
         pad[: x.shape[0]] = x
-        outs = [torch.empty_like(pad) for _ in range(world)]
-        dist.all_gather(outs, pad, group=group)
-        return torch.cat([outs[r][: counts[r]] for r in range(world)], dim=0)
+        if fill is not None:
+            pad[x.shape[0]:] = fill
+        out = torch.empty((world * cap,) + tuple(x.shape[1:]), dtype=x.dtype, device=dev)
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(out, pad, group=group)
+        else:
+            dist.all_gather(list(out.chunk(world)), pad, group=group)
+        return out
 
-    return PackedShard(gather(shard.keys), gather(shard.records), gather(shard.leaf_sq))
+    return PackedShard(gather(shard.keys, HOLE), gather(shard.records, None), gather(shard.leaf_sq, 0.0))
 
 
-def tree_from_shard(m: int, n: int, shard: PackedShard, device=None):
-    """Whole-matrix tree from gathered leaves: transposed copies, leaf grids and the norm pyramid are
-    rebuilt on the device; the leaf norms are the ones their owners computed."""
+def drop_holes(shard: PackedShard) -> PackedShard:
+    """The stored leaves of a gathered shard, unused slots removed (tests and host export)."""
+    keep = torch.nonzero(shard.keys != HOLE).flatten()
+    return PackedShard(shard.keys[keep], shard.records[keep], shard.leaf_sq[keep])
+
+
+def tree_from_shard(m: int, n: int, shard: PackedShard, device=None, transposed: bool = True):
+    """Tree of an m x n matrix from packed leaves (global keys, possibly with HOLE slots): leaf
+    grids and the norm pyramid are built on the device from the norms the owners computed.
+
+    ``transposed=False`` skips the transposed leaf copies: enough for a right-hand operand, which the
+    numeric kernel reads through ``values`` only (the left-hand operand is read through ``values_t``)."""
     from . import _lib
     from .tree import QuadtreeMatrix, _stream
     q = QuadtreeMatrix(m, n, device=device)
@@ -155,11 +177,13 @@ def tree_from_shard(m: int, n: int, shard: PackedShard, device=None):
     keys = shard.keys.to(q.device).contiguous()
     values = shard.records.to(q.device).contiguous()
     leaf_sq = shard.leaf_sq.to(q.device).contiguous()
-    values_t = torch.empty_like(values)
-    _lib.check(_lib.lib().spamm_transpose_records(values.data_ptr(), cnt, values_t.data_ptr(), _stream()),
-               "transpose_records")
+    values_t = None
+    if transposed:
+        values_t = torch.empty_like(values)
+        _lib.check(_lib.lib().spamm_transpose_records(values.data_ptr(), cnt, values_t.data_ptr(), _stream()),
+                   "transpose_records")
     q._adopt_packed(keys, values, values_t, leaf_sq, cnt)
-    q._keys_sorted = False          # rank order, not one ascending Morton sequence
+    q._keys_sorted = False          # rank order with unused slots, not one ascending Morton sequence
     return q
 
 
@@ -176,21 +200,15 @@ def row_task_counts(plan, depth: int) -> torch.Tensor:
 
 def multiply_sharded(a_shard: PackedShard, b_shard: PackedShard | None, shape_a: tuple[int, int],
                      shape_b: tuple[int, int], cfg, group=None, device=None):
-    """C = A B with C's leaf rows split across the ranks of ``group``.
+    """C = A B with C's leaf rows split across the ranks of ``group`` like the rows of A.
 
     ``a_shard`` / ``b_shard`` are this rank's row blocks of the operands (``b_shard is None`` means
-    B is A).  Returns ``(c, plan, counters, (r0, r1))``: ``c`` has the global shape and holds this
-    rank's rows [r0, r1) of product leaves."""
+    B is A).  The one exchange step is the all-gather of B's packed leaves.  The left operand stays
+    local: a tree holding only this rank's rows of A times the whole of B gives exactly this rank's
+    rows of C, so the partition of A (see ``balanced_row_split``) is the partition of the work.
+    Returns ``(c, plan, counters)``; ``c`` has the global shape and holds this rank's rows."""
     from .numeric import multiply_async
-    from .symbolic import build_plan
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
-    a_full = tree_from_shard(shape_a[0], shape_a[1], allgather_shards(a_shard, group), device)
-    b_full = a_full if b_shard is None else tree_from_shard(shape_b[0], shape_b[1],
-                                                            allgather_shards(b_shard, group), device)
-    # balance: every rank plans the whole product on the replicated norms (cheap) and cuts alike
-    plan = build_plan(a_full, b_full, cfg.tau)
-    counts = row_task_counts(plan, plan.depth).cpu().numpy()
-    nrows = -(-shape_a[0] // 16)
-    r0, r1 = balanced_row_split(counts[:nrows], world)[rank]
-    c, myplan, counters = multiply_async(a_full, b_full, cfg, None, row_range=(r0, r1))
-    return c, myplan, counters, (r0, r1)
+    a_local = tree_from_shard(shape_a[0], shape_a[1], a_shard, device)
+    b_full = tree_from_shard(shape_b[0], shape_b[1], allgather_shards(a_shard if b_shard is None else b_shard, group),
+                             device, transposed=False)
+    return multiply_async(a_local, b_full, cfg, None)

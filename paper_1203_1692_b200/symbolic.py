@@ -255,7 +255,7 @@ def build_plan(a: QuadtreeMatrix, b: QuadtreeMatrix, tau: float,
         z = torch.zeros((1, _lib.STEP_WORDS), dtype=torch.int32, device=dev)
         e = torch.zeros((_lib.PLAN_COUNTS,), dtype=torch.int32, device=dev)
         return MultiplyPlan(tau, depth, 0, 0, 0, z, e, e, e, e, a, b, (r0, r1))
-    va, vb = a.view(depth), b.view(depth)
+    va, vb = a.view(depth), b.view(depth, left=False)
     hint_key, (step_cap, leaf_cap) = plan_capacity(a, b, tau, depth, r0, r1)
     while True:
         pb = PlanAlloc(dev, depth, step_cap, leaf_cap)

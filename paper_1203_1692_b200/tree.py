@@ -306,10 +306,17 @@ class QuadtreeMatrix:
         g = self._grids.get(depth)
         return g if g is not None else self._index(depth)
 
-    def view(self, depth: int | None = None) -> _lib.TreeView:
-        """ctypes view for the kernels, indexed at a (possibly larger) common depth."""
+    def view(self, depth: int | None = None, left: bool = True) -> _lib.TreeView:
+        """ctypes view for the kernels, indexed at a (possibly larger) common depth.  A tree built
+        without transposed leaf copies (a gathered right-hand operand, parallel.tree_from_shard)
+        gets them on its first use as a left-hand operand."""
         g = self.grids(depth)
         nz = self._nleaf is None or self._nleaf > 0        # do not force a pending count to the host
+        if left and nz and self._values_t is None and self._values is not None:
+            vt = torch.empty_like(self.values)
+            _lib.check(_lib.lib().spamm_transpose_records(self.values.data_ptr(), self.values.shape[0], vt.data_ptr(),
+                                                          _stream()), "transpose_records")
+            self.values_t = vt
         return _lib.TreeView(self.m, self.n, g.depth, self._leaf_bound() if nz else 0,
                              _ptr(self._keys) if nz else None, _ptr(self._values) if nz else None,
                              _ptr(self._values_t) if nz else None,
@@ -338,11 +345,13 @@ class QuadtreeMatrix:
         n = self.nleaf
         if n == 0:
             return (np.empty(0, np.uint64), np.empty((0, 16, 16), np.float32), np.empty((0, 4, 4), np.float32))
-        keys = self.keys[:n].cpu().numpy().astype(np.uint64)
-        vals = np.ascontiguousarray(self.values[:n, :256].cpu().numpy()).reshape(n, 16, 16)
-        subs = np.ascontiguousarray(self.values_t[:n, 256:].cpu().numpy()).reshape(n, 4, 4)
-        if not getattr(self, "_keys_sorted", True):     # gathered from several ranks: rank order
-            order = np.argsort(keys, kind="stable")
+        keys = self.keys[:n].cpu().numpy().astype(np.uint32).astype(np.uint64)
+        rec = self.values[:n].cpu().numpy()
+        vals = np.ascontiguousarray(rec[:, :256]).reshape(n, 16, 16)
+        subs = np.ascontiguousarray(rec[:, 256:].reshape(n, 4, 4).transpose(0, 2, 1))   # tail is [q][p]
+        if not getattr(self, "_keys_sorted", True):     # gathered from several ranks: rank order, unused slots
+            keep = np.flatnonzero(keys != 0xFFFFFFFF)
+            order = keep[np.argsort(keys[keep], kind="stable")]
             keys, vals, subs = keys[order], vals[order], subs[order]
         return keys, vals, subs
 

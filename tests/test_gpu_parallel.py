@@ -51,3 +51,51 @@ def test_row_blocks_reproduce_single_gpu_product(world):
     assert np.array_equal(got, dense_ref)
     loads = np.array([counts[r0:r1].sum() for r0, r1 in split])
     assert loads.max() <= 1.35 * loads.mean()
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_local_rows_of_a_times_gathered_b(world):
+    """parallel.multiply_sharded's data flow without the collective: every rank multiplies a tree of
+    its own rows of A by B rebuilt from the gathered buffer (fixed stride per rank, HOLE keys in
+    the unused slots, no transposed copies) and gets exactly its rows of the single-GPU product."""
+    import paper_1203_1692_b200 as P
+    n, tau = 1000, 1e-6                       # ragged: 62.5 leaf rows
+    a = inputs.exponential_decay(n, 0.9, seed=2)
+    b = inputs.exponential_decay(n, 0.93, seed=5)
+    qa, qb = P.QuadtreeMatrix.from_dense(a), P.QuadtreeMatrix.from_dense(b)
+    cfg = P.MultiplyConfig(tau=tau, exact=True)
+    c_ref, plan_ref, k_ref = P.multiply(qa, qb, cfg)
+    dense_ref = c_ref.to_dense().data
+    nrows = -(-n // 16)
+    split = parallel.even_row_split(nrows, world)
+    b_shards = [parallel.shard_of_tree(qb, r0, r1) for r0, r1 in split]
+    cap = max(s.n for s in b_shards)
+    dev = b_shards[0].keys.device
+    keys = torch.full((world * cap,), parallel.HOLE, dtype=torch.int32, device=dev)
+    recs = torch.full((world * cap, 272), float("nan"), dtype=torch.float32, device=dev)   # garbage must never be read
+    sq = torch.zeros((world * cap,), dtype=torch.float64, device=dev)
+    for r, s in enumerate(b_shards):
+        keys[r * cap:r * cap + s.n] = s.keys
+        recs[r * cap:r * cap + s.n] = s.records
+        sq[r * cap:r * cap + s.n] = s.leaf_sq
+    b_full = parallel.tree_from_shard(n, n, parallel.PackedShard(keys, recs, sq), transposed=False)
+    assert np.array_equal(b_full.to_dense().data, b)
+    bk, bv, bs = b_full.packed_leaves()
+    rk, rv, rs = qb.packed_leaves()
+    assert np.array_equal(bk, rk) and np.array_equal(bv, rv) and np.array_equal(bs, rs)
+    got = np.zeros_like(dense_ref)
+    tasks = p4 = 0
+    for r0, r1 in split:
+        a_local = parallel.tree_from_shard(n, n, parallel.shard_of_tree(qa, r0, r1))
+        c, p, k = P.numeric.multiply_async(a_local, b_full, cfg, None)
+        d = c.to_dense().data
+        assert not d[:r0 * 16].any() and not d[r1 * 16:].any()
+        got[r0 * 16:r1 * 16] = d[r0 * 16:r1 * 16]
+        tasks += len(p)
+        p4 += k.products4
+    assert tasks == len(plan_ref) and p4 == k_ref.products4
+    assert np.array_equal(got, dense_ref)
+    # a right-hand-only tree still works on the left: the transposed copies are made on first use
+    c2, _, _ = P.multiply(b_full, qa, P.MultiplyConfig(tau=tau, exact=True))
+    c3, _, _ = P.multiply(qb, qa, P.MultiplyConfig(tau=tau, exact=True))
+    assert np.array_equal(c2.to_dense().data, c3.to_dense().data)

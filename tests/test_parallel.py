@@ -87,7 +87,14 @@ def _worker(rank: int, world: int, port: int, n: int, tau: float, out_dir: str):
         nrows = -(-n // 16)
         r0, r1 = parallel.even_row_split(nrows, world)[rank]
         mine = _shard_of_oracle_tree(full, r0, r1)
-        gathered = parallel.allgather_shards(mine)                      # the one exchange step
+        raw = parallel.allgather_shards(mine)                           # the one exchange step
+        # every rank's part sits at a fixed stride; the unused slots behind a part carry the HOLE key
+        assert raw.n % world == 0 and int((raw.keys != parallel.HOLE).sum()) == full.keys.size
+        part = raw.keys.numpy().reshape(world, -1)
+        for r in range(world):
+            used = part[r] != parallel.HOLE
+            assert not used[np.argmin(used):].any() or used.all()         # holes only at the end of a part
+        gathered = parallel.drop_holes(raw)
         # the gathered leaves are exactly the stored leaves of the whole matrix, with their norms
         order = np.argsort(gathered.keys.numpy().astype(np.uint64), kind="stable")
         assert np.array_equal(gathered.keys.numpy().astype(np.uint64)[order], full.keys.astype(np.uint64))
