@@ -108,6 +108,14 @@ int spamm_build_interior(const double *leaf_sq, int depth, float *norm, float *n
 int spamm_leaf_norms_packed(float *values, int64_t nleaf, float *values_t, double *leaf_sq,
                             void *stream);
 
+/* QuadtreeMatrix.sparsify (core.py:347-383) on packed leaves: zeroes every 4x4 sub-block with
+ * 0 < sub-norm < eps in both record layouts, refreshes the norms of the leaves it touched
+ * (compute_norms order) and sets leaf_sq of the untouched ones to float64(norm)^2, the value the
+ * reference feeds to the interior sums.  *dropped += zeroed sub-blocks.  Leaves left with
+ * leaf_sq == 0 are to be removed by the caller before re-indexing. */
+int spamm_sparsify_leaves(float *values, float *values_t, double *leaf_sq, int64_t nleaf, float eps,
+                          unsigned long long *dropped, void *stream);
+
 /* values_t records from values records whose sub-norm tails are already filled (leaves received
  * from another GPU keep the norms their owner computed): transposition only. */
 int spamm_transpose_records(const float *values, int64_t nleaf, float *values_t, void *stream);

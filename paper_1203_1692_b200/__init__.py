@@ -8,7 +8,8 @@ All arithmetic runs in hand-written CUDA kernels for sm_100a behind the C ABI in
 """
 
 from .morton import c_index, decode, encode, k_match, k_of_a, k_of_b  # noqa: F401
-from .tree import DEFAULT_BLOCK, DenseMatrix, QuadtreeMatrix, TreeNode, tree_depth  # noqa: F401
+from .tree import DEFAULT_BLOCK, DenseMatrix, QuadtreeMatrix, TreeNode, drop_tolerance, tree_depth  # noqa: F401
+from .io import QUADTREE_MAGIC, MatrixFormatError, load_quadtree, save_quadtree  # noqa: F401
 from .symbolic import MultiplyPlan, PlanStats, ProductTask, build_plan, plan_dump, plan_stats  # noqa: F401
 from .numeric import (  # noqa: F401
     GRANULARITIES,

@@ -376,6 +376,64 @@ extern "C" int spamm_leaf_norms_packed(float *values, int64_t nleaf, float *valu
     return SPAMM_OK;
 }
 
+// QuadtreeMatrix.sparsify (core.py:347-383): zero every 4x4 sub-block with 0 < sub-norm < eps.  A
+// leaf that lost a sub-block gets its norms refreshed in compute_norms order; an untouched leaf
+// keeps its norms and contributes float64(norm)^2 to the interior sums, as the reference does.
+// 16 threads per leaf, thread (p,q) owns one sub-block.  dropped += number of zeroed sub-blocks.
+__global__ void __launch_bounds__(256) sparsify_kernel(float *__restrict__ values, float *__restrict__ values_t,
+                                                       double *__restrict__ leaf_sq, int64_t nleaf, float eps,
+                                                       unsigned long long *dropped)
+{
+    const int64_t leaf = (int64_t)blockIdx.x * 16 + (threadIdx.x >> 4);
+    const int t = threadIdx.x & 15, p = t >> 2, q = t & 3;
+    const bool ok = leaf < nleaf;
+    const float sn = ok ? values[leaf * SPAMM_REC + 256 + q * 4 + p] : 0.0f;
+    const bool drop = ok && sn > 0.0f && sn < eps;
+    const uint32_t bal = __ballot_sync(FULL_MASK, drop);
+    const uint32_t mine = (bal >> (threadIdx.x & 16)) & 0xFFFFu;      // my leaf's 16 lanes
+    float4 r[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        r[i] = (ok && !drop) ? *reinterpret_cast<const float4 *>(values + leaf * SPAMM_REC + (4 * p + i) * 16 + 4 * q)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+    const double S = sub_block_sq(r[0], r[1], r[2], r[3]);
+    const double total = leaf_total_refresh(S);
+    if (!ok) return;
+    if (!mine) {
+        if (t == 0) {
+            const double nv = (double)(float)sqrt(leaf_sq[leaf]);
+            leaf_sq[leaf] = nv * nv;
+        }
+        return;
+    }
+    if (drop) {
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        float *v = values + leaf * SPAMM_REC, *vt = values_t + leaf * SPAMM_REC;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            *reinterpret_cast<float4 *>(v + (4 * p + i) * 16 + 4 * q) = z;
+            *reinterpret_cast<float4 *>(vt + (4 * q + i) * 16 + 4 * p) = z;
+        }
+        v[256 + q * 4 + p] = 0.0f;
+        vt[256 + t] = 0.0f;
+    }
+    if (t == 0) {
+        leaf_sq[leaf] = total;
+        atomicAdd(dropped, (unsigned long long)__popc(mine));
+    }
+}
+
+extern "C" int spamm_sparsify_leaves(float *values, float *values_t, double *leaf_sq, int64_t nleaf, float eps,
+                                     unsigned long long *dropped, void *stream)
+{
+    if (nleaf == 0) return SPAMM_OK;
+    if (!values || !values_t || !leaf_sq || !dropped || nleaf < 0 || !(eps >= 0.0f)) return SPAMM_EINVAL;
+    sparsify_kernel<<<(unsigned)((nleaf + 15) / 16), 256, 0, (cudaStream_t)stream>>>(values, values_t, leaf_sq, nleaf, eps,
+                                                                                   dropped);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
+}
+
 // values -> values_t for leaves whose norms are already in the record tails (e.g. leaves that
 // arrived from another GPU): transposes the 16x16 values and the 4x4 sub-norm tail, nothing else.
 __global__ void __launch_bounds__(256) transpose_records_kernel(const float *__restrict__ values,

@@ -39,6 +39,19 @@ def tree_depth(m: int, n: int, n_b: int = DEFAULT_BLOCK) -> int:
     return (q - 1).bit_length()
 
 
+def drop_tolerance(tau: float, norm_a: float, norm_b: float) -> float:
+    """Element-wise drop threshold that goes with a product tolerance tau: tau over the larger
+    operand norm (`core.py:42-51`); the eps to hand to ``QuadtreeMatrix.sparsify``."""
+    if not tau >= 0:
+        raise ValueError(f"tau must be nonnegative, got {tau}")
+    if norm_a < 0 or norm_b < 0:
+        raise ValueError("operand norms must be nonnegative")
+    largest = max(norm_a, norm_b)
+    if largest == 0:
+        raise ValueError("both operand norms are zero, drop tolerance undefined")
+    return tau / largest
+
+
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -390,6 +403,38 @@ class QuadtreeMatrix:
         self._pending.clear()
         self._set_empty()
         self._rev += 1
+
+    def sparsify(self, eps: float) -> int:
+        """Zero every 4x4 sub-block with 0 < sub-norm < eps, drop the leaves left empty and rebuild
+        the interior norms (`core.py:347-383`).  Returns the number of sub-blocks dropped;
+        ``eps = 0`` is an exact no-op.  The comparison is done in float32, as numpy does for a
+        float32 array against a Python float."""
+        self._require_16()
+        if not eps >= 0:
+            raise ValueError(f"eps must be nonnegative, got {eps}")
+        self._flush_guard()
+        if eps == 0 or self.nleaf == 0:
+            return 0
+        n = self.nleaf
+        if not getattr(self, "_keys_sorted", True):
+            raise ValueError("sparsify needs a tree with its leaves in key order")
+        if self._values_t is None:
+            self.view()                                         # builds the transposed copies
+        values, values_t = self.values[:n].contiguous(), self.values_t[:n].contiguous()
+        leaf_sq = self._packed_leaf_sq()[:n].clone()
+        dropped = torch.zeros((1,), dtype=torch.int64, device=self.device)
+        _lib.check(_lib.lib().spamm_sparsify_leaves(values.data_ptr(), values_t.data_ptr(), leaf_sq.data_ptr(), n,
+                                                    float(np.float32(eps)), dropped.data_ptr(), _stream()), "sparsify")
+        keep = torch.nonzero(leaf_sq > 0).flatten()
+        if keep.numel() == 0:
+            self._set_empty()
+            self._rev += 1
+        elif keep.numel() == n:
+            self._adopt_packed(self.keys[:n].contiguous(), values, values_t, leaf_sq, n)
+        else:
+            self._adopt_packed(self.keys[:n][keep].contiguous(), values[keep].contiguous(), values_t[keep].contiguous(),
+                               leaf_sq[keep].contiguous(), int(keep.numel()))
+        return int(dropped.item())
 
     def compute_norms(self) -> None:
         """Rebuild all norms bottom-up from leaf values (`core.py:331-345`)."""
