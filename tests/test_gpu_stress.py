@@ -1,0 +1,33 @@
+"""The numeric kernel's scheduling knobs must never change a bit of the result: chained segments of
+any length (accumulators handed between CTAs), ring depth, CTAs per SM, programmatic dependent
+launch on or off.  Each setting runs in its own process (the knobs are read once per process) and
+repeats the product, so a hand-over race would show up as a mismatch with the oracle."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SETTINGS = [
+    {},                                                                  # defaults
+    {"SPAMM_EX_CTAS": "1", "SPAMM_UNIT_MIN_SEG": "1"},                   # 148 CTAs: tiles cut into 1-record segments
+    {"SPAMM_EX_CTAS": "1", "SPAMM_UNIT_MIN_SEG": "1", "SPAMM_UNIT_TARGET": "8000"},
+    {"SPAMM_EX_CTAS": "1", "SPAMM_EX_STAGES": "2", "SPAMM_UNIT_MIN_SEG": "3"},
+    {"SPAMM_UNIT_TARGET": "0"},                                          # whole tiles only
+    {"SPAMM_PDL": "0", "SPAMM_EX_CTAS": "1", "SPAMM_UNIT_MIN_SEG": "2"},
+]
+
+
+@pytest.mark.parametrize("env", SETTINGS, ids=lambda e: ",".join(f"{k[6:]}={v}" for k, v in e.items()) or "defaults")
+def test_scheduling_knobs_do_not_change_results(env):
+    full = dict(os.environ)
+    full.update(env)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "stress_child.py"), "2048", "1e-8", "6"],
+                         env=full, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("OK"), out.stdout[-2000:] + out.stderr[-2000:]
+    if env.get("SPAMM_EX_CTAS") == "1" and env.get("SPAMM_UNIT_TARGET") != "0":
+        assert "seg_len=0" not in out.stdout, "this setting is meant to exercise chained segments: " + out.stdout
