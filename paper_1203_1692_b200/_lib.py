@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "csrc", "libspamm_b200.so")
+# SPAMM_B200_LIB: another build of the same library (A/B comparisons of kernel variants)
+LIB_PATH = os.environ.get("SPAMM_B200_LIB") or os.path.join(_HERE, "csrc", "libspamm_b200.so")
 
 SPAMM_OK, SPAMM_EINVAL, SPAMM_ECUDA, SPAMM_EWORKSPACE = 0, 1, 2, 3
 FINE4, COARSE16 = 0, 1
