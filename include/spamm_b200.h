@@ -246,7 +246,10 @@ typedef struct {
  * are plan->c_keys[0 .. counts[0]) with their records in c->values / c->values_t; the number of
  * executed micro products (ExecCounters.products4) accumulates in counts[8..9].  The caller
  * reads plan->counts when it next synchronises; counts[2] != 0 means a capacity was too small
- * (nothing was computed) and the call must be repeated with larger buffers. */
+ * (nothing was computed) and the call must be repeated with larger buffers.
+ * plan_ws (spamm_plan_workspace_bytes() bytes) must be ALL ZERO when the call is enqueued and is
+ * all zero again once the multiply has run: clear it once after allocating it, then reuse it for
+ * every multiply on the same stream -- the four kernels of a multiply run without any memset. */
 int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
                    int exact, float alpha, int32_t row0, int32_t row1,
                    const spamm_plan_buffers *plan, void *plan_ws, size_t plan_ws_bytes,
@@ -255,9 +258,11 @@ int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b, double ta
 /* The same on ONE caller-provided device allocation: spamm_multiply_arena_layout() gives the byte
  * offset of every buffer of the plan and of the product (fields named as in spamm_plan_buffers /
  * spamm_product_buffers) and the total size; spamm_multiply_arena() carves `arena` that way and
- * runs spamm_multiply.  One allocation and one call per product on the host side. */
+ * runs spamm_multiply.  One allocation and one call per product on the host side; the planner's
+ * workspace (plan_ws_bytes of the layout, zero-initialised, see spamm_multiply) is shared by all
+ * products of a stream and therefore not part of the arena. */
 typedef struct {
-    int64_t counts, steps, c_keys, tile_off, tile_order, chain, plan_ws, plan_ws_bytes;
+    int64_t counts, steps, c_keys, tile_off, tile_order, chain, plan_ws_bytes;   /* plan_ws_bytes: size of the separate workspace */
     int64_t values, values_t, leaf_sq, slot, slot_t, norm, norm_t, leaf_sq_grid, sq_levels;
     int64_t total;
 } spamm_arena_layout;
@@ -266,7 +271,7 @@ int spamm_multiply_arena_layout(int depth, int c_depth, int64_t step_capacity, i
 int spamm_multiply_arena(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
                          int exact, float alpha, int32_t row0, int32_t row1, int c_depth,
                          int64_t step_capacity, int64_t leaf_capacity, void *arena, size_t arena_bytes,
-                         void *stream);
+                         void *plan_ws, size_t plan_ws_bytes, void *stream);
 
 /* _compose with beta != 0 (numeric.py:276-284): out leaf x = (alpha32 * prod[ip]) + (old[io] * beta32)
  * with ip / io = -1 when that side has no leaf; the alpha == 1 / beta == 1 special cases keep

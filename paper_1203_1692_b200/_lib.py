@@ -46,8 +46,7 @@ class ProductBuffers(C.Structure):
 class ArenaLayout(C.Structure):
     """``spamm_arena_layout`` (byte offsets into the single allocation of spamm_multiply_arena)."""
 
-    _fields_ = [(n, i64) for n in ("counts", "steps", "c_keys", "tile_off", "tile_order", "chain", "plan_ws",
-                                   "plan_ws_bytes",
+    _fields_ = [(n, i64) for n in ("counts", "steps", "c_keys", "tile_off", "tile_order", "chain", "plan_ws_bytes",
                                    "values", "values_t", "leaf_sq", "slot", "slot_t", "norm", "norm_t", "leaf_sq_grid",
                                    "sq_levels", "total")]
 
@@ -84,7 +83,7 @@ SIGNATURES = {
                                  C.POINTER(PlanBuffers), vp, sz, C.POINTER(ProductBuffers), vp]),
     "spamm_multiply_arena_layout": (C.c_int, [C.c_int, C.c_int, i64, i64, C.POINTER(ArenaLayout)]),
     "spamm_multiply_arena": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, C.c_int, C.c_int, f32, i32, i32,
-                                       C.c_int, i64, i64, vp, sz, vp]),
+                                       C.c_int, i64, i64, vp, sz, vp, sz, vp]),
     "spamm_union_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp, sz, vp]),
     "spamm_compose": (C.c_int, [vp, vp, vp, vp, i64, f32, f32, C.c_int, C.c_int, vp, vp]),
 }

@@ -7,11 +7,9 @@
 
 #include "common.cuh"
 
-int spamm_clear_leaf_grids(int depth, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid,
-                           void *zero0, size_t zero0_bytes, void *zero1, size_t zero1_bytes, cudaStream_t st);
-size_t spamm_plan_zero_bytes(int64_t step_capacity, int64_t leaf_capacity);
 int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
-                    const spamm_plan_buffers *out, void *ws, size_t ws_bytes, bool prezeroed, void *stream);
+                    const spamm_plan_buffers *out, void *ws, size_t ws_bytes, bool prezeroed,
+                    const spamm_product_buffers *cgrid, void *stream);
 int spamm_launch_interior(const double *leaf_sq, int depth, float *norm, float *norm_t, double *sq_levels,
                           unsigned int *ticket, cudaStream_t st);
 int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const spamm_plan_buffers *plan,
@@ -25,16 +23,11 @@ extern "C" int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b
 {
     if (!a || !b || !plan || !c) return SPAMM_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    // C's leaf grids start empty (the numeric kernel's epilogue fills in the product leaves); the same
-    // kernel clears the planner's look-back state and the plan counts
-    const size_t zero_ws = spamm_plan_zero_bytes(plan->step_capacity, plan->leaf_capacity);
-    if (!plan_ws || plan_ws_bytes < zero_ws) return SPAMM_EWORKSPACE;
-    int rc = spamm_clear_leaf_grids(c->depth, c->slot, c->slot_t, c->norm, c->norm_t, c->leaf_sq_grid, plan_ws, zero_ws,
-                                    plan->counts, SPAMM_PLAN_COUNTS * sizeof(int32_t), st);
-    if (rc != SPAMM_OK) return rc;
+    // Four kernels, no memset: plan tiles, plan order (which also empties C's leaf grids, publishes
+    // the counts and returns the workspace to its all-zero state), execute, interior norms.
+    if (!plan_ws) return SPAMM_EWORKSPACE;
     static const int stop = getenv("SPAMM_PIPE_STOP") ? atoi(getenv("SPAMM_PIPE_STOP")) : 0;   // tuning aid: truncate
-    if (stop == 1) return SPAMM_OK;
-    rc = spamm_plan_impl(a, b, tau, row0, row1, plan, plan_ws, plan_ws_bytes, true, stream);
+    int rc = spamm_plan_impl(a, b, tau, row0, row1, plan, plan_ws, plan_ws_bytes, true, c, stream);
     if (rc != SPAMM_OK || stop == 2) return rc;
     // executed micro products are counted in plan->counts[8..9]
     rc = spamm_execute_impl(a, b, plan, -1, -1, tau, alpha, granularity, exact, c->values, c->values_t, c->leaf_sq,
@@ -67,8 +60,7 @@ extern "C" int spamm_multiply_arena_layout(int depth, int c_depth, int64_t step_
     out->tile_off = arena_take(o, (leaf_capacity + 1) * 4);
     out->tile_order = arena_take(o, (2 * leaf_capacity + SPAMM_UNIT_EXTRA) * 4);   // units, then the chain flags
     out->chain = out->tile_order + (leaf_capacity + SPAMM_UNIT_EXTRA) * 4;
-    out->plan_ws_bytes = (int64_t)spamm_plan_workspace_bytes(depth, step_capacity, leaf_capacity);
-    out->plan_ws = arena_take(o, out->plan_ws_bytes);
+    out->plan_ws_bytes = (int64_t)spamm_plan_workspace_bytes(depth, step_capacity, leaf_capacity);   // not in the arena
     out->values = arena_take(o, leaf_capacity * SPAMM_REC_BYTES);
     out->values_t = arena_take(o, leaf_capacity * SPAMM_REC_BYTES);
     out->leaf_sq = arena_take(o, leaf_capacity * 8);
@@ -84,13 +76,14 @@ extern "C" int spamm_multiply_arena_layout(int depth, int c_depth, int64_t step_
 
 extern "C" int spamm_multiply_arena(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
                                     int exact, float alpha, int32_t row0, int32_t row1, int c_depth, int64_t step_capacity,
-                                    int64_t leaf_capacity, void *arena, size_t arena_bytes, void *stream)
+                                    int64_t leaf_capacity, void *arena, size_t arena_bytes, void *plan_ws,
+                                    size_t plan_ws_bytes, void *stream)
 {
-    if (!a || !b || !arena) return SPAMM_EINVAL;
+    if (!a || !b || !arena || !plan_ws) return SPAMM_EINVAL;
     spamm_arena_layout l;
     int rc = spamm_multiply_arena_layout(a->depth, c_depth, step_capacity, leaf_capacity, &l);
     if (rc != SPAMM_OK) return rc;
-    if ((int64_t)arena_bytes < l.total) return SPAMM_EWORKSPACE;
+    if ((int64_t)arena_bytes < l.total || (int64_t)plan_ws_bytes < l.plan_ws_bytes) return SPAMM_EWORKSPACE;
     char *p = reinterpret_cast<char *>(arena);
     spamm_plan_buffers plan;
     plan.steps = reinterpret_cast<spamm_step *>(p + l.steps);
@@ -112,6 +105,5 @@ extern "C" int spamm_multiply_arena(const spamm_tree_view *a, const spamm_tree_v
     c.leaf_sq_grid = reinterpret_cast<double *>(p + l.leaf_sq_grid);
     c.sq_levels = reinterpret_cast<double *>(p + l.sq_levels);
     c.depth = c_depth;
-    return spamm_multiply(a, b, tau, granularity, exact, alpha, row0, row1, &plan, p + l.plan_ws, (size_t)l.plan_ws_bytes,
-                          &c, stream);
+    return spamm_multiply(a, b, tau, granularity, exact, alpha, row0, row1, &plan, plan_ws, plan_ws_bytes, &c, stream);
 }

@@ -19,6 +19,7 @@
 //   (K, 4 x 16 live bits = the tasks (4I+di, 4K+kk, 4J+dj) that survive, where the two leaf blocks sit)
 // so the compacted task list comes out already in the order and grouping the numeric phase
 // consumes: ascending k per product leaf (numeric.py:203-217), leaves in Morton order.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -36,7 +37,12 @@ struct LevelBuf {
 
 #define PLAN_BINS 1024       // super-tiles are binned by their number of step records
 
-struct PlanShared {      // lives at the start of the workspace, zeroed once per plan
+// Lives at the start of the workspace.  The workspace prefix (this struct and the look-back states
+// behind it) must be zero when a plan starts; the last kernel of a plan leaves it zero again, so
+// one workspace serves a sequence of plans on a stream without memsets.
+struct PlanShared {
+    int32_t res[SPAMM_PLAN_COUNTS];           // the plan counts while they are being accumulated
+    unsigned int order_ticket;
     unsigned int tile_counter[PLAN_MAX_LEVELS + 1];
     int32_t counts[PLAN_MAX_LEVELS + 1][2];   // (nodes, candidates) per level
     unsigned int bins[PLAN_BINS];             // histogram of super-tile sizes
@@ -261,7 +267,15 @@ __global__ void __launch_bounds__(PLAN_THREADS) plan_expand_kernel(ExpandArgs a)
 }
 
 // ---- last stage: super-tile nodes -> step records --------------------------------------------
+__device__ __forceinline__ unsigned long long plan_timer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 struct TileArgs {
+    unsigned long long *trace;   // tuning aid (SPAMM_PLAN_TRACE): per block 6 timestamps
     const float *norm_a;      // leaf level grid of A, row-major (i,k)
     const float *norm_bt;     // leaf level grid of B transposed (j,k)
     const int32_t *slot_a;    // leaf slots of A (i,k)
@@ -293,26 +307,36 @@ struct LaneTests {
     uint32_t b_here;     // bit dj: leaf B(k, sub*J+dj) stored
 };
 
-__device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, uint32_t I, uint32_t J, uint32_t k, uint32_t rowok)
+struct LaneNorms { float na[4], nb[4]; };      // leaf norms of A(sub*I+d, k) and B(k, sub*J+d); -1 = absent
+
+__device__ __forceinline__ LaneNorms tile_norms(const TileArgs &a, uint32_t I, uint32_t J, uint32_t k, bool valid)
 {
-    float na[4], nb[4];
+    LaneNorms n;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+        n.na[d] = -1.0f;
+        n.nb[d] = -1.0f;
+        if (valid && d < a.sub) {
+            n.na[d] = __ldg(a.norm_a + (int64_t)(a.sub * I + d) * a.L + k);
+            n.nb[d] = __ldg(a.norm_bt + (int64_t)(a.sub * J + d) * a.L + k);
+        }
+    }
+    return n;
+}
+
+__device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, const LaneNorms &n, uint32_t rowok)
+{
     LaneTests t{0u, 0u, 0u};
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
-        na[d] = -1.0f;
-        nb[d] = -1.0f;
-        if (d < a.sub) {
-            na[d] = __ldg(a.norm_a + (int64_t)(a.sub * I + d) * a.L + k);
-            nb[d] = __ldg(a.norm_bt + (int64_t)(a.sub * J + d) * a.L + k);
-        }
-        t.a_here |= (na[d] >= 0.0f) ? (1u << d) : 0u;
-        t.b_here |= (nb[d] >= 0.0f) ? (1u << d) : 0u;
+        t.a_here |= (n.na[d] >= 0.0f) ? (1u << d) : 0u;
+        t.b_here |= (n.nb[d] >= 0.0f) ? (1u << d) : 0u;
     }
 #pragma unroll
     for (int di = 0; di < 4; ++di)
 #pragma unroll
         for (int dj = 0; dj < 4; ++dj)
-            if ((rowok >> di & 1u) && norm_test(na[di], nb[dj], a.tau)) t.live |= 1u << step_pos(di, dj);
+            if ((rowok >> di & 1u) && norm_test(n.na[di], n.nb[dj], a.tau)) t.live |= 1u << step_pos(di, dj);
     return t;
 }
 
@@ -336,12 +360,16 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
     const uint32_t kk = lane % sub;              // my k inside the block
     const uint32_t grp = (lane / sub) * sub;     // first lane of my group
     unsigned long long tasks_total = 0;
-    for (;;) {
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6] = plan_timer();
+    // dense start with no more tiles than blocks: block b takes tile b, no hand-out counter
+    const bool fixed_tiles = DENSE && ntiles <= (int)gridDim.x;
+    for (int round = 0;; ++round) {
         __syncthreads();
-        if (threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_counter, 1u);
+        if (!fixed_tiles && threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_counter, 1u);
         __syncthreads();
-        const int tile = s_tile;
+        const int tile = fixed_tiles ? (round == 0 ? (int)blockIdx.x : ntiles) : s_tile;
         if (tile >= ntiles) break;
+        if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 1] = plan_timer();
         const int pidx = tile * TILE_WARPS + warp;
         const bool valid = pidx < n_nodes;
         uint32_t pm = 0, I = 0, J = 0, rowok = 0;
@@ -372,12 +400,18 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
                 e = a.in.off[pidx + 1];
             }
         }
+        if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 2] = plan_timer();
         // phase 1: count step records and product leaves of this super-tile
         uint32_t nsteps = 0, present = 0, ntasks = 0;
+        // the norms of the next pass are fetched before the tests of the current one
+        LaneNorms nrm = tile_norms(a, I, J, (s + (int)lane / sub < e) ? sub * ks[s + (int)lane / sub] + kk : 0u,
+                                   s + (int)lane / sub < e);
         for (int b = s; b < e; b += per) {
-            const int t = b + (int)lane / sub;
+            const int t = b + (int)lane / sub, t2 = t + per;
+            const LaneNorms nxt = tile_norms(a, I, J, t2 < e ? sub * ks[t2] + kk : 0u, t2 < e);
             uint32_t live = 0;
-            if (t < e) live = tile_tests(a, I, J, sub * ks[t] + kk, rowok).live;
+            if (t < e) live = tile_tests(a, nrm, rowok).live;
+            nrm = nxt;
             const uint32_t bal = __ballot_sync(FULL_MASK, live != 0);
             // one record per group of `sub` lanes with any live task
             uint32_t groups = bal;
@@ -396,6 +430,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
             if (valid) atomicAdd(&a.bins[nsteps < PLAN_BINS ? nsteps : PLAN_BINS - 1], 1u);
         }
         __syncthreads();
+        if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 3] = plan_timer();
         // phase 2: block scan + look-back over (records, product leaves)
         if (warp == 0) {
             uint32_t vs = lane < TILE_WARPS ? s_wsteps[lane] : 0u, vl = lane < TILE_WARPS ? s_wleaves[lane] : 0u;
@@ -408,7 +443,8 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
             const uint32_t rs = __shfl_sync(FULL_MASK, is, TILE_WARPS - 1), rl = __shfl_sync(FULL_MASK, il, TILE_WARPS - 1);
             if (lane < TILE_WARPS) { s_wsteps[lane] = is - vs; s_wleaves[lane] = il - vl; }
             uint32_t ex_lo, ex_hi;
-            lb_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
+            if (DENSE && ntiles <= 128 && ntiles <= (int)gridDim.x) all_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
+            else lb_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
             if (lane == 0) {
                 s_base_lo = ex_lo;
                 s_base_hi = ex_hi;
@@ -423,6 +459,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
             }
         }
         __syncthreads();
+        if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 4] = plan_timer();
         if (valid && lane == 0) a.tile_off[pidx] = (int32_t)(s_base_lo + s_wsteps[warp]);
         if (!valid || nsteps == 0) continue;
         // phase 3: product leaf keys and step records, in ascending K
@@ -437,15 +474,17 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
         const int64_t s_first = sb, s_last = sb + nsteps - 1;
         const uint32_t lt = lanemask_lt();
         const uint32_t lead_mask = (sub == 4 ? 0x11111111u : sub == 2 ? 0x55555555u : 0xFFFFFFFFu);
+        nrm = tile_norms(a, I, J, (s + (int)lane / sub < e) ? sub * ks[s + (int)lane / sub] + kk : 0u, s + (int)lane / sub < e);
         for (int b = s; b < e; b += per) {
-            const int t = b + (int)lane / sub;
+            const int t = b + (int)lane / sub, t2 = t + per;
+            const LaneNorms nxt = tile_norms(a, I, J, t2 < e ? sub * ks[t2] + kk : 0u, t2 < e);
             LaneTests lt4{0u, 0u, 0u};
-            uint32_t K = 0, k = 0;
+            uint32_t K = 0;
             if (t < e) {
                 K = ks[t];
-                k = sub * K + kk;
-                lt4 = tile_tests(a, I, J, k, rowok);
+                lt4 = tile_tests(a, nrm, rowok);
             }
+            nrm = nxt;
             // gather the group's four lanes: live per kk, stored leaves of both blocks
             uint32_t live4[4] = {0, 0, 0, 0}, a_present = 0, b_present = 0, any = 0;
             // first stored leaf of each block in Morton order and the lane that knows its slot
@@ -488,20 +527,55 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
         }
     }
     if (lane == 0 && tasks_total) atomicAdd(reinterpret_cast<unsigned long long *>(a.counts + 6), tasks_total);
+    __syncthreads();
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 5] = plan_timer();
 }
 
 // Longest-first order of the super-tiles for the numeric kernel's dynamic scheduler: a counting
 // sort by step count (any order inside a bin; the product does not depend on it).
-__global__ void __launch_bounds__(256) plan_order_kernel(const int32_t *__restrict__ tile_off, int32_t *counts,
-                                                         const unsigned int *__restrict__ bins, unsigned int *cursor,
-                                                         int32_t *__restrict__ tile_order, int unit_target, int min_seg,
-                                                         int grid_ctas, int32_t *__restrict__ chain,
-                                                         int64_t leaf_capacity)
+struct OrderArgs {
+    const int32_t *tile_off;
+    int32_t *counts;              // the caller's plan counts: written here, all SPAMM_PLAN_COUNTS of them
+    PlanShared *shared;
+    uint32_t *ws_tail;            // workspace prefix behind PlanShared (look-back states), left zero
+    int64_t ws_tail_words;
+    int32_t *tile_order;
+    int unit_target, min_seg, grid_ctas;
+    int32_t *chain;
+    int64_t leaf_capacity;
+    // optional: C's leaf grids, emptied here for the numeric kernel's epilogue to fill
+    int64_t cells;
+    int32_t *slot, *slot_t;
+    float *norm, *norm_t;
+    double *leaf_sq_grid;
+};
+
+__global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
 {
+    const int32_t *__restrict__ tile_off = a.tile_off;
+    int32_t *counts = a.shared->res;
+    const unsigned int *__restrict__ bins = a.shared->bins;
+    unsigned int *cursor = a.shared->cursor;
+    int32_t *__restrict__ tile_order = a.tile_order;
+    const int unit_target = a.unit_target, min_seg = a.min_seg, grid_ctas = a.grid_ctas;
+    int32_t *__restrict__ chain = a.chain;
+    const int64_t leaf_capacity = a.leaf_capacity;
+    __shared__ bool s_last;
     pdl_enter();
-    // the numeric kernel's per-leaf hand-over flags start clear
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < leaf_capacity; x += (int64_t)gridDim.x * blockDim.x)
-        chain[x] = 0;
+    // the numeric kernel's per-leaf hand-over flags start clear; the planner's look-back states are
+    // done with and go back to zero; C's leaf grids start empty
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gsz = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = gtid; x < leaf_capacity; x += gsz) chain[x] = 0;
+    for (int64_t x = gtid; x < a.ws_tail_words; x += gsz) a.ws_tail[x] = 0u;
+    if (a.slot) {
+        for (int64_t x = gtid; x < a.cells; x += gsz) {
+            a.slot[x] = -1;
+            a.slot_t[x] = -1;
+            a.norm[x] = -1.0f;
+            a.norm_t[x] = -1.0f;
+            a.leaf_sq_grid[x] = 0.0;
+        }
+    }
     __shared__ unsigned int s_start[PLAN_BINS];
     __shared__ unsigned int s_base[256];
     __shared__ unsigned int s_part[256];
@@ -561,10 +635,8 @@ __global__ void __launch_bounds__(256) plan_order_kernel(const int32_t *__restri
     unsigned int base = inc2 - cnt;
     for (int w = 0; w < (t >> 5); ++w) base += s_part[w];
     s_base[t] = base;
-    if (blockIdx.x == 0 && t == 255) {
-        counts[5] = (int)(base + cnt);      // work units the numeric kernel hands out
-        counts[12] = seg_len;
-    }
+    __shared__ int s_units;
+    if (t == 255) s_units = (int)(base + cnt);      // work units the numeric kernel hands out
     __syncthreads();
     for (int idx = blockIdx.x * blockDim.x + t; idx < n_nodes; idx += gridDim.x * blockDim.x) {
         const int ns = tile_off[idx + 1] - tile_off[idx];
@@ -581,6 +653,23 @@ __global__ void __launch_bounds__(256) plan_order_kernel(const int32_t *__restri
         tile_order[rank >= whole ? rank - whole : n_tiles - whole + rank] = (int32_t)unit_pack(idx, 0, nseg);
         for (int sgm = 1; sgm < nseg; ++sgm) tile_order[s_base[sgm] + rank - whole] = (int32_t)unit_pack(idx, sgm, nseg);
     }
+    // the last block publishes the counts and leaves the shared planner state zero for the next plan
+    __threadfence();
+    __syncthreads();
+    if (t == 0) s_last = atomicAdd(&a.shared->order_ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (t < SPAMM_PLAN_COUNTS) {
+        int32_t v = 0;
+        if (t == 0 || t == 2 || t == 3 || t == 4 || t == 6 || t == 7 || t == 11) v = counts[t];
+        if (t == 5) v = s_units;
+        if (t == 12) v = seg_len;
+        a.counts[t] = v;
+    }
+    __syncthreads();
+    uint32_t *sh = reinterpret_cast<uint32_t *>(a.shared);
+    for (int x = t; x < (int)(sizeof(PlanShared) / 4); x += blockDim.x) sh[x] = 0u;
 }
 
 // ---- host side ---------------------------------------------------------------------------------
@@ -672,7 +761,8 @@ size_t spamm_plan_zero_bytes(int64_t step_capacity, int64_t leaf_capacity)
 
 // prezeroed: the caller has already cleared that region and out->counts on the stream
 int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
-                    const spamm_plan_buffers *out, void *ws, size_t ws_bytes, bool prezeroed, void *stream)
+                    const spamm_plan_buffers *out, void *ws, size_t ws_bytes, bool prezeroed,
+                    const spamm_product_buffers *cgrid, void *stream)
 {
     if (!a || !b || !out || !ws) return SPAMM_EINVAL;
     if (!(tau >= 0.0)) return SPAMM_EINVAL;                       // NaN or negative (symbolic.py:99-100)
@@ -681,15 +771,13 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     cudaStream_t st = (cudaStream_t)stream;
     PlanWorkspace w = carve(ws, out->step_capacity, out->leaf_capacity);
     if (ws_bytes < w.total) return SPAMM_EWORKSPACE;
-    if (!prezeroed) {
-        if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return SPAMM_ECUDA;
-        if (cudaMemsetAsync(out->counts, 0, SPAMM_PLAN_COUNTS * sizeof(int32_t), st) != cudaSuccess) return SPAMM_ECUDA;
-    }
+    if (!prezeroed && cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return SPAMM_ECUDA;
 
     const int depth = a->depth;
     const int tl = depth >= 2 ? depth - 2 : 0;          // super-tile level
     const int l0 = tl < ROOT_MAX_LEVEL ? tl : ROOT_MAX_LEVEL;   // start level
-    int32_t *overflow = out->counts + 2, *max_list = out->counts + 3;
+    int32_t *res = w.shared->res;       // accumulated here, copied to out->counts by the last kernel
+    int32_t *overflow = res + 2, *max_list = res + 3;
     int cur = 0;
     const bool dense = tl <= 6 && out->leaf_capacity >= (int64_t(1) << (2 * tl));
     const int grid = SPAMM_NUM_SMS * 4;
@@ -720,6 +808,10 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     }
     }
     TileArgs t;
+    t.trace = nullptr;
+    static const char *trace_path = getenv("SPAMM_PLAN_TRACE");      // tuning aid: allocates and synchronises
+    const int tgrid = dense ? SPAMM_NUM_SMS : SPAMM_NUM_SMS * 2;
+    if (trace_path && cudaMalloc(&t.trace, 8 * 6 * tgrid) == cudaSuccess) cudaMemsetAsync(t.trace, 0, 8 * 6 * tgrid, st);
     t.norm_a_t = a->norm + spamm_level_offset(tl);
     t.norm_bt_t = b->norm_t + spamm_level_offset(tl);
     t.St = 1 << tl;
@@ -737,7 +829,7 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     t.tile_off = out->tile_off;
     t.bins = w.shared->bins;
     t.cap_steps = out->step_capacity; t.cap_leaves = out->leaf_capacity;
-    t.counts = out->counts;
+    t.counts = res;
     t.tile_counter = &w.shared->tile_counter[PLAN_MAX_LEVELS];
     t.tile_state = w.tile_state[PLAN_MAX_LEVELS];
     if (spamm_launch_pdl(dense ? plan_tiles_kernel<true> : plan_tiles_kernel<false>,
@@ -746,10 +838,42 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     SPAMM_CHECK_LAUNCH();
     static const int unit_target = plan_env("SPAMM_UNIT_TARGET", 6 * 2 * SPAMM_NUM_SMS, 0, SPAMM_UNIT_EXTRA);
     static const int min_seg = plan_env("SPAMM_UNIT_MIN_SEG", 2, 1, 1024);
-    if (spamm_launch_pdl(plan_order_kernel, dim3(SPAMM_NUM_SMS), dim3(256), 0, st, out->tile_off, out->counts,
-                         w.shared->bins, w.shared->cursor, out->tile_order, unit_target, min_seg, spamm_execute_grid(),
-                         out->chain, out->leaf_capacity) != cudaSuccess)
-        return SPAMM_ECUDA;
+    if (t.trace) {
+        unsigned long long *h = (unsigned long long *)malloc(8 * 6 * tgrid);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, t.trace, 8 * 6 * tgrid, cudaMemcpyDeviceToHost);
+        if (FILE *f = fopen(trace_path, "w")) {
+            for (int x = 0; x < tgrid; ++x)
+                fprintf(f, "%d %llu %llu %llu %llu %llu %llu\n", x, h[6 * x], h[6 * x + 1], h[6 * x + 2], h[6 * x + 3],
+                        h[6 * x + 4], h[6 * x + 5]);
+            fclose(f);
+        }
+        free(h);
+        cudaFree(t.trace);
+    }
+    OrderArgs oa;
+    oa.tile_off = out->tile_off;
+    oa.counts = out->counts;
+    oa.shared = w.shared;
+    {
+        const size_t head = align_up(sizeof(PlanShared), 256);
+        oa.ws_tail = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(ws) + head);
+        oa.ws_tail_words = (int64_t)((w.zero_bytes - head) / 4);
+    }
+    oa.tile_order = out->tile_order;
+    oa.unit_target = unit_target; oa.min_seg = min_seg; oa.grid_ctas = spamm_execute_grid();
+    oa.chain = out->chain;
+    oa.leaf_capacity = out->leaf_capacity;
+    oa.cells = 0;
+    oa.slot = oa.slot_t = nullptr; oa.norm = oa.norm_t = nullptr; oa.leaf_sq_grid = nullptr;
+    if (cgrid) {
+        const int64_t off = spamm_level_offset(cgrid->depth);
+        oa.cells = int64_t(1) << (2 * cgrid->depth);
+        oa.slot = cgrid->slot; oa.slot_t = cgrid->slot_t;
+        oa.norm = cgrid->norm + off; oa.norm_t = cgrid->norm_t + off;
+        oa.leaf_sq_grid = cgrid->leaf_sq_grid;
+    }
+    if (spamm_launch_pdl(plan_order_kernel, dim3(SPAMM_NUM_SMS), dim3(256), 0, st, oa) != cudaSuccess) return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
 }
@@ -757,5 +881,5 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
 extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
                           const spamm_plan_buffers *out, void *ws, size_t ws_bytes, void *stream)
 {
-    return spamm_plan_impl(a, b, tau, row0, row1, out, ws, ws_bytes, false, stream);
+    return spamm_plan_impl(a, b, tau, row0, row1, out, ws, ws_bytes, false, nullptr, stream);
 }

@@ -224,6 +224,20 @@ def multiply(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig | None = 
     return out, plan, counters
 
 
+_planner_ws: dict = {}
+
+
+def _planner_workspace(dev, nbytes: int) -> torch.Tensor:
+    """The planner's workspace, one per (device, stream): the library needs it all zero when a
+    multiply is enqueued and leaves it all zero, so it is cleared only when it is (re)allocated."""
+    key = (dev.index if dev.index is not None else torch.cuda.current_device(), _stream())
+    ws = _planner_ws.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros((max(nbytes, 1 << 20),), dtype=torch.uint8, device=dev)
+        _planner_ws[key] = ws
+    return ws
+
+
 def multiply_async(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig, c: QuadtreeMatrix | None = None,
                    row_range: tuple[int, int] | None = None) -> tuple[QuadtreeMatrix, MultiplyPlan, ExecCounters]:
     """C = alpha A B through ``spamm_multiply``: one C call, no host synchronisation."""
@@ -259,10 +273,15 @@ def multiply_async(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig, c:
             leaf_cap = max(leaf_cap, 1 << (2 * tl))
         lay = _arena_layout(depth, cd, step_cap, leaf_cap)
         arena = torch.empty((lay.total,), dtype=torch.uint8, device=dev)
+        ws = _planner_workspace(dev, lay.plan_ws_bytes)
         va, vb = a.view(depth), b.view(depth, left=False)
-        _lib.check(lib.spamm_multiply_arena(C.byref(va), C.byref(vb), float(cfg.tau), gran, int(cfg.exact), alpha32,
-                                            r0, r1, cd, step_cap, leaf_cap, arena.data_ptr(), lay.total, _stream()),
-                   "multiply")
+        try:
+            _lib.check(lib.spamm_multiply_arena(C.byref(va), C.byref(vb), float(cfg.tau), gran, int(cfg.exact), alpha32,
+                                                r0, r1, cd, step_cap, leaf_cap, arena.data_ptr(), lay.total,
+                                                ws.data_ptr(), ws.numel(), _stream()), "multiply")
+        except Exception:
+            _planner_ws.clear()         # a failed enqueue may leave the workspace dirty: start from a fresh one
+            raise
         return arena, lay, step_cap, leaf_cap
 
     def bind(plan: MultiplyPlan, c: QuadtreeMatrix, arena, lay, step_cap: int, leaf_cap: int) -> None:

@@ -41,7 +41,7 @@ def test_version_and_level_offsets_without_a_gpu():
     offs = [getattr(lay, f) for f, _ in _lib.ArenaLayout._fields_ if f not in ("plan_ws_bytes", "total", "chain")]
     assert offs == sorted(offs) and all(o % 256 == 0 for o in offs) and lay.total > offs[-1]
     # the chain flags follow the work units inside the tile_order region
-    assert lay.chain == lay.tile_order + 4 * (20000 + _lib.UNIT_EXTRA) and lay.chain + 4 * 20000 <= lay.plan_ws
+    assert lay.chain == lay.tile_order + 4 * (20000 + _lib.UNIT_EXTRA) and lay.chain + 4 * 20000 <= lay.values and lay.plan_ws_bytes > 0
 
 
 def test_missing_library_fails_loudly(monkeypatch):
