@@ -23,7 +23,8 @@
 
 #define EX_MAX_STAGES 6
 #define EX_CONSUMERS 8
-#define EX_THREADS (32 * (EX_CONSUMERS + 1))
+#define EX_THREADS (32 * (EX_CONSUMERS + 1))          // coarse16: consumers + producer
+#define EX_THREADS_FINE (32 * (EX_CONSUMERS + 2))     // fine4: + the classifier warp
 #define EX_EXIT (1u << 31)
 #define EX_CHAIN_IN (1u << 30)    // first step of a later segment: accumulators come from C's records
 #define EX_CHAIN_OUT (1u << 29)   // last step of a segment that is not the tile's last: hand them on
@@ -40,6 +41,10 @@ struct __align__(16) StageDesc {
     uint32_t tile;         // Morton index of the super-tile
     uint32_t seg;          // segment of the tile this step belongs to
     uint32_t pad;
+    // fine4, written by the classifier warp: tasks whose 64 micro products all run / none runs,
+    // bit morton4(di,dj) + 16 * (kk & 1) of word kk >> 1
+    uint32_t full[2];
+    uint32_t dead[2];
 };
 
 struct ExecArgs {
@@ -104,7 +109,7 @@ template <bool EXACT, bool FINE>
 #ifndef EX_MIN_BLOCKS
 #define EX_MIN_BLOCKS 2
 #endif
-__global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(ExecArgs g)
+__global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel(ExecArgs g)
 {
     // dynamic shared memory: nstages x (A block + B block), then descriptors and barriers
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -114,6 +119,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
     StageDesc *desc = reinterpret_cast<StageDesc *>(smem_raw + (size_t)nstages * 2 * EX_BLOCK_BYTES);
     uint64_t *full_bar = reinterpret_cast<uint64_t *>(desc + EX_MAX_STAGES);
     uint64_t *empty_bar = full_bar + EX_MAX_STAGES;
+    uint64_t *ready_bar = empty_bar + EX_MAX_STAGES;      // fine4: the stage's tasks are classified
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
@@ -122,6 +128,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
         for (int s = 0; s < nstages; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], EX_CONSUMERS);
+            mbar_init(&ready_bar[s], 1);
         }
         fence_barrier_init();
     }
@@ -213,6 +220,62 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
         return;
     }
 
+    if (FINE && warp == EX_CONSUMERS + 1) {
+        // ============ classifier warp (fine4) ============
+        // Most tasks away from the band edge run all 64 micro products, and some run none.  Both
+        // cases follow from the extreme sub-block norms of the two leaves: min(subA) * min(subB) >= tau
+        // means every product passes the gate, max(subA) * max(subB) < tau means none does (products
+        // of non-negative floats are exact in double and monotone).  Lane l finds the extremes of
+        // staged leaf l (A block: lanes 0..15, B block: 16..31); consumers then skip the per-lane
+        // gate arithmetic for classified tasks.  A NaN sub-norm leaves the task unclassified.
+        for (;;) {
+            mbar_wait(&full_bar[stage], phase);
+            StageDesc &ds = desc[stage];
+            if (ds.flags & EX_EXIT) {
+                if (lane == 0) mbar_arrive(&ready_bar[stage]);
+                break;
+            }
+            const uint32_t a_present = ds.a_present, b_present = ds.b_present;
+            const uint32_t mine_present = lane < 16 ? a_present : b_present;
+            const float *blk = reinterpret_cast<const float *>((lane < 16 ? sA : sB) + (size_t)stage * EX_BLOCK_BYTES);
+            float mn = 0.0f, mx = 0.0f;
+            bool bad = true;
+            if ((lane & 15u) < (uint32_t)__popc(mine_present) && !(g.dbg & 1)) {
+                const float4 *tl = reinterpret_cast<const float4 *>(blk + (lane & 15u) * SPAMM_REC + 256);
+                const float4 t0 = tl[0], t1 = tl[1], t2 = tl[2], t3 = tl[3];
+                mn = fminf(fminf(fminf(t0.x, t0.y), fminf(t0.z, t0.w)), fminf(fminf(t1.x, t1.y), fminf(t1.z, t1.w)));
+                mn = fminf(mn, fminf(fminf(fminf(t2.x, t2.y), fminf(t2.z, t2.w)), fminf(fminf(t3.x, t3.y), fminf(t3.z, t3.w))));
+                mx = fmaxf(fmaxf(fmaxf(t0.x, t0.y), fmaxf(t0.z, t0.w)), fmaxf(fmaxf(t1.x, t1.y), fmaxf(t1.z, t1.w)));
+                mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(t2.x, t2.y), fmaxf(t2.z, t2.w)), fmaxf(fmaxf(t3.x, t3.y), fmaxf(t3.z, t3.w))));
+                const float sum = ((t0.x + t0.y) + (t0.z + t0.w)) + ((t1.x + t1.y) + (t1.z + t1.w)) +
+                                  ((t2.x + t2.y) + (t2.z + t2.w)) + ((t3.x + t3.y) + (t3.z + t3.w));
+                bad = !(sum == sum) || !(sum - sum == 0.0f);      // a NaN or an infinity among the 16 norms
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int kk = 2 * h + (int)(lane >> 4), pos = (int)(lane & 15u);
+                const int gi = step_pos_di(pos), gj = step_pos_dj(pos);
+                const int ia = __popc(a_present & ((1u << step_pos(gi, kk)) - 1u));
+                const int ib = 16 + __popc(b_present & ((1u << step_pos(kk, gj)) - 1u));
+                const float mna = __shfl_sync(FULL_MASK, mn, ia), mnb = __shfl_sync(FULL_MASK, mn, ib);
+                const float mxa = __shfl_sync(FULL_MASK, mx, ia), mxb = __shfl_sync(FULL_MASK, mx, ib);
+                const int bad_a = __shfl_sync(FULL_MASK, (int)bad, ia), bad_b = __shfl_sync(FULL_MASK, (int)bad, ib);
+                const bool unk = (bad_a | bad_b) != 0;       // both shuffles unconditionally: all lanes take part
+                const bool full = !unk && __dmul_rn((double)mna, (double)mnb) >= g.tau;
+                const bool dead = !unk && __dmul_rn((double)mxa, (double)mxb) < g.tau;
+                const uint32_t fb = __ballot_sync(FULL_MASK, full), db = __ballot_sync(FULL_MASK, dead);
+                if (lane == 0) {
+                    ds.full[h] = fb;
+                    ds.dead[h] = db;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ready_bar[stage]);
+            if (++stage == nstages) { stage = 0; phase ^= 1u; }
+        }
+        return;
+    }
+
     // ======================================= consumers =======================================
     // lane = p1 q1 half p0 q0 (bits 4..0).  A 128-bit shared load is served one quarter-warp at a
     // time and quarters only share a wavefront when their banks are disjoint (measured with ncu):
@@ -227,7 +290,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
     float2 acc2[2][4];     // acc2[h][j] = C sub-block elements (2h, j) and (2h+1, j)
     bool traced = false;
     for (;;) {
-        mbar_wait(&full_bar[stage], phase);
+        mbar_wait(FINE ? &ready_bar[stage] : &full_bar[stage], phase);
         const StageDesc &ds = desc[stage];
         const uint32_t flags = ds.flags;
         if (g.trace && threadIdx.x == 0 && !traced) {
@@ -264,6 +327,11 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
         const float *Ablk = reinterpret_cast<const float *>(sA + (size_t)stage * EX_BLOCK_BYTES);
         const float *Bblk = reinterpret_cast<const float *>(sB + (size_t)stage * EX_BLOCK_BYTES);
         const uint4 live4 = *reinterpret_cast<const uint4 *>(ds.live);
+        uint32_t cls_full[2] = {0u, 0u}, cls_dead[2] = {0u, 0u};
+        if (FINE) {
+            cls_full[0] = ds.full[0]; cls_full[1] = ds.full[1];
+            cls_dead[0] = ds.dead[0]; cls_dead[1] = ds.dead[1];
+        }
 #pragma unroll     // all four k unrolled: +4-5 % (their addresses become constants), measured
         for (int kk = 0; kk < 4; ++kk) {
             const uint32_t live = kk == 0 ? live4.x : kk == 1 ? live4.y : kk == 2 ? live4.z : live4.w;
@@ -274,7 +342,10 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
             const float *Bs = Bblk + __popc(b_present & ((1u << step_pos(kk, dj)) - 1u)) * SPAMM_REC;
             uint32_t on = 0;       // bit r: micro product (p,q,r) of my task runs
             if (FINE) {
-                if (mine) {
+                const uint32_t cbit = 1u << (mypos + 16 * (kk & 1));
+                if (mine && (cls_full[kk >> 1] & cbit)) {
+                    on = 15u;
+                } else if (mine && !(cls_dead[kk >> 1] & cbit)) {
                     const float4 sa = *reinterpret_cast<const float4 *>(As + 256 + 4 * p);   // subA[p][0..3]
                     const float4 sb = *reinterpret_cast<const float4 *>(Bs + 256 + 4 * q);   // subB[0..3][q]
                     on |= (__dmul_rn((double)sa.x, (double)sb.x) >= g.tau) ? 1u : 0u;
@@ -497,7 +568,7 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     g.nstages = tune.stages;
     g.dbg = tune.dbg;
     const int grid = SPAMM_NUM_SMS * tune.ctas_per_sm;
-    const size_t smem = (size_t)tune.stages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16);
+    const size_t smem = (size_t)tune.stages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 24);
     const bool fine = granularity == SPAMM_FINE4;
     void (*kern)(ExecArgs) = exact ? (fine ? execute_kernel<true, true> : execute_kernel<true, false>)
                                    : (fine ? execute_kernel<false, true> : execute_kernel<false, false>);
@@ -506,7 +577,8 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     static const char *trace_path = getenv("SPAMM_EX_TRACE");     // tuning aid: allocates and synchronises
     if (trace_path && cudaMalloc(&g.trace, sizeof(unsigned long long) * 4 * grid) != cudaSuccess) g.trace = nullptr;
     if (g.trace) cudaMemsetAsync(g.trace, 0, sizeof(unsigned long long) * 4 * grid, st);
-    if (spamm_launch_pdl(kern, dim3(grid), dim3(EX_THREADS), smem, st, g) != cudaSuccess) return SPAMM_ECUDA;
+    if (spamm_launch_pdl(kern, dim3(grid), dim3(fine ? EX_THREADS_FINE : EX_THREADS), smem, st, g) != cudaSuccess)
+        return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
     if (g.trace) {
         unsigned long long *h = (unsigned long long *)malloc(sizeof(unsigned long long) * 4 * grid);
