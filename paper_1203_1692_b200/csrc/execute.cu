@@ -139,16 +139,17 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
 
     if (warp == EX_CONSUMERS) {
         // ============ producer: stream step records, stage leaf blocks with bulk copies ============
+        // the first unit is read together with the counts (tile_order always has room for one entry per CTA)
+        uint32_t unit_pre = (uint32_t)__ldg(g.tile_order + blockIdx.x);
         const int ntiles = g.counts[2] ? 0 : g.counts[5];      // an overflowed plan is incomplete: do nothing
         const int seg_len = g.counts[12];
         const bool claim_late = ntiles < 16 * (int)gridDim.x;
         const uint32_t *words = reinterpret_cast<const uint32_t *>(g.steps);
         int tile = 0, units_done = 0;
-        if (lane == 0) tile = (int)atomicAdd(g.tile_counter, 1u);
-        tile = __shfl_sync(FULL_MASK, tile, 0);
+        tile = (int)blockIdx.x;        // the first unit needs no hand-out: CTA b takes unit b, the counter the rest
         while (tile < ntiles) {
             ++units_done;
-            const uint32_t unit = (uint32_t)g.tile_order[tile];
+            const uint32_t unit = unit_pre;
             const int node = seg_len ? (int)(unit & ((1u << UNIT_NODE_BITS) - 1u)) : (int)unit;
             const int seg = seg_len ? (int)((unit >> UNIT_NODE_BITS) & 63u) : 0;
             int beg = g.tile_off[node], end = g.tile_off[node + 1];
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
             // on a whole unit it has not started while others run dry.  With many whole tiles it is
             // claimed right away.
             int next_tile = 0;
-            if (lane == 0 && !claim_late) next_tile = (int)atomicAdd(g.tile_counter, 1u);
+            if (lane == 0 && !claim_late) next_tile = (int)(atomicAdd(g.tile_counter, 1u) + gridDim.x);
             // lane l < 16 holds word l of a record (struct spamm_step)
             uint32_t w[EX_PREFETCH];
 #pragma unroll
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
                 w[x] = (lane < 16 && beg + x < end) ? __ldg(words + (size_t)(beg + x) * 16 + lane) : 0u;
             for (int r = beg; r < end; ++r) {
                 if (lane == 0 && claim_late && (r + 2 == end || (r == beg && r + 2 > end)))
-                    next_tile = (int)atomicAdd(g.tile_counter, 1u);
+                    next_tile = (int)(atomicAdd(g.tile_counter, 1u) + gridDim.x);
                 const uint32_t cur = w[0];
 #pragma unroll
                 for (int x = 0; x + 1 < EX_PREFETCH; ++x) w[x] = w[x + 1];
@@ -205,6 +206,7 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
                 if (++stage == nstages) { stage = 0; phase ^= 1u; }
             }
             tile = __shfl_sync(FULL_MASK, next_tile, 0);
+            if (tile < ntiles) unit_pre = (uint32_t)g.tile_order[tile];
         }
         mbar_wait(&empty_bar[stage], phase ^ 1u);
         if (lane == 0) {
