@@ -414,7 +414,8 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
     from paper_1203_1692_b200.symbolic import build_plan
     probe = build_plan(full, full, cfg.tau)
     counts = parallel.row_task_counts(probe, probe.depth).cpu().numpy()
-    r0, r1 = parallel.balanced_row_split(counts[:nrows], world)[rank]
+    splits = parallel.balanced_row_split(counts[:nrows], world)
+    r0, r1 = splits[rank]
     del probe
     mine = parallel.shard_of_tree(full, r0, r1)
     host_rows = full.to_dense_tensor()[r0 * 16:min(m, r1 * 16)].cpu().pin_memory()
@@ -422,13 +423,14 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
     torch.cuda.empty_cache()
 
     def step_resident():
-        return parallel.multiply_sharded(mine, None, (m, n), (m, n), cfg)
+        return parallel.multiply_sharded(mine, None, (m, n), (m, n), cfg, exchange=args.exchange, splits=splits)
 
     host_out = {}
 
     def step_e2e():
         shard = parallel.shard_from_dense_rows(host_rows, r0)
-        c, plan, counters = parallel.multiply_sharded(shard, None, (m, n), (m, n), cfg)
+        c, plan, counters = parallel.multiply_sharded(shard, None, (m, n), (m, n), cfg, exchange=args.exchange,
+                                                      splits=splits)
         nc = c.nleaf                         # this rank's product leaves, read back as packed leaves
         if host_out.get("vals") is None or host_out["vals"].shape[0] < nc:
             host_out["vals"] = torch.empty((nc, 272), dtype=torch.float32).pin_memory()
@@ -467,6 +469,11 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
     tot_tasks = sum(float(w[1]) for w in per_rank)
     flops = 128.0 * tot_p4 if cfg.granularity == "fine4" else 8192.0 * tot_tasks
     e2e_ms, _ = timed(step_e2e, max(2, min(args.steps, 5)), 2)
+    # for reference: the same step with B already replicated (no exchange, trees prebuilt)
+    from paper_1203_1692_b200.numeric import multiply_async
+    a_local = parallel.tree_from_shard(m, n, mine)
+    b_have = parallel.tree_from_shard(m, n, parallel.allgather_shards(mine), transposed=False)
+    local_ms, _ = timed(lambda: multiply_async(a_local, b_have, cfg, None), max(2, min(args.steps, 10)), 3)
     d2h = host_out.get("bytes", 0)
     io = torch.tensor([float(host_rows.numel() * 4), float(d2h)], dtype=torch.float64, device="cuda")
     dist.all_reduce(io)
@@ -477,8 +484,10 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": name, "n": m, "tau": args.tau, "granularity": args.granularity,
                        "tasks": int(tot_tasks), "products4": int(tot_p4),
-                       "parallelism": f"row blocks of A and C x{world} cut by task count, B all-gathered (NCCL) inside "
-                                      "the timed region",
+                       "parallelism": f"row blocks of A and C x{world} cut by task count; exchange of B inside the timed "
+                                      f"region: {'all-gather' if args.exchange == 'all' else 'needed leaf rows only'} (NCCL)",
+                       "without_exchange": {"ms_per_step": local_ms, "value": flops / (local_ms * 1e-3) / 1e9,
+                                            "note": "B already replicated, trees prebuilt: the local multiply alone"},
                        "tasks_per_rank": [int(w[1]) for w in per_rank],
                        "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write)"},
             "roofline": None, "cpu_baseline": None,
@@ -524,6 +533,8 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--exchange", default=os.environ.get("SPAMM_EXCHANGE", "all"), choices=("all", "needed"),
+                    help="N > 1: bring all of B to every rank (all-gather) or only the leaf rows it reaches")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

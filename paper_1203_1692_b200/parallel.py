@@ -156,6 +156,67 @@ def allgather_shards(shard: PackedShard, group=None) -> PackedShard:
     return PackedShard(gather(shard.keys, HOLE), gather(shard.records, None), gather(shard.leaf_sq, 0.0))
 
 
+def needed_rows(a_shard: PackedShard, nrows_b: int) -> torch.Tensor:
+    """Leaf rows of B that a rank holding ``a_shard`` can reach: the leaf columns of its stored A
+    leaves, widened to whole groups of ROW_ALIGN rows so 4x4 blocks of leaves travel complete."""
+    groups = -(-nrows_b // ROW_ALIGN)
+    hit = torch.zeros((groups,), dtype=torch.bool, device=a_shard.keys.device)
+    if a_shard.n:
+        cols = _squeeze16(a_shard.keys.to(torch.int64))
+        hit[torch.div(cols, ROW_ALIGN, rounding_mode="floor").clamp_(max=groups - 1)] = True
+    return hit.repeat_interleave(ROW_ALIGN)[:nrows_b]
+
+
+def exchange_needed_rows(b_shard: PackedShard, need: torch.Tensor, splits: list[tuple[int, int]], group=None) -> PackedShard:
+    """The band-limited alternative to ``allgather_shards``: every rank receives only the leaf rows
+    of B it asked for (``need``, a bool per leaf row of B), from the ranks that own them
+    (``splits[r]`` = rows of rank r).  One small all-gather of the requests and of the piece sizes,
+    then point-to-point transfers straight into the result (pieces in rank order, own rows in
+    place, no unused slots).  For a banded matrix split over N ranks a rank fetches its band, not
+    (N-1)/N of the matrix."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = b_shard.keys.device
+    nrows = int(need.shape[0])
+    asked = [torch.zeros((nrows,), dtype=torch.uint8, device=dev) for _ in range(world)]
+    dist.all_gather(asked, need.to(torch.uint8), group=group)
+    r0, r1 = splits[rank]
+    my_rows = _squeeze16(b_shard.keys.to(torch.int64) >> 1) if b_shard.n else torch.zeros((0,), dtype=torch.int64, device=dev)
+    picks = []
+    for p in range(world):
+        want = asked[p].to(torch.bool)
+        want[:r0] = False
+        want[r1:] = False
+        picks.append(torch.nonzero(want[my_rows]).flatten() if b_shard.n else my_rows)
+    sizes = torch.tensor([int(x.numel()) for x in picks], dtype=torch.int64, device=dev)
+    table = [torch.zeros((world,), dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(table, sizes, group=group)
+    incoming = [int(table[src][rank].item()) for src in range(world)]        # leaves rank src sends me
+    offs = [0]
+    for c in incoming:
+        offs.append(offs[-1] + c)
+    out = PackedShard(torch.empty((offs[-1],), dtype=b_shard.keys.dtype, device=dev),
+                      torch.empty((offs[-1], 272), dtype=torch.float32, device=dev),
+                      torch.empty((offs[-1],), dtype=torch.float64, device=dev))
+    ops, keep = [], []
+    for p in range(world):
+        sel = picks[p]
+        if p == rank:
+            sl = slice(offs[p], offs[p + 1])
+            out.keys[sl], out.records[sl], out.leaf_sq[sl] = b_shard.keys[sel], b_shard.records[sel], b_shard.leaf_sq[sel]
+            continue
+        if sel.numel():
+            bufs = (b_shard.keys[sel].contiguous(), b_shard.records[sel].contiguous(), b_shard.leaf_sq[sel].contiguous())
+            keep.append(bufs)
+            ops += [dist.P2POp(dist.isend, t, p, group) for t in bufs]
+        if incoming[p]:
+            sl = slice(offs[p], offs[p + 1])
+            ops += [dist.P2POp(dist.irecv, t[sl], p, group) for t in (out.keys, out.records, out.leaf_sq)]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return out
+
+
 def drop_holes(shard: PackedShard) -> PackedShard:
     """The stored leaves of a gathered shard, unused slots removed (tests and host export)."""
     keep = torch.nonzero(shard.keys != HOLE).flatten()
@@ -199,16 +260,27 @@ def row_task_counts(plan, depth: int) -> torch.Tensor:
 
 
 def multiply_sharded(a_shard: PackedShard, b_shard: PackedShard | None, shape_a: tuple[int, int],
-                     shape_b: tuple[int, int], cfg, group=None, device=None):
+                     shape_b: tuple[int, int], cfg, group=None, device=None, exchange: str = "all",
+                     splits: list[tuple[int, int]] | None = None):
     """C = A B with C's leaf rows split across the ranks of ``group`` like the rows of A.
 
     ``a_shard`` / ``b_shard`` are this rank's row blocks of the operands (``b_shard is None`` means
-    B is A).  The one exchange step is the all-gather of B's packed leaves.  The left operand stays
-    local: a tree holding only this rank's rows of A times the whole of B gives exactly this rank's
-    rows of C, so the partition of A (see ``balanced_row_split``) is the partition of the work.
+    B is A).  The one exchange step brings B's packed leaves to the rank: ``exchange="all"`` is the
+    all-gather; ``exchange="needed"`` fetches only the leaf rows of B that the columns of the local A
+    reach (``splits`` = the row block of every rank, needed to find the owners).  The left operand
+    stays local: a tree holding only this rank's rows of A times B gives exactly this rank's rows of
+    C, so the partition of A (see ``balanced_row_split``) is the partition of the work.
     Returns ``(c, plan, counters)``; ``c`` has the global shape and holds this rank's rows."""
     from .numeric import multiply_async
     a_local = tree_from_shard(shape_a[0], shape_a[1], a_shard, device)
-    b_full = tree_from_shard(shape_b[0], shape_b[1], allgather_shards(a_shard if b_shard is None else b_shard, group),
-                             device, transposed=False)
+    mine_b = a_shard if b_shard is None else b_shard
+    if exchange == "all":
+        got = allgather_shards(mine_b, group)
+    elif exchange == "needed":
+        if splits is None:
+            raise ValueError('exchange="needed" needs the row blocks of all ranks (splits)')
+        got = exchange_needed_rows(mine_b, needed_rows(a_shard, -(-shape_b[0] // 16)), splits, group)
+    else:
+        raise ValueError(f"unknown exchange {exchange!r}")
+    b_full = tree_from_shard(shape_b[0], shape_b[1], got, device, transposed=False)
     return multiply_async(a_local, b_full, cfg, None)

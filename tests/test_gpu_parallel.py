@@ -99,3 +99,41 @@ def test_local_rows_of_a_times_gathered_b(world):
     c2, _, _ = P.multiply(b_full, qa, P.MultiplyConfig(tau=tau, exact=True))
     c3, _, _ = P.multiply(qb, qa, P.MultiplyConfig(tau=tau, exact=True))
     assert np.array_equal(c2.to_dense().data, c3.to_dense().data)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_band_limited_exchange_gives_the_same_rows(world):
+    """exchange="needed": a rank multiplies its rows of A by ONLY the leaf rows of B its columns
+    reach (what parallel.exchange_needed_rows delivers, pieces in owner order).  Rows of C must be
+    bit-identical to the single-GPU product, and for a banded matrix most of B is never fetched."""
+    import paper_1203_1692_b200 as P
+    n, tau = 2048, 1e-6
+    a = inputs.exponential_decay(n, 0.5, seed=0)            # narrow band: entries underflow ~150 columns out
+    qa = P.QuadtreeMatrix.from_dense(a)
+    cfg = P.MultiplyConfig(tau=tau, exact=True)
+    c_ref, plan_ref, k_ref = P.multiply(qa, qa, cfg)
+    dense_ref = c_ref.to_dense().data
+    nrows = n // 16
+    split = parallel.even_row_split(nrows, world)
+    shards = [parallel.shard_of_tree(qa, r0, r1) for r0, r1 in split]
+    got = np.zeros_like(dense_ref)
+    tasks = fetched = 0
+    for rank, (r0, r1) in enumerate(split):
+        need = parallel.needed_rows(shards[rank], nrows)
+        rows_of = [parallel._squeeze16(s.keys.to(torch.int64) >> 1) for s in shards]
+        pieces = [torch.nonzero(need[rows_of[src]]).flatten() for src in range(world)]
+        part = parallel.PackedShard(torch.cat([shards[s].keys[pieces[s]] for s in range(world)]),
+                                    torch.cat([shards[s].records[pieces[s]] for s in range(world)]),
+                                    torch.cat([shards[s].leaf_sq[pieces[s]] for s in range(world)]))
+        fetched += part.n - int(pieces[rank].numel())
+        b_part = parallel.tree_from_shard(n, n, part, transposed=False)
+        a_local = parallel.tree_from_shard(n, n, shards[rank])
+        c, p, k = P.numeric.multiply_async(a_local, b_part, cfg, None)
+        d = c.to_dense().data
+        got[r0 * 16:r1 * 16] = d[r0 * 16:r1 * 16]
+        assert not d[:r0 * 16].any() and not d[r1 * 16:].any()
+        tasks += len(p)
+    assert tasks == len(plan_ref)
+    assert np.array_equal(got, dense_ref)
+    if world == 8:
+        assert fetched < 0.3 * (world - 1) * qa.nleaf          # an all-gather would move (world-1) * nleaf

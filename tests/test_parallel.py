@@ -107,6 +107,24 @@ def _worker(rank: int, world: int, port: int, n: int, tau: float, out_dir: str):
         blocks = k >> 4
         starts = np.flatnonzero(np.r_[True, blocks[1:] != blocks[:-1]])
         assert np.unique(blocks[starts]).size == starts.size          # one run per block
+        # band-limited exchange: ask only for the leaf rows of B that the local columns of A reach
+        splits = parallel.even_row_split(nrows, world)
+        need = parallel.needed_rows(mine, nrows)
+        part = parallel.exchange_needed_rows(mine, need, splits)
+        cols = np.unique(np.nonzero(full.slot[r0:r1] >= 0)[1])                  # leaf columns of my A rows
+        want_rows = np.unique(np.concatenate([np.arange(4 * (c // 4), min(nrows, 4 * (c // 4) + 4)) for c in cols]))
+        assert np.array_equal(np.flatnonzero(need.numpy()), want_rows)
+        pi, pj = morton.decode_array(part.keys.numpy().astype(np.uint64))
+        fi, fj = np.nonzero(full.slot >= 0)
+        sel = np.isin(fi, want_rows)
+        assert sorted(zip(pi.tolist(), pj.tolist())) == sorted(zip(fi[sel].tolist(), fj[sel].tolist()))
+        assert np.array_equal(part.records.numpy()[:, :256].reshape(-1, 16, 16),
+                              full.values[full.slot[pi.astype(np.int64), pj.astype(np.int64)]])
+        sq_grid = full.sq_levels[O.level_offset(full.depth):].reshape(full.L, full.L)
+        assert np.array_equal(part.leaf_sq.numpy(), sq_grid[pi.astype(np.int64), pj.astype(np.int64)])
+        pk = part.keys.numpy().astype(np.int64)
+        same_block = (pk[1:] >> 4) == (pk[:-1] >> 4)
+        assert np.all(pk[1:][same_block] > pk[:-1][same_block])                 # blocks stay in Morton order
         # balance on the replicated norms, then compute this rank's row block with the oracle
         plan = O.build_plan(full, full, tau)
         counts = np.bincount(plan.ti, minlength=nrows)
