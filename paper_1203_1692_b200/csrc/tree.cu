@@ -130,30 +130,57 @@ extern "C" int spamm_assign_slots(const float *leaf_norm, int depth, int32_t *sl
     return scan_flags(op, (int64_t)L * L, nleaf_dev, ws, ws_bytes, (cudaStream_t)stream);
 }
 
-// K1c. One 256-thread block per stored leaf.  A stored leaf is a 272-float record: 256 values
-// followed by its 16 sub-block norms, so one bulk copy stages both.  `values` holds the leaf
+// K1c. One warp per stored leaf (8 per block, grid-stride).  A stored leaf is a 272-float record: 256
+// values followed by its 16 sub-block norms, so one bulk copy stages both.  `values` holds the leaf
 // row-major with the sub-norms transposed (tail[q*4+r] = sub4[r][q], what a B operand reads);
 // `values_t` holds the transposed leaf with the sub-norms row-major (what an A operand reads).
+// VEC: the dense rows can be read 16 bytes at a time (base and row stride aligned).
+template <bool VEC>
 __global__ void __launch_bounds__(256) pack_leaves_kernel(const float *__restrict__ dense, int64_t m, int64_t n, int64_t ld,
-                                                          int L, const uint32_t *__restrict__ keys,
+                                                          int L, const uint32_t *__restrict__ keys, int64_t nleaf,
                                                           const float *__restrict__ sub4_grid, float *__restrict__ values,
                                                           float *__restrict__ values_t)
 {
-    __shared__ float tile[16][17];
-    const int64_t s = blockIdx.x;
-    uint32_t bi, bj;
-    morton_decode(keys[s], bi, bj);
-    const int r = threadIdx.x >> 4, c = threadIdx.x & 15;
-    const int64_t gi = (int64_t)bi * 16 + r, gj = (int64_t)bj * 16 + c;
-    const float v = (gi < m && gj < n) ? __ldg(dense + gi * ld + gj) : 0.0f;
-    values[s * SPAMM_REC + threadIdx.x] = v;
-    tile[r][c] = v;
-    __syncthreads();
-    values_t[s * SPAMM_REC + threadIdx.x] = tile[c][r];
-    if (threadIdx.x < 16) {
-        const float sn = sub4_grid[((int64_t)bi * L + bj) * 16 + threadIdx.x];   // threadIdx.x = p*4+q
-        values_t[s * SPAMM_REC + 256 + threadIdx.x] = sn;
-        values[s * SPAMM_REC + 256 + (threadIdx.x & 3) * 4 + (threadIdx.x >> 2)] = sn;
+    __shared__ float tile[8][16][17];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float(*t)[17] = tile[warp];
+    for (int64_t s = (int64_t)blockIdx.x * 8 + warp; s < nleaf; s += (int64_t)gridDim.x * 8) {
+        uint32_t bi, bj;
+        morton_decode(keys[s], bi, bj);
+        float4 *dst = reinterpret_cast<float4 *>(values + s * SPAMM_REC);
+        float4 *dst_t = reinterpret_cast<float4 *>(values_t + s * SPAMM_REC);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = lane + 32 * h, r = e >> 2, c = (e & 3) * 4;
+            const int64_t gi = (int64_t)bi * 16 + r, gj = (int64_t)bj * 16 + c;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (gi < m) {
+                const float *src = dense + gi * ld + gj;
+                if (VEC && gj + 3 < n) {
+                    v = __ldg(reinterpret_cast<const float4 *>(src));
+                } else {
+                    if (gj < n) v.x = __ldg(src);
+                    if (gj + 1 < n) v.y = __ldg(src + 1);
+                    if (gj + 2 < n) v.z = __ldg(src + 2);
+                    if (gj + 3 < n) v.w = __ldg(src + 3);
+                }
+            }
+            dst[e] = v;
+            t[r][c] = v.x; t[r][c + 1] = v.y; t[r][c + 2] = v.z; t[r][c + 3] = v.w;
+        }
+        float sn = 0.0f;
+        if (lane < 16) sn = sub4_grid[((int64_t)bi * L + bj) * 16 + lane];      // lane = p*4+q
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int e = lane + 32 * h, r = e >> 2, c = (e & 3) * 4;
+            dst_t[e] = make_float4(t[c][r], t[c + 1][r], t[c + 2][r], t[c + 3][r]);
+        }
+        if (lane < 16) {
+            values_t[s * SPAMM_REC + 256 + lane] = sn;
+            values[s * SPAMM_REC + 256 + (lane & 3) * 4 + (lane >> 2)] = sn;
+        }
+        __syncwarp();
     }
 }
 
@@ -163,8 +190,15 @@ extern "C" int spamm_pack_leaves(const float *dense, int64_t m, int64_t n, int64
 {
     if (nleaf == 0) return SPAMM_OK;
     if (!dense || nleaf < 0 || depth < 0 || depth > 15) return SPAMM_EINVAL;
-    pack_leaves_kernel<<<(unsigned)nleaf, 256, 0, (cudaStream_t)stream>>>(dense, m, n, ld, 1 << depth, keys, sub4_grid,
-                                                                         values, values_t);
+    int64_t blocks = (nleaf + 7) / 8;
+    if (blocks > SPAMM_NUM_SMS * 16) blocks = SPAMM_NUM_SMS * 16;
+    const bool vec = (reinterpret_cast<uintptr_t>(dense) % 16 == 0) && (ld % 4 == 0);
+    if (vec)
+        pack_leaves_kernel<true><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(dense, m, n, ld, 1 << depth, keys, nleaf,
+                                                                                    sub4_grid, values, values_t);
+    else
+        pack_leaves_kernel<false><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(dense, m, n, ld, 1 << depth, keys, nleaf,
+                                                                                     sub4_grid, values, values_t);
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
 }
@@ -478,16 +512,9 @@ extern "C" int spamm_transpose_records(const float *values, int64_t nleaf, float
 }
 
 // Grids of a tree given by packed leaves: clear, then scatter.
-// zero / nzero: optionally a region of 32-bit words to clear as well (the planner's workspace and
-// counts when the multiply pipeline runs this kernel first)
 __global__ void clear_grids_kernel(int64_t cells, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t,
-                                   double *leaf_sq_grid, uint32_t *zero0, int64_t nzero0, uint32_t *zero1, int64_t nzero1)
+                                   double *leaf_sq_grid)
 {
-    pdl_enter();
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nzero0; x += (int64_t)gridDim.x * blockDim.x)
-        zero0[x] = 0u;
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nzero1; x += (int64_t)gridDim.x * blockDim.x)
-        zero1[x] = 0u;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < cells; x += (int64_t)gridDim.x * blockDim.x) {
         slot[x] = -1;
         slot_t[x] = -1;
@@ -516,23 +543,6 @@ __global__ void scatter_leaves_kernel(const uint32_t *__restrict__ keys, const d
     }
 }
 
-int spamm_clear_leaf_grids(int depth, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid,
-                           void *zero0, size_t zero0_bytes, void *zero1, size_t zero1_bytes, cudaStream_t st)
-{
-    if (depth < 0 || depth > 15) return SPAMM_EINVAL;
-    const int L = 1 << depth;
-    const int64_t cells = (int64_t)L * L;
-    const int64_t off = spamm_level_offset(depth);
-    int blocks = (int)((cells + 255) / 256);
-    if (blocks > SPAMM_NUM_SMS * 16) blocks = SPAMM_NUM_SMS * 16;
-    if (spamm_launch_pdl(clear_grids_kernel, dim3(blocks), dim3(256), 0, st, cells, slot, slot_t, norm + off, norm_t + off,
-                         leaf_sq_grid, reinterpret_cast<uint32_t *>(zero0), (int64_t)(zero0_bytes / 4),
-                         reinterpret_cast<uint32_t *>(zero1), (int64_t)(zero1_bytes / 4)) != cudaSuccess)
-        return SPAMM_ECUDA;
-    SPAMM_CHECK_LAUNCH();
-    return SPAMM_OK;
-}
-
 int spamm_index_leaves_impl(const uint32_t *keys, const double *leaf_sq_packed, int64_t nleaf, const int32_t *nleaf_dev,
                             int depth, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t, double *leaf_sq_grid,
                             cudaStream_t st)
@@ -543,8 +553,7 @@ int spamm_index_leaves_impl(const uint32_t *keys, const double *leaf_sq_packed, 
     const int64_t off = spamm_level_offset(depth);
     int blocks = (int)((cells + 255) / 256);
     if (blocks > SPAMM_NUM_SMS * 16) blocks = SPAMM_NUM_SMS * 16;
-    clear_grids_kernel<<<blocks, 256, 0, st>>>(cells, slot, slot_t, norm + off, norm_t + off, leaf_sq_grid, nullptr, 0,
-                                               nullptr, 0);
+    clear_grids_kernel<<<blocks, 256, 0, st>>>(cells, slot, slot_t, norm + off, norm_t + off, leaf_sq_grid);
     SPAMM_CHECK_LAUNCH();
     if (nleaf > 0) {
         int sb = (int)((nleaf + 255) / 256);
