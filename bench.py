@@ -348,6 +348,20 @@ def run_single(args, torch, P, local: int) -> None:
             del ta, tb
             torch.cuda.empty_cache()
 
+    # ---- time and rate against n (the metric's other axis): the config-2 law at tau = 1e-8
+    n_sweep = []
+    if not args.no_configs and args.workload is None:
+        for nn in (1024, 2048, 8192, 16384):
+            xa, _ = inputs.make_operands("cfg2", nn)
+            ta = P.QuadtreeMatrix.from_dense(xa)
+            del xa
+            for gran in ("fine4", "coarse16"):
+                r = measure_case(P, torch, ta, ta, HEADLINE_TAU, gran, flush, fp32_peak, None, steps=3)
+                r.update({"workload": "cfg2 law", "n": nn, "effective_gflops_2n3": 2.0 * nn ** 3 / (r["ms"] * 1e-3) / 1e9})
+                n_sweep.append(r)
+            del ta
+            torch.cuda.empty_cache()
+
     line = {
         "metric": "spamm_surviving_gflops", "value": value, "unit": "GFLOP/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -371,6 +385,7 @@ def run_single(args, torch, P, local: int) -> None:
         "clocks": clocks.summary(),
         "sweep": sweep,
         "configs": others,
+        "n_sweep": n_sweep,
     }
     print(json.dumps(line))
 

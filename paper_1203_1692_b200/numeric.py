@@ -227,10 +227,10 @@ def multiply(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig | None = 
 _planner_ws: dict = {}
 
 
-def _planner_workspace(dev, nbytes: int) -> torch.Tensor:
+def _planner_workspace(dev, nbytes: int, stream: int | None = None) -> torch.Tensor:
     """The planner's workspace, one per (device, stream): the library needs it all zero when a
     multiply is enqueued and leaves it all zero, so it is cleared only when it is (re)allocated."""
-    key = (dev.index if dev.index is not None else torch.cuda.current_device(), _stream())
+    key = (dev.index, _stream() if stream is None else stream)
     ws = _planner_ws.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.zeros((max(nbytes, 1 << 20),), dtype=torch.uint8, device=dev)
@@ -273,12 +273,13 @@ def multiply_async(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig, c:
             leaf_cap = max(leaf_cap, 1 << (2 * tl))
         lay = _arena_layout(depth, cd, step_cap, leaf_cap)
         arena = torch.empty((lay.total,), dtype=torch.uint8, device=dev)
-        ws = _planner_workspace(dev, lay.plan_ws_bytes)
+        st = _stream()
+        ws = _planner_workspace(dev, lay.plan_ws_bytes, st)
         va, vb = a.view(depth), b.view(depth, left=False)
         try:
             _lib.check(lib.spamm_multiply_arena(C.byref(va), C.byref(vb), float(cfg.tau), gran, int(cfg.exact), alpha32,
                                                 r0, r1, cd, step_cap, leaf_cap, arena.data_ptr(), lay.total,
-                                                ws.data_ptr(), ws.numel(), _stream()), "multiply")
+                                                ws.data_ptr(), ws.numel(), st), "multiply")
         except Exception:
             _planner_ws.clear()         # a failed enqueue may leave the workspace dirty: start from a fresh one
             raise
