@@ -36,6 +36,7 @@ struct LevelBuf {
 };
 
 #define PLAN_BINS 1024       // super-tiles are binned by their number of step records
+#define PLAN_DENSE_MAX_LEVEL 7   // up to 128 x 128 super-tiles (n <= 8192) the walk starts densely at the tile level
 
 // Lives at the start of the workspace.  The workspace prefix (this struct and the look-back states
 // behind it) must be zero when a plan starts; the last kernel of a plan leaves it zero again, so
@@ -341,7 +342,7 @@ __device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, const LaneNor
 }
 
 // DENSE: there is no list from a coarser level; every super-tile node of the 2^tl x 2^tl grid
-// (tl <= 6) builds its candidate list itself from the level-tl norms, into shared memory.
+// (tl <= PLAN_DENSE_MAX_LEVEL) builds its candidate list itself from the level-tl norms, into shared memory.
 #define TILE_WARPS 32          // one super-tile node per warp, 32 per block: short look-back chains
 #define TILE_THREADS (TILE_WARPS * 32)
 template <bool DENSE>
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
     __shared__ int s_tile;
     __shared__ uint32_t s_wsteps[TILE_WARPS], s_wleaves[TILE_WARPS];
     __shared__ uint32_t s_base_lo, s_base_hi;
-    __shared__ uint32_t s_ks[DENSE ? TILE_WARPS : 1][DENSE ? 64 : 1];
+    __shared__ uint32_t s_ks[DENSE ? TILE_WARPS : 1][DENSE ? (1 << PLAN_DENSE_MAX_LEVEL) : 1];
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
     const int n_nodes = DENSE ? (a.St * a.St) : (a.counts[2] ? 0 : a.counts_in[0]);
@@ -779,7 +780,7 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     int32_t *res = w.shared->res;       // accumulated here, copied to out->counts by the last kernel
     int32_t *overflow = res + 2, *max_list = res + 3;
     int cur = 0;
-    const bool dense = tl <= 6 && out->leaf_capacity >= (int64_t(1) << (2 * tl));
+    const bool dense = tl <= PLAN_DENSE_MAX_LEVEL && out->leaf_capacity >= (int64_t(1) << (2 * tl));
     const int grid = SPAMM_NUM_SMS * 4;
     if (!dense) {
     if (spamm_launch_pdl(plan_root_kernel, dim3(1), dim3(ROOT_THREADS), 0, st, a->norm + spamm_level_offset(l0),

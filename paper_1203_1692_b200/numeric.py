@@ -269,7 +269,7 @@ def multiply_async(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig, c:
 
     def launch(step_cap: int, leaf_cap: int):
         """One allocation, one C call; returns the arena and its layout."""
-        if tl <= 6:     # room for every super-tile node: lets the planner start densely at that level
+        if tl <= 7:     # room for every super-tile node: lets the planner start densely at that level
             leaf_cap = max(leaf_cap, 1 << (2 * tl))
         lay = _arena_layout(depth, cd, step_cap, leaf_cap)
         arena = torch.empty((lay.total,), dtype=torch.uint8, device=dev)

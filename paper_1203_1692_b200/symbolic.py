@@ -277,7 +277,7 @@ class PlanAlloc:
 
     def __init__(self, dev, depth: int, step_cap: int, leaf_cap: int):
         tl = max(depth - 2, 0)
-        if tl <= 6:     # room for every super-tile node: lets the planner start densely at that level
+        if tl <= 7:     # room for every super-tile node: lets the planner start densely at that level
             leaf_cap = max(leaf_cap, 1 << (2 * tl))
         self.step_cap, self.leaf_cap = step_cap, leaf_cap
         self.steps = torch.empty((step_cap, _lib.STEP_WORDS), dtype=torch.int32, device=dev)
