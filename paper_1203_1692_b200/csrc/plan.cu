@@ -811,7 +811,8 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     TileArgs t;
     t.trace = nullptr;
     static const char *trace_path = getenv("SPAMM_PLAN_TRACE");      // tuning aid: allocates and synchronises
-    const int tgrid = dense ? SPAMM_NUM_SMS : SPAMM_NUM_SMS * 2;
+    // two 1024-thread blocks per SM; a dense start with at most one tile per SM (n <= 4096) keeps one
+    const int tgrid = (dense && tl <= 6) ? SPAMM_NUM_SMS : SPAMM_NUM_SMS * 2;
     if (trace_path && cudaMalloc(&t.trace, 8 * 6 * tgrid) == cudaSuccess) cudaMemsetAsync(t.trace, 0, 8 * 6 * tgrid, st);
     t.norm_a_t = a->norm + spamm_level_offset(tl);
     t.norm_bt_t = b->norm_t + spamm_level_offset(tl);
@@ -834,7 +835,7 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     t.tile_counter = &w.shared->tile_counter[PLAN_MAX_LEVELS];
     t.tile_state = w.tile_state[PLAN_MAX_LEVELS];
     if (spamm_launch_pdl(dense ? plan_tiles_kernel<true> : plan_tiles_kernel<false>,
-                         dim3(dense ? SPAMM_NUM_SMS : SPAMM_NUM_SMS * 2), dim3(TILE_THREADS), 0, st, t) != cudaSuccess)
+                         dim3(tgrid), dim3(TILE_THREADS), 0, st, t) != cudaSuccess)
         return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
     static const int unit_target = plan_env("SPAMM_UNIT_TARGET", 6 * 2 * SPAMM_NUM_SMS, 0, SPAMM_UNIT_EXTRA);
