@@ -277,6 +277,7 @@ __device__ __forceinline__ unsigned long long plan_timer()
 
 struct TileArgs {
     unsigned long long *trace;   // tuning aid (SPAMM_PLAN_TRACE): per block 6 timestamps
+    int32_t *tile_class;         // size class of every super-tile node (scratch for the order kernel)
     const float *norm_a;      // leaf level grid of A, row-major (i,k)
     const float *norm_bt;     // leaf level grid of B transposed (j,k)
     const int32_t *slot_a;    // leaf slots of A (i,k)
@@ -428,7 +429,11 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
         const uint32_t nleaves = __popc(present);
         if (lane == 0) {
             s_wsteps[warp] = nsteps; s_wleaves[warp] = nleaves; tasks_total += ntasks;
-            if (valid) atomicAdd(&a.bins[nsteps < PLAN_BINS ? nsteps : PLAN_BINS - 1], 1u);
+            if (valid) {
+                const int cls = tile_size_class((int)nsteps, (int)ntasks);
+                a.tile_class[pidx] = cls;
+                atomicAdd(&a.bins[cls], 1u);
+            }
         }
         __syncthreads();
         if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 3] = plan_timer();
@@ -536,6 +541,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
 // sort by step count (any order inside a bin; the product does not depend on it).
 struct OrderArgs {
     const int32_t *tile_off;
+    const int32_t *tile_class;    // size class per node, from the tiles kernel
     int32_t *counts;              // the caller's plan counts: written here, all SPAMM_PLAN_COUNTS of them
     PlanShared *shared;
     uint32_t *ws_tail;            // workspace prefix behind PlanShared (look-back states), left zero
@@ -620,8 +626,8 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
     }
     unsigned int cnt = 0;                   // cut tiles with more than t segments (t = 0: all tiles)
     if (t == 0) cnt = (unsigned int)n_tiles;
-    else if (seg_len && t < UNIT_MAX_SEGMENTS && (long long)t * seg_len < PLAN_BINS) {
-        const int longer = (int)s_start[t * seg_len];          // tiles with more than t * seg_len records
+    else if (seg_len && t < UNIT_MAX_SEGMENTS && (long long)t * seg_len <= UNIT_SIZE_CLAMP) {
+        const int longer = (int)s_start[t * seg_len * 8 + 7];  // tiles with more than t * seg_len records
         cnt = longer > whole ? (unsigned int)(longer - whole) : 0u;
     }
     __syncthreads();                        // s_part is reused
@@ -642,7 +648,7 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
     for (int idx = blockIdx.x * blockDim.x + t; idx < n_nodes; idx += gridDim.x * blockDim.x) {
         const int ns = tile_off[idx + 1] - tile_off[idx];
         if (ns == 0) continue;
-        const int bin = ns < PLAN_BINS ? ns : PLAN_BINS - 1;
+        const int bin = a.tile_class[idx];
         const int rank = (int)(s_start[bin] + atomicAdd(&cursor[bin], 1u));
         if (!seg_len) {
             tile_order[rank] = idx;
@@ -829,6 +835,7 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     t.steps = out->steps;
     t.c_keys = out->c_keys;
     t.tile_off = out->tile_off;
+    t.tile_class = reinterpret_cast<int32_t *>(w.buf[cur ^ 1].node);     // the level buffer not in use any more
     t.bins = w.shared->bins;
     t.cap_steps = out->step_capacity; t.cap_leaves = out->leaf_capacity;
     t.counts = res;
@@ -855,6 +862,7 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     }
     OrderArgs oa;
     oa.tile_off = out->tile_off;
+    oa.tile_class = t.tile_class;
     oa.counts = out->counts;
     oa.shared = w.shared;
     {

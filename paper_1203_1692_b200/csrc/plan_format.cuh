@@ -14,7 +14,17 @@ __host__ __device__ __forceinline__ int step_pos_dj(int pos) { return ((pos >> 2
 // node | segment << 20 | segments << 26, otherwise just the node.
 #define UNIT_NODE_BITS 20
 #define UNIT_MAX_SEGMENTS 63
-#define UNIT_SIZE_CLAMP 1023     // = PLAN_BINS - 1: tiles are ranked by min(ns, 1023)
+#define UNIT_SIZE_CLAMP 127      // tiles are ranked by (min(records, 127), how full the records are)
+// size class of a super-tile for the longest-first hand-out: records first, then eighths of fill
+// (live tasks per record slot), 0 for a tile without records; 1024 classes
+__host__ __device__ __forceinline__ int tile_size_class(int nsteps, int ntasks)
+{
+    if (nsteps <= 0) return 0;
+    const int st = nsteps < UNIT_SIZE_CLAMP ? nsteps : UNIT_SIZE_CLAMP;
+    int fill = (int)(((long long)ntasks * 8 - 1) / (64ll * nsteps));
+    fill = fill < 0 ? 0 : (fill > 7 ? 7 : fill);
+    return st * 8 + fill;
+}
 __host__ __device__ __forceinline__ uint32_t unit_pack(int node, int seg, int nseg)
 {
     return (uint32_t)node | ((uint32_t)seg << UNIT_NODE_BITS) | ((uint32_t)nseg << 26);
