@@ -14,7 +14,12 @@
 // producer warp stages each block with ONE bulk copy (TMA 1-D, cp.async.bulk, SASS UBLKCP; up to
 // 17 KB: 16 leaf records of 1088 B holding values and sub-block norms) into a ring of
 // shared-memory stages guarded by mbarriers.  Eight consumer warps (two product leaves each)
-// gate and multiply from shared memory.  Super-tiles are handed out through an atomic counter.
+// gate and multiply from shared memory; with fine4 a tenth warp first classifies the tasks of each
+// stage (all 64 micro products run / none / undecided).  The persistent CTAs (two per SM) claim work
+// units from an atomic counter: whole super-tiles, or -- when the product has few of them -- chained
+// segments of a super-tile's records whose accumulators pass from CTA to CTA through C's value
+// records (plan_format.cuh, spamm_b200.h).  Launched with programmatic dependent launch.
+// Tuning aids: SPAMM_EX_STAGES, SPAMM_EX_CTAS, SPAMM_EX_DEBUG, SPAMM_EX_TRACE (per-CTA time stamps).
 #include <stdio.h>
 #include <stdlib.h>
 

@@ -19,6 +19,10 @@
 //   (K, 4 x 16 live bits = the tasks (4I+di, 4K+kk, 4J+dj) that survive, where the two leaf blocks sit)
 // so the compacted task list comes out already in the order and grouping the numeric phase
 // consumes: ascending k per product leaf (numeric.py:203-217), leaves in Morton order.
+// For n <= 8192 the walk starts densely at the super-tile level (one kernel, no coarser levels).
+// A last kernel sorts the super-tiles into work units for the numeric kernel (longest first, the
+// last ones cut into chained segments), empties C's leaf grids, publishes the counts and returns
+// the workspace to all-zero, so a sequence of plans on one stream needs no memset.
 #include <stdio.h>
 #include <stdlib.h>
 
