@@ -172,7 +172,8 @@ typedef struct {
  * tile_order, [6..7] tasks T as one uint64, [8..9] executed 4x4x4 products as one uint64
  * (spamm_multiply only), [10] scratch, [11] all super-tile nodes (tile_off has one more entry),
  * [12] records per segment (0: every unit is a whole super-tile), [13..14] the numeric kernel's
- * hand-out and exit counters (zero between launches), [15] reserved */
+ * hand-out and exit counters (zero between launches), [15] set by the numeric kernel if a wait for
+ * a chained segment ever gives up (a scheduling bug, never in a correct run): results invalid */
 #define SPAMM_PLAN_COUNTS 16
 typedef struct {
     spamm_step *steps;       /* [step_capacity]                                   */

@@ -75,6 +75,8 @@ struct ExecArgs {
     int c_L;                     // side of C's leaf grid
     int sub2;                    // leaves per super-tile (16; 4 or 1 for tiny trees)
     int nstages;                 // depth of the shared-memory ring
+    int static_first;            // every CTA of the grid is resident: CTA b may take unit b without asking
+    int32_t *error_flag;         // plan counts[15]: set when a hand-over wait gives up (never in a correct run)
     int dbg;                     // tuning aid (SPAMM_EX_DEBUG): 1 = no copies, 2 = no math
     unsigned long long *trace;   // tuning aid (SPAMM_EX_TRACE): per CTA start / first data / end / units
 };
@@ -151,7 +153,15 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
         const bool claim_late = ntiles < 16 * (int)gridDim.x;
         const uint32_t *words = reinterpret_cast<const uint32_t *>(g.steps);
         int tile = 0, units_done = 0;
-        tile = (int)blockIdx.x;        // the first unit needs no hand-out: CTA b takes unit b, the counter the rest
+        // With the whole grid resident the first unit needs no hand-out: CTA b takes unit b, the counter
+        // hands out the rest.  (Otherwise a unit could wait for a predecessor owned by a CTA that has
+        // not started yet, so every unit is claimed.)
+        tile = (int)blockIdx.x;
+        if (!g.static_first) {
+            if (lane == 0) tile = (int)atomicAdd(g.tile_counter, 1u);
+            tile = __shfl_sync(FULL_MASK, tile, 0);
+        }
+        const int claim_base = g.static_first ? (int)gridDim.x : 0;
         while (tile < ntiles) {
             ++units_done;
             const uint32_t unit = unit_pre;
@@ -171,7 +181,7 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
             // on a whole unit it has not started while others run dry.  With many whole tiles it is
             // claimed right away.
             int next_tile = 0;
-            if (lane == 0 && !claim_late) next_tile = (int)(atomicAdd(g.tile_counter, 1u) + gridDim.x);
+            if (lane == 0 && !claim_late) next_tile = (int)atomicAdd(g.tile_counter, 1u) + claim_base;
             // lane l < 16 holds word l of a record (struct spamm_step)
             uint32_t w[EX_PREFETCH];
 #pragma unroll
@@ -179,7 +189,7 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
                 w[x] = (lane < 16 && beg + x < end) ? __ldg(words + (size_t)(beg + x) * 16 + lane) : 0u;
             for (int r = beg; r < end; ++r) {
                 if (lane == 0 && claim_late && (r + 2 == end || (r == beg && r + 2 > end)))
-                    next_tile = (int)(atomicAdd(g.tile_counter, 1u) + gridDim.x);
+                    next_tile = (int)atomicAdd(g.tile_counter, 1u) + claim_base;
                 const uint32_t cur = w[0];
 #pragma unroll
                 for (int x = 0; x + 1 < EX_PREFETCH; ++x) w[x] = w[x + 1];
@@ -317,7 +327,15 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
             if ((present_in >> mypos) & 1u) {
                 const int64_t cs = (int64_t)ds.c_base + __popc(present_in & ((1u << mypos) - 1u));
                 const int want = (int)ds.seg;
-                while (ld_acquire_gpu(g.chain + cs) < want) __nanosleep(40);
+                // the predecessor was handed out earlier to a running CTA; the bound only turns a
+                // scheduling bug into an error flag instead of a hang
+                for (unsigned spins = 0; ld_acquire_gpu(g.chain + cs) < want; ++spins) {
+                    __nanosleep(40);
+                    if (spins > (1u << 25)) {
+                        if (g.error_flag) *g.error_flag = 1;
+                        break;
+                    }
+                }
                 // thread t16 keeps its 16 partial sums in registers order at floats [16 t16, 16 t16 + 16)
                 const float4 *cv = reinterpret_cast<const float4 *>(g.c_values + cs * SPAMM_REC + 16 * t16);
 #pragma unroll
@@ -545,6 +563,7 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     g.counts = plan->counts;
     g.tile_counter = reinterpret_cast<unsigned int *>(plan->counts + 13);   // [13] hand-out, [14] exited CTAs
     g.chain = plan->chain;
+    g.error_flag = plan->counts + 15;
     g.tau = tau;
     g.alpha = alpha;
     g.alpha_is_one = (alpha == 1.0f);
@@ -584,6 +603,19 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     static const char *trace_path = getenv("SPAMM_EX_TRACE");     // tuning aid: allocates and synchronises
     if (trace_path && cudaMalloc(&g.trace, sizeof(unsigned long long) * 4 * grid) != cudaSuccess) g.trace = nullptr;
     if (g.trace) cudaMemsetAsync(g.trace, 0, sizeof(unsigned long long) * 4 * grid, st);
+    {
+        // is the whole persistent grid resident at once on this device?
+        static int resident[4] = {-1, -1, -1, -1};
+        const int which = (exact ? 2 : 0) + (fine ? 1 : 0);
+        if (resident[which] < 0) {
+            int dev = 0, sms = 0, per_sm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fine ? EX_THREADS_FINE : EX_THREADS, smem);
+            resident[which] = (long long)per_sm * sms >= grid ? 1 : 0;
+        }
+        g.static_first = resident[which];
+    }
     if (spamm_launch_pdl(kern, dim3(grid), dim3(fine ? EX_THREADS_FINE : EX_THREADS), smem, st, g) != cudaSuccess)
         return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();

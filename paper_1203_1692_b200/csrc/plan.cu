@@ -282,6 +282,7 @@ __device__ __forceinline__ unsigned long long plan_timer()
 struct TileArgs {
     unsigned long long *trace;   // tuning aid (SPAMM_PLAN_TRACE): per block 6 timestamps
     int32_t *tile_class;         // size class of every super-tile node (scratch for the order kernel)
+    int all_resident;            // every block of the grid is resident at once (one per SM on this device)
     const float *norm_a;      // leaf level grid of A, row-major (i,k)
     const float *norm_bt;     // leaf level grid of B transposed (j,k)
     const int32_t *slot_a;    // leaf slots of A (i,k)
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
     unsigned long long tasks_total = 0;
     if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6] = plan_timer();
     // dense start with no more tiles than blocks: block b takes tile b, no hand-out counter
-    const bool fixed_tiles = DENSE && ntiles <= (int)gridDim.x;
+    const bool fixed_tiles = DENSE && a.all_resident && ntiles <= (int)gridDim.x;
     for (int round = 0;; ++round) {
         __syncthreads();
         if (!fixed_tiles && threadIdx.x == 0) s_tile = (int)atomicAdd(a.tile_counter, 1u);
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
             const uint32_t rs = __shfl_sync(FULL_MASK, is, TILE_WARPS - 1), rl = __shfl_sync(FULL_MASK, il, TILE_WARPS - 1);
             if (lane < TILE_WARPS) { s_wsteps[lane] = is - vs; s_wleaves[lane] = il - vl; }
             uint32_t ex_lo, ex_hi;
-            if (DENSE && ntiles <= 128 && ntiles <= (int)gridDim.x) all_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
+            if (fixed_tiles && ntiles <= 128) all_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
             else lb_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
             if (lane == 0) {
                 s_base_lo = ex_lo;
@@ -838,6 +839,15 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     t.counts_in = w.shared->counts[tl];
     t.steps = out->steps;
     t.c_keys = out->c_keys;
+    {
+        static int sms = -1;
+        if (sms < 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        t.all_resident = sms >= tgrid ? 1 : 0;      // 1024 threads x 64 registers: one block per SM
+    }
     t.tile_off = out->tile_off;
     t.tile_class = reinterpret_cast<int32_t *>(w.buf[cur ^ 1].node);     // the level buffer not in use any more
     t.bins = w.shared->bins;

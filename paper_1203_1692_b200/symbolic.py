@@ -74,6 +74,8 @@ class MultiplyPlan:
             cnt = self.counts.tolist()
         if cnt[2]:
             raise RuntimeError("plan buffers overflowed")
+        if cnt[15]:
+            raise RuntimeError("the numeric kernel gave up waiting for a chained segment (scheduling bug): results invalid")
         self._n_cleaves, self._n_steps = cnt[0], cnt[4]
         self._n_tasks = (cnt[6] & 0xFFFFFFFF) | ((cnt[7] & 0xFFFFFFFF) << 32)
         self._products4 = (cnt[8] & 0xFFFFFFFF) | ((cnt[9] & 0xFFFFFFFF) << 32)   # spamm_multiply only

@@ -19,15 +19,19 @@ SETTINGS = [
     {"SPAMM_EX_CTAS": "1", "SPAMM_EX_STAGES": "2", "SPAMM_UNIT_MIN_SEG": "3"},
     {"SPAMM_UNIT_TARGET": "0"},                                          # whole tiles only
     {"SPAMM_PDL": "0", "SPAMM_EX_CTAS": "1", "SPAMM_UNIT_MIN_SEG": "2"},
+    # a grid larger than what is resident (3 CTAs per SM requested, 2 fit) with chained segments:
+    # every unit must then be claimed dynamically or a wait could starve its predecessor
+    {"SPAMM_EX_CTAS": "3", "SPAMM_UNIT_MIN_SEG": "1", "N": "4096"},
 ]
 
 
-@pytest.mark.parametrize("env", SETTINGS, ids=lambda e: ",".join(f"{k[6:]}={v}" for k, v in e.items()) or "defaults")
+@pytest.mark.parametrize("env", SETTINGS, ids=lambda e: ",".join(f"{k[6:] if k.startswith('SPAMM_') else k}={v}" for k, v in e.items()) or "defaults")
 def test_scheduling_knobs_do_not_change_results(env):
     full = dict(os.environ)
-    full.update(env)
-    out = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "stress_child.py"), "2048", "1e-8", "6"],
+    full.update({k: v for k, v in env.items() if k != "N"})
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "stress_child.py"), env.get("N", "2048"), "1e-8",
+                          "6" if "N" not in env else "3"],
                          env=full, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("OK"), out.stdout[-2000:] + out.stderr[-2000:]
-    if env.get("SPAMM_EX_CTAS") == "1" and env.get("SPAMM_UNIT_TARGET") != "0":
+    if (env.get("SPAMM_EX_CTAS") == "1" or "N" in env) and env.get("SPAMM_UNIT_TARGET") != "0":
         assert "seg_len=0" not in out.stdout, "this setting is meant to exercise chained segments: " + out.stdout
