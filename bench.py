@@ -223,7 +223,7 @@ def kernel_time_execute(P, torch, plan, qa, qb, cfg, reps, flush):
     return float(np.mean(times))
 
 
-def measure_case(P, torch, qa, qb, tau, gran, flush, fp32_peak, ref64=None, steps=5):
+def measure_case(P, torch, qa, qb, tau, gran, flush, fp32_peak, ref64=None, steps=5, hbm_gbs=None):
     cf = P.MultiplyConfig(tau=tau, granularity=gran)
     ts, (cs, pl, ks) = timed_multiply(P, torch, qa, qb, cf, steps, 3, flush)
     fl = 128 * ks.products4 if gran == "fine4" else 8192 * len(pl)
@@ -233,10 +233,17 @@ def measure_case(P, torch, qa, qb, tau, gran, flush, fp32_peak, ref64=None, step
         err = float((cs.to_dense_tensor().double() - ref64).abs().max().item())
     L = 1 << pl.depth
     med = float(np.median(ts))
-    return {"tau": tau, "granularity": gran, "ms": med, "tasks": len(pl), "task_fraction": len(pl) / float(L) ** 3,
-            "products4": ks.products4, "gflops": fl / (med * 1e-3) / 1e9, "kernel_ms": kt,
-            "kernel_tflops": fl / (kt * 1e-3) / 1e12, "kernel_frac_fp32_peak": fl / (kt * 1e-3) / 1e12 / fp32_peak,
-            "max_abs_err_vs_fp64": err}
+    # compulsory traffic of the leaf-multiply kernel: every stored operand leaf once (A and B are the same
+    # records when the operands are one tree), the product leaves in both layouts, the step records
+    operand_leaves = qa.nleaf + (0 if qb is qa else qb.nleaf) + (qa.nleaf if qb is qa else 0)
+    alg_bytes = 1088 * (operand_leaves + 2 * pl.n_cleaves) + 64 * pl.n_steps
+    out = {"tau": tau, "granularity": gran, "ms": med, "tasks": len(pl), "task_fraction": len(pl) / float(L) ** 3,
+           "products4": ks.products4, "product_leaves": pl.n_cleaves, "gflops": fl / (med * 1e-3) / 1e9, "kernel_ms": kt,
+           "kernel_tflops": fl / (kt * 1e-3) / 1e12, "kernel_frac_fp32_peak": fl / (kt * 1e-3) / 1e12 / fp32_peak,
+           "kernel_algorithmic_bytes": int(alg_bytes), "max_abs_err_vs_fp64": err}
+    if hbm_gbs:
+        out["kernel_frac_hbm_peak"] = alg_bytes / (kt * 1e-3) / 1e9 / hbm_gbs
+    return out
 
 
 def run_single(args, torch, P, local: int) -> None:
@@ -309,7 +316,7 @@ def run_single(args, torch, P, local: int) -> None:
             del ad, bd
         for tau in inputs.WORKLOADS[name].taus:
             for gran in ("fine4", "coarse16"):
-                sweep.append(measure_case(P, torch, qa, qb, tau, gran, flush, fp32_peak, ref64))
+                sweep.append(measure_case(P, torch, qa, qb, tau, gran, flush, fp32_peak, ref64, hbm_gbs=pk["hbm_gbs"]))
         del ref64
 
     # ---- CPU baseline beside it: the oracle port on the host cores
@@ -342,7 +349,7 @@ def run_single(args, torch, P, local: int) -> None:
             del xa, xb
             for tau in inputs.WORKLOADS[wl].taus:
                 for gran in ("fine4", "coarse16"):
-                    r = measure_case(P, torch, ta, tb, tau, gran, flush, fp32_peak, None, steps=3)
+                    r = measure_case(P, torch, ta, tb, tau, gran, flush, fp32_peak, None, steps=3, hbm_gbs=pk["hbm_gbs"])
                     r.update({"workload": wl, "n": nn})
                     others.append(r)
             del ta, tb
@@ -356,7 +363,7 @@ def run_single(args, torch, P, local: int) -> None:
             ta = P.QuadtreeMatrix.from_dense(xa)
             del xa
             for gran in ("fine4", "coarse16"):
-                r = measure_case(P, torch, ta, ta, HEADLINE_TAU, gran, flush, fp32_peak, None, steps=3)
+                r = measure_case(P, torch, ta, ta, HEADLINE_TAU, gran, flush, fp32_peak, None, steps=3, hbm_gbs=pk["hbm_gbs"])
                 r.update({"workload": "cfg2 law", "n": nn, "effective_gflops_2n3": 2.0 * nn ** 3 / (r["ms"] * 1e-3) / 1e9})
                 n_sweep.append(r)
             del ta
