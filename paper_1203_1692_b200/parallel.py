@@ -261,7 +261,7 @@ def row_task_counts(plan, depth: int) -> torch.Tensor:
 
 def multiply_sharded(a_shard: PackedShard, b_shard: PackedShard | None, shape_a: tuple[int, int],
                      shape_b: tuple[int, int], cfg, group=None, device=None, exchange: str = "all",
-                     splits: list[tuple[int, int]] | None = None):
+                     splits: list[tuple[int, int]] | None = None, a_tree=None):
     """C = A B with C's leaf rows split across the ranks of ``group`` like the rows of A.
 
     ``a_shard`` / ``b_shard`` are this rank's row blocks of the operands (``b_shard is None`` means
@@ -270,9 +270,11 @@ def multiply_sharded(a_shard: PackedShard, b_shard: PackedShard | None, shape_a:
     reach (``splits`` = the row block of every rank, needed to find the owners).  The left operand
     stays local: a tree holding only this rank's rows of A times B gives exactly this rank's rows of
     C, so the partition of A (see ``balanced_row_split``) is the partition of the work.
+    ``a_tree``: the tree of the local rows when the caller already holds one (a resident operand, or
+    the product of a previous sharded multiply), which saves rebuilding its transposed leaf copies.
     Returns ``(c, plan, counters)``; ``c`` has the global shape and holds this rank's rows."""
     from .numeric import multiply_async
-    a_local = tree_from_shard(shape_a[0], shape_a[1], a_shard, device)
+    a_local = a_tree if a_tree is not None else tree_from_shard(shape_a[0], shape_a[1], a_shard, device)
     mine_b = a_shard if b_shard is None else b_shard
     if exchange == "all":
         got = allgather_shards(mine_b, group)
