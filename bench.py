@@ -223,6 +223,36 @@ def kernel_time_execute(P, torch, plan, qa, qb, cfg, reps, flush):
     return float(np.mean(times))
 
 
+def touched_leaves(torch, plan, nleaf_a: int, nleaf_b: int):
+    """Distinct stored leaves of A and of B that occur in at least one task of the plan (SURVEY.md 8d:
+    the operand part of the numeric kernel's compulsory traffic), counted on the device from the
+    step records."""
+    st = plan.steps[: plan.n_steps].to(torch.int64) & 0xFFFFFFFF
+
+    def popc16(x):
+        x = x - ((x >> 1) & 0x5555)
+        x = (x & 0x3333) + ((x >> 2) & 0x3333)
+        x = (x + (x >> 4)) & 0x0F0F
+        return (x + (x >> 8)) & 0x1F
+
+    def pos(r, c):          # Morton position of leaf (r, c) inside its 4x4 block
+        return ((r >> 1) << 3) | ((c >> 1) << 2) | ((r & 1) << 1) | (c & 1)
+
+    rowmask = [sum(1 << pos(d, c) for c in range(4)) for d in range(4)]
+    colmask = [sum(1 << pos(r, d) for r in range(4)) for d in range(4)]
+    hit_a = torch.zeros((max(nleaf_a, 1),), dtype=torch.bool, device=st.device)
+    hit_b = torch.zeros((max(nleaf_b, 1),), dtype=torch.bool, device=st.device)
+    a_first, a_present, b_first, b_present = st[:, 4], st[:, 5], st[:, 6], st[:, 7]
+    for kk in range(4):
+        live = st[:, 8 + kk]
+        for d in range(4):
+            use = (live & rowmask[d]) != 0
+            hit_a[(a_first + popc16(a_present & ((1 << pos(d, kk)) - 1)))[use]] = True
+            use = (live & colmask[d]) != 0
+            hit_b[(b_first + popc16(b_present & ((1 << pos(kk, d)) - 1)))[use]] = True
+    return int(hit_a.sum().item()), int(hit_b.sum().item())
+
+
 def measure_case(P, torch, qa, qb, tau, gran, flush, fp32_peak, ref64=None, steps=5, hbm_gbs=None):
     cf = P.MultiplyConfig(tau=tau, granularity=gran)
     ts, (cs, pl, ks) = timed_multiply(P, torch, qa, qb, cf, steps, 3, flush)
@@ -233,14 +263,15 @@ def measure_case(P, torch, qa, qb, tau, gran, flush, fp32_peak, ref64=None, step
         err = float((cs.to_dense_tensor().double() - ref64).abs().max().item())
     L = 1 << pl.depth
     med = float(np.median(ts))
-    # compulsory traffic of the leaf-multiply kernel: every stored operand leaf once (A and B are the same
-    # records when the operands are one tree), the product leaves in both layouts, the step records
-    operand_leaves = qa.nleaf + (0 if qb is qa else qb.nleaf) + (qa.nleaf if qb is qa else 0)
-    alg_bytes = 1088 * (operand_leaves + 2 * pl.n_cleaves) + 64 * pl.n_steps
+    # compulsory traffic of the leaf-multiply kernel: every operand leaf that occurs in a task once, the
+    # product leaves in both layouts, the step records
+    ta_hit, tb_hit = touched_leaves(torch, pl, qa.nleaf, qb.nleaf)
+    alg_bytes = 1088 * (ta_hit + tb_hit + 2 * pl.n_cleaves) + 64 * pl.n_steps
     out = {"tau": tau, "granularity": gran, "ms": med, "tasks": len(pl), "task_fraction": len(pl) / float(L) ** 3,
            "products4": ks.products4, "product_leaves": pl.n_cleaves, "gflops": fl / (med * 1e-3) / 1e9, "kernel_ms": kt,
            "kernel_tflops": fl / (kt * 1e-3) / 1e12, "kernel_frac_fp32_peak": fl / (kt * 1e-3) / 1e12 / fp32_peak,
-           "kernel_algorithmic_bytes": int(alg_bytes), "max_abs_err_vs_fp64": err}
+           "kernel_algorithmic_bytes": int(alg_bytes), "operand_leaves_in_tasks": [ta_hit, tb_hit],
+           "max_abs_err_vs_fp64": err}
     if hbm_gbs:
         out["kernel_frac_hbm_peak"] = alg_bytes / (kt * 1e-3) / 1e9 / hbm_gbs
     return out
@@ -272,9 +303,10 @@ def run_single(args, torch, P, local: int) -> None:
     # ---- the dominant kernel alone, for the roofline
     k3_ms = kernel_time_execute(P, torch, plan, qa, qb, cfg, max(5, min(args.steps, 50)), flush)
     k3_tflops = flops / (k3_ms * 1e-3) / 1e12
-    # compulsory traffic of the kernel: every stored A leaf (transposed copy) and B leaf once, C leaves
-    # written in both layouts, step records
-    alg_bytes = 1088 * (qa.nleaf + qb.nleaf + 2 * plan.n_cleaves) + 64 * plan.n_steps
+    # compulsory traffic of the kernel: every A leaf (transposed copy) and B leaf that occurs in a task
+    # once, C leaves written in both layouts, step records
+    ta_hit, tb_hit = touched_leaves(torch, plan, qa.nleaf, qb.nleaf)
+    alg_bytes = 1088 * (ta_hit + tb_hit + 2 * plan.n_cleaves) + 64 * plan.n_steps
     n_tasks, n_cleaves = len(plan), plan.n_cleaves
 
     # ---- end to end through the public API with host buffers

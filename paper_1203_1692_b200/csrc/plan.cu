@@ -283,6 +283,7 @@ struct TileArgs {
     unsigned long long *trace;   // tuning aid (SPAMM_PLAN_TRACE): per block 6 timestamps
     int32_t *tile_class;         // size class of every super-tile node (scratch for the order kernel)
     int all_resident;            // every block of the grid is resident at once (one per SM on this device)
+    int flat_order;              // experiment (SPAMM_ORDER_FLAT): one size class, i.e. hand-out in about Morton order
     const float *norm_a;      // leaf level grid of A, row-major (i,k)
     const float *norm_bt;     // leaf level grid of B transposed (j,k)
     const int32_t *slot_a;    // leaf slots of A (i,k)
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
         if (lane == 0) {
             s_wsteps[warp] = nsteps; s_wleaves[warp] = nleaves; tasks_total += ntasks;
             if (valid) {
-                const int cls = tile_size_class((int)nsteps, (int)ntasks);
+                const int cls = a.flat_order ? (nsteps ? 8 : 0) : tile_size_class((int)nsteps, (int)ntasks);
                 a.tile_class[pidx] = cls;
                 atomicAdd(&a.bins[cls], 1u);
             }
@@ -848,6 +849,8 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
         }
         t.all_resident = sms >= tgrid ? 1 : 0;      // 1024 threads x 64 registers: one block per SM
     }
+    static const int flat_env = plan_env("SPAMM_ORDER_FLAT", 0, 0, 1);
+    t.flat_order = flat_env;
     t.tile_off = out->tile_off;
     t.tile_class = reinterpret_cast<int32_t *>(w.buf[cur ^ 1].node);     // the level buffer not in use any more
     t.bins = w.shared->bins;
