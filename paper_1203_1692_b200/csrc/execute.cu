@@ -77,6 +77,8 @@ struct ExecArgs {
     int nstages;                 // depth of the shared-memory ring
     int static_first;            // every CTA of the grid is resident: CTA b may take unit b without asking
     int32_t *error_flag;         // plan counts[15]: set when a hand-over wait gives up (never in a correct run)
+    uint32_t *clean_ptr;         // the planner's shared state, returned to zero here on behalf of the planner
+    int clean_words;             // (spamm_multiply; 0 otherwise)
     int dbg;                     // tuning aid (SPAMM_EX_DEBUG): 1 = no copies, 2 = no math
     unsigned long long *trace;   // tuning aid (SPAMM_EX_TRACE): per CTA start / first data / end / units
 };
@@ -131,6 +133,8 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
     pdl_enter();
+    if (blockIdx.x == 0)
+        for (int x = threadIdx.x; x < g.clean_words; x += blockDim.x) g.clean_ptr[x] = 0u;
     if (threadIdx.x == 0) {
         for (int s = 0; s < nstages; ++s) {
             mbar_init(&full_bar[s], 1);
@@ -548,7 +552,7 @@ static ExecTuning exec_tuning()
 int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const spamm_plan_buffers *plan,
                        int64_t nsteps, int64_t nC, double tau, float alpha, int granularity, int exact,
                        float *c_values, float *c_values_t, double *c_leaf_sq, unsigned long long *counters,
-                       const spamm_product_buffers *cgrid, void *stream)
+                       const spamm_product_buffers *cgrid, uint32_t *clean_ptr, int clean_words, void *stream)
 {
     if (!a || !b || !plan || nsteps < -1 || nC < -1) return SPAMM_EINVAL;
     if (granularity != SPAMM_FINE4 && granularity != SPAMM_COARSE16) return SPAMM_EINVAL;
@@ -564,6 +568,8 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     g.tile_counter = reinterpret_cast<unsigned int *>(plan->counts + 13);   // [13] hand-out, [14] exited CTAs
     g.chain = plan->chain;
     g.error_flag = plan->counts + 15;
+    g.clean_ptr = clean_ptr;
+    g.clean_words = clean_words;
     g.tau = tau;
     g.alpha = alpha;
     g.alpha_is_one = (alpha == 1.0f);
@@ -640,7 +646,7 @@ extern "C" int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b,
                              void *stream)
 {
     return spamm_execute_impl(a, b, plan, nsteps, nC, tau, alpha, granularity, exact, c_values, c_values_t, c_leaf_sq,
-                              counters, nullptr, stream);
+                              counters, nullptr, nullptr, 0, stream);
 }
 
 // ---- beta != 0: union of the old and the produced leaf sets, then _compose ----------------------

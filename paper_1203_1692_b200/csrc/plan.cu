@@ -548,6 +548,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
 struct OrderArgs {
     const int32_t *tile_off;
     const int32_t *tile_class;    // size class per node, from the tiles kernel
+    int defer_clean;              // the caller's next kernel clears PlanShared (spamm_multiply)
     int32_t *counts;              // the caller's plan counts: written here, all SPAMM_PLAN_COUNTS of them
     PlanShared *shared;
     uint32_t *ws_tail;            // workspace prefix behind PlanShared (look-back states), left zero
@@ -666,6 +667,18 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
         tile_order[rank >= whole ? rank - whole : n_tiles - whole + rank] = (int32_t)unit_pack(idx, 0, nseg);
         for (int sgm = 1; sgm < nseg; ++sgm) tile_order[s_base[sgm] + rank - whole] = (int32_t)unit_pack(idx, sgm, nseg);
     }
+    if (a.defer_clean) {
+        // the numeric kernel that follows returns the shared planner state to zero (its first block,
+        // once this kernel has completed); the counts are final already, block 0 publishes them
+        if (blockIdx.x == 0 && t < SPAMM_PLAN_COUNTS) {
+            int32_t v = 0;
+            if (t == 0 || t == 2 || t == 3 || t == 4 || t == 6 || t == 7 || t == 11) v = counts[t];
+            if (t == 5) v = s_units;
+            if (t == 12) v = seg_len;
+            a.counts[t] = v;
+        }
+        return;
+    }
     // the last block publishes the counts and leaves the shared planner state zero for the next plan
     __threadfence();
     __syncthreads();
@@ -775,7 +788,7 @@ size_t spamm_plan_zero_bytes(int64_t step_capacity, int64_t leaf_capacity)
 // prezeroed: the caller has already cleared that region and out->counts on the stream
 int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
                     const spamm_plan_buffers *out, void *ws, size_t ws_bytes, bool prezeroed,
-                    const spamm_product_buffers *cgrid, void *stream)
+                    const spamm_product_buffers *cgrid, uint32_t **clean_ptr, int *clean_words, void *stream)
 {
     if (!a || !b || !out || !ws) return SPAMM_EINVAL;
     if (!(tau >= 0.0)) return SPAMM_EINVAL;                       // NaN or negative (symbolic.py:99-100)
@@ -878,6 +891,11 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
         cudaFree(t.trace);
     }
     OrderArgs oa;
+    oa.defer_clean = (cgrid != nullptr && clean_words) ? 1 : 0;
+    if (clean_words) {
+        *clean_ptr = reinterpret_cast<uint32_t *>(w.shared);
+        *clean_words = oa.defer_clean ? (int)(sizeof(PlanShared) / 4) : 0;
+    }
     oa.tile_off = out->tile_off;
     oa.tile_class = t.tile_class;
     oa.counts = out->counts;
@@ -908,5 +926,5 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
 extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
                           const spamm_plan_buffers *out, void *ws, size_t ws_bytes, void *stream)
 {
-    return spamm_plan_impl(a, b, tau, row0, row1, out, ws, ws_bytes, false, nullptr, stream);
+    return spamm_plan_impl(a, b, tau, row0, row1, out, ws, ws_bytes, false, nullptr, nullptr, nullptr, stream);
 }
