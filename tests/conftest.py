@@ -18,6 +18,14 @@ for p in (ROOT, os.path.join(ROOT, "tests"), os.path.join(ROOT, "tests", "golden
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (run on the B200 box)")
+    # a fresh checkout has no built library (it is git-ignored): build it once, as __graft_entry__.build() does
+    lib = os.path.join(ROOT, "paper_1203_1692_b200", "csrc", "libspamm_b200.so")
+    if not os.path.exists(lib):
+        import shutil
+        import subprocess
+        if shutil.which("nvcc") or os.path.exists("/usr/local/cuda/bin/nvcc"):
+            subprocess.run(["sh", os.path.join(ROOT, "paper_1203_1692_b200", "csrc", "build.sh")], check=False,
+                           stdout=subprocess.DEVNULL)
 
 
 def pytest_collection_modifyitems(config, items):
