@@ -560,6 +560,11 @@ def run_own(args) -> None:
     import torch
     import torch.distributed as dist
 
+    if not os.path.exists(os.path.join(ROOT, "paper_1203_1692_b200", "csrc", "libspamm_b200.so")):
+        if int(os.environ.get("LOCAL_RANK", "0")) == 0:     # a bare checkout: compile the library once
+            import __graft_entry__
+            __graft_entry__.build()
+
     import paper_1203_1692_b200 as P
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
