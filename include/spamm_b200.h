@@ -9,7 +9,8 @@
  * through ctypes; INTEGRATION.md shows the stub a maintainer of the reference
  * would add.  Every function:
  *   - takes raw DEVICE pointers, sizes and a cudaStream_t (as void*),
- *   - is stream-ordered, never allocates and never synchronises,
+ *   - is stream-ordered, never allocates and never synchronises (the env-gated tuning traces
+ *     SPAMM_EX_TRACE / SPAMM_PLAN_TRACE do both; they are diagnostics, off by default),
  *   - returns 0 on success, a SPAMM_E* code otherwise (spamm_error_string()).
  * Counts that the host needs (leaves, tasks) are written to device memory; the
  * caller decides when to read them back.
@@ -29,7 +30,7 @@
 extern "C" {
 #endif
 
-#define SPAMM_ABI_VERSION 1
+#define SPAMM_ABI_VERSION 2
 
 enum {
     SPAMM_OK = 0,
@@ -53,6 +54,11 @@ enum { SPAMM_EXEC_FMA = 0, SPAMM_EXEC_EXACT = 1 };   /* EXACT: separate mul/add 
  *   slot_t    [L*L]         transposed grid: (j,i) -> index
  *   norm      level buffer  node norms, -1 = absent node        (TreeNode.norm, core.py:138-143)
  *   norm_t    level buffer  every level's grid transposed
+ *   sub       [L*L]         optional (may be NULL): per leaf the range of its 16 sub-block norms,
+ *                           bf16(max) rounded up << 16 | bf16(min) rounded down, 0xFFFFFFFF = absent
+ *                           or not finite (spamm_subrange_grids); lets the planner classify the
+ *                           tasks whose 64 gated micro products (numeric.py:233-238) all pass or all fail
+ *   sub_t     [L*L]         the same grid transposed
  */
 typedef struct {
     int32_t m, n;           /* logical size */
@@ -65,6 +71,8 @@ typedef struct {
     const int32_t *slot_t;
     const float *norm;
     const float *norm_t;
+    const uint32_t *sub;
+    const uint32_t *sub_t;
 } spamm_tree_view;
 
 int spamm_abi_version(void);
@@ -127,6 +135,11 @@ int spamm_index_leaves(const uint32_t *keys, const double *leaf_sq_packed, int64
                        int32_t *slot, int32_t *slot_t, float *norm, float *norm_t,
                        double *leaf_sq_grid, void *stream);
 
+/* Sub-norm range grids of a tree (see spamm_tree_view.sub): from the sub-norm tails of the `values`
+ * records through the slot grid at `depth`. */
+int spamm_subrange_grids(const float *values, const int32_t *slot, int depth, uint32_t *sub,
+                         uint32_t *sub_t, void *stream);
+
 /* QuadtreeMatrix.to_dense (core.py:268-276): out is m x n, row stride ld, fully written. */
 int spamm_to_dense(const spamm_tree_view *t, float *out, int64_t ld, void *stream);
 
@@ -162,9 +175,15 @@ typedef struct {
     uint32_t a_present;    /* its stored leaves, bit morton4(di,kk)                        */
     uint32_t b_first;      /* packed index of the first stored leaf of block B[K,J]        */
     uint32_t b_present;    /* its stored leaves, bit morton4(kk,dj)                        */
-    uint32_t live[4];      /* live tasks of k = 4K + kk, bit morton4(di,dj)                */
+    uint32_t live[4];      /* bits 0..15: live tasks of k = 4K + kk, bit morton4(di,dj);
+                              bits 16..31: those of them whose 64 gated micro products all
+                              pass (fine4, numeric.py:233-238), known from the sub-norm ranges */
     uint32_t present;      /* product leaves of the super-tile (same bit numbering)        */
-    uint32_t pad[3];
+    uint32_t dead[2];      /* live tasks of which NO gated micro product passes: kk = 0, 1
+                              in the halves of dead[0], kk = 2, 3 in dead[1]; a task in
+                              neither set is gated per micro product by the numeric kernel
+                              (all zero when the operands carry no sub-norm ranges)         */
+    uint32_t pad;
 } spamm_step;
 
 /* counts[]: [0] product leaves nC, [1] unused,
@@ -217,6 +236,15 @@ int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b,
                   float *c_values, float *c_values_t, double *c_leaf_sq,
                   unsigned long long *counters, void *stream);
 
+/* spamm_execute (fine4, fused multiply-add, alpha = 1) that also reports the gate the kernel itself
+ * evaluated: gates[record * 64 + kk * 16 + morton4(di,dj)] receives bit r*16 + p*4 + q for every
+ * 4x4x4 micro product (p,q,r) of that task that ran (numeric.py:233-238).  gates holds 64 words per
+ * step record and must be zero when the call is enqueued.  Evidence for the parity tests. */
+int spamm_execute_gates(const spamm_tree_view *a, const spamm_tree_view *b,
+                        const spamm_plan_buffers *plan, int64_t nsteps, int64_t nC, double tau,
+                        float *c_values, float *c_values_t, double *c_leaf_sq,
+                        unsigned long long *counters, unsigned long long *gates, void *stream);
+
 /* Leaf set of C for beta != 0: the union of the accumulator's stored leaves (slot_old, an L*L
  * grid) and the produced leaves (prod_keys, ascending), in ascending Morton order.  For output
  * leaf x: out_keys[x], and the packed index of the leaf on either side (idx_old / idx_prod, -1
@@ -245,7 +273,7 @@ typedef struct {
 /* build_plan + execute_plan + compute_norms on C, enqueued back to back on `stream` with no
  * host synchronisation: C = alpha32 * sum of the surviving leaf products.  The product leaves
  * are plan->c_keys[0 .. counts[0]) with their records in c->values / c->values_t; the number of
- * executed micro products (ExecCounters.products4) accumulates in counts[8..9].  The caller
+ * executed micro products (ExecCounters.products4) is left in counts[8..9] (set afresh by every call).  The caller
  * reads plan->counts when it next synchronises; counts[2] != 0 means a capacity was too small
  * (nothing was computed) and the call must be repeated with larger buffers.
  * plan_ws (spamm_plan_workspace_bytes() bytes) must be ALL ZERO when the call is enqueued and is

@@ -25,7 +25,7 @@ class TreeView(C.Structure):
 
     _fields_ = [("m", i32), ("n", i32), ("depth", i32), ("nleaf", i32),
                 ("keys", vp), ("values", vp), ("values_t", vp),
-                ("slot", vp), ("slot_t", vp), ("norm", vp), ("norm_t", vp)]
+                ("slot", vp), ("slot_t", vp), ("norm", vp), ("norm_t", vp), ("sub", vp), ("sub_t", vp)]
 
 
 class PlanBuffers(C.Structure):
@@ -72,6 +72,7 @@ SIGNATURES = {
     "spamm_transpose_records": (C.c_int, [vp, i64, vp, vp]),
     "spamm_sparsify_leaves": (C.c_int, [vp, vp, vp, i64, C.c_float, vp, vp]),
     "spamm_index_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp]),
+    "spamm_subrange_grids": (C.c_int, [vp, vp, C.c_int, vp, vp, vp]),
     "spamm_to_dense": (C.c_int, [C.POINTER(TreeView), vp, i64, vp]),
     "spamm_plan_workspace_bytes": (sz, [C.c_int, i64, i64]),
     "spamm_plan": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, i32, i32,
@@ -79,6 +80,8 @@ SIGNATURES = {
     "spamm_plan_row_counts": (C.c_int, [C.POINTER(PlanBuffers), C.c_int, vp, vp]),
     "spamm_execute": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), C.POINTER(PlanBuffers), i64, i64,
                                 f64, f32, C.c_int, C.c_int, vp, vp, vp, vp, vp]),
+    "spamm_execute_gates": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), C.POINTER(PlanBuffers), i64, i64,
+                                      f64, vp, vp, vp, vp, vp, vp]),
     "spamm_multiply": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, C.c_int, C.c_int, f32, i32, i32,
                                  C.POINTER(PlanBuffers), vp, sz, C.POINTER(ProductBuffers), vp]),
     "spamm_multiply_arena_layout": (C.c_int, [C.c_int, C.c_int, i64, i64, C.POINTER(ArenaLayout)]),
@@ -104,7 +107,7 @@ def lib():
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
-        if handle.spamm_abi_version() != 1:
+        if handle.spamm_abi_version() != 2:
             raise RuntimeError("libspamm_b200.so ABI version mismatch; rebuild it")
         _lib = handle
     return _lib

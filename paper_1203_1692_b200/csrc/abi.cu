@@ -18,6 +18,17 @@ bool spamm_pdl_enabled()
     return on;
 }
 
+int spamm_num_sms()
+{
+    static const int sms = [] {
+        int dev = 0, n = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1)
+            n = 148;      // B200
+        return n;
+    }();
+    return sms;
+}
+
 extern "C" int64_t spamm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 extern "C" int spamm_abi_version(void) { return SPAMM_ABI_VERSION; }

@@ -10,7 +10,9 @@
 #define SPAMM_LEAF 256
 #define SPAMM_REC 272              // floats per stored leaf: 256 values + 16 sub-block norms
 #define SPAMM_REC_BYTES 1088
-#define SPAMM_NUM_SMS 148
+// SMs of the current device (queried once per process, abi.cu); grids are sized in multiples of it
+int spamm_num_sms();
+#define SPAMM_NUM_SMS (spamm_num_sms())
 
 // ---- launch bookkeeping -----------------------------------------------------
 extern "C" int64_t spamm_launch_count(void);
@@ -162,9 +164,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity)
         : "memory");
     return ok != 0;
 }
+// try_wait with a suspend-time hint: the warp sleeps in hardware until the phase completes or the
+// hint (ns) expires, instead of coming back to the issue stage every few dozen cycles.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t *bar, uint32_t parity, uint32_t ns)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
-    while (!mbar_try_wait(bar, parity)) {
+    if (mbar_try_wait(bar, parity)) return;
+    while (!mbar_try_wait_hint(bar, parity, 20000u)) {
     }
 }
 // 1-D bulk copy global -> shared, completion counted on an mbarrier (SASS: UBLKCP).
@@ -297,4 +314,78 @@ __device__ __forceinline__ void lb_exclusive(volatile unsigned long long *state,
     ex_hi = hi;
     __threadfence();
     state[tile] = lb_pack(LB_PREFIX, lo + agg_lo, hi + agg_hi);
+}
+
+// ---- the same for ONE 62-bit counter (task totals exceed 31 bits) ----------------------------------
+// 64-bit word: [63:62] status, [61:0] counter.  The tile's aggregate is published first with
+// lb64_publish (so that several look-backs of one tile can be in flight together), then
+// lb64_exclusive_warp waits for the predecessors.
+#define LB64_MASK 0x3FFFFFFFFFFFFFFFull
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
+{
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+    return v;
+}
+// one lane of the tile
+__device__ __forceinline__ void lb64_publish(volatile unsigned long long *state, int tile, unsigned long long agg)
+{
+    __threadfence();
+    state[tile] = ((tile == 0 ? LB_PREFIX : LB_AGGREGATE) << 62) | (agg & LB64_MASK);
+}
+// one warp of the tile, all lanes, after lb64_publish: exclusive prefix in every lane
+__device__ __forceinline__ unsigned long long lb64_exclusive_warp(volatile unsigned long long *state, int tile,
+                                                                  unsigned long long agg)
+{
+    const uint32_t lane = threadIdx.x & 31u;
+    if (tile == 0) return 0ull;
+    unsigned long long sum = 0ull;
+    for (int base = tile - 1; base >= 0; base -= 32) {
+        const int idx = base - (int)lane;
+        unsigned long long w = LB_PREFIX << 62;
+        if (idx >= 0) {
+            do {
+                w = state[idx];
+            } while (lb_status(w) == LB_INVALID);
+        }
+        const uint32_t pref = __ballot_sync(0xFFFFFFFFu, lb_status(w) == LB_PREFIX);
+        const uint32_t take = pref ? ((2u << (__ffs(pref) - 1)) - 1u) : 0xFFFFFFFFu;
+        sum += warp_sum_u64(((take >> lane) & 1u) ? (w & LB64_MASK) : 0ull);
+        if (pref) break;
+    }
+    if (lane == 0) {
+        __threadfence();
+        state[tile] = (LB_PREFIX << 62) | ((sum + agg) & LB64_MASK);
+    }
+    return sum;
+}
+// at most 128 tiles, all resident (see all_exclusive_warp): aggregates only, read in one batch
+__device__ __forceinline__ unsigned long long all64_exclusive_warp(volatile unsigned long long *state, int tile)
+{
+    const int lane = (int)(threadIdx.x & 31u);
+    unsigned long long w[4];
+    bool need[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+        need[x] = lane + 32 * x < tile;
+        w[x] = 0ull;
+    }
+    bool again;
+    do {
+        again = false;
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+            if (need[x]) w[x] = state[lane + 32 * x];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+            if (need[x]) {
+                if (lb_status(w[x]) == LB_INVALID) again = true;
+                else need[x] = false;
+            }
+    } while (__any_sync(0xFFFFFFFFu, again));
+    unsigned long long s = 0ull;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+        if (lane + 32 * x < tile) s += w[x] & LB64_MASK;
+    return warp_sum_u64(s);
 }

@@ -14,11 +14,16 @@
 // producer warp stages each block with ONE bulk copy (TMA 1-D, cp.async.bulk, SASS UBLKCP; up to
 // 17 KB: 16 leaf records of 1088 B holding values and sub-block norms) into a ring of
 // shared-memory stages guarded by mbarriers.  Eight consumer warps (two product leaves each)
-// gate and multiply from shared memory; with fine4 a tenth warp first classifies the tasks of each
-// stage (all 64 micro products run / none / undecided).  The persistent CTAs (two per SM) claim work
-// units from an atomic counter: whole super-tiles, or -- when the product has few of them -- chained
-// segments of a super-tile's records whose accumulators pass from CTA to CTA through C's value
-// records (plan_format.cuh, spamm_b200.h).  Launched with programmatic dependent launch.
+// gate and multiply from shared memory; with fine4 the planner has already classified most tasks from
+// the sub-norm ranges of their leaves (all 64 micro products run / none / undecided, spamm_step.live
+// and .dead), so only band-edge tasks pay for per-lane gate arithmetic.  The persistent CTAs (two per SM) run a
+// STATIC partition of the record stream that the planner cut into pieces of equal weight, one per SM
+// (plan.cu, plan_order_kernel); a piece is whole super-tiles plus at most one head and one tail
+// segment of a tile shared with the neighbouring piece, whose accumulators pass from CTA to CTA
+// through C's value records (spamm_b200.h).  The CTAs resident on one SM find each other through
+// %smid and share the SM's piece tile by tile (a compare-and-swap cursor per piece): two CTAs on an SM
+// do not advance equally, SMs do, so all SMs finish together without a global hand-out counter.
+// Launched with programmatic dependent launch.
 // Tuning aids: SPAMM_EX_STAGES, SPAMM_EX_CTAS, SPAMM_EX_DEBUG, SPAMM_EX_TRACE (per-CTA time stamps).
 #include <stdio.h>
 #include <stdlib.h>
@@ -28,8 +33,7 @@
 
 #define EX_MAX_STAGES 6
 #define EX_CONSUMERS 8
-#define EX_THREADS (32 * (EX_CONSUMERS + 1))          // coarse16: consumers + producer
-#define EX_THREADS_FINE (32 * (EX_CONSUMERS + 2))     // fine4: + the classifier warp
+#define EX_THREADS (32 * (EX_CONSUMERS + 1))          // consumers + producer
 #define EX_EXIT (1u << 31)
 #define EX_CHAIN_IN (1u << 30)    // first step of a later segment: accumulators come from C's records
 #define EX_CHAIN_OUT (1u << 29)   // last step of a segment that is not the tile's last: hand them on
@@ -44,23 +48,22 @@ struct __align__(16) StageDesc {
     uint32_t a_present;    // stored leaves of the staged A block, bit morton4(di,kk)
     uint32_t b_present;    // stored leaves of the staged B block, bit morton4(kk,dj)
     uint32_t tile;         // Morton index of the super-tile
-    uint32_t seg;          // segment of the tile this step belongs to
+    uint32_t rec;          // index of the record in the plan
     uint32_t pad;
-    // fine4, written by the classifier warp: tasks whose 64 micro products all run / none runs,
-    // bit morton4(di,dj) + 16 * (kk & 1) of word kk >> 1
-    uint32_t full[2];
-    uint32_t dead[2];
+    uint32_t dead[2];      // fine4: live tasks none of whose micro products runs (spamm_step.dead)
+    uint32_t pad2[2];
 };
 
 struct ExecArgs {
     const float *a_values_t;
     const float *b_values;
     const spamm_step *steps;
-    const int32_t *tile_off;     // step offset of every super-tile node, one extra entry
-    const int32_t *tile_order;   // work units (node | segment << 24) in hand-out order
-    const int32_t *counts;       // plan counts (device): [5] = number of units, [12] = records per segment
-    int32_t *chain;              // finished segments per product leaf (zeroed before the launch)
-    unsigned int *tile_counter;
+    const int32_t *pieces;       // plan.tile_order: (b, mb, me, e) per piece, see plan_order_kernel
+    int32_t *cursor;             // per piece: how far its jobs (head segment, tiles, tail segment) are handed out
+    const int32_t *counts;       // plan counts (device): [5] = number of pieces
+    int32_t *chain;              // per product leaf: the record up to which its partial sums are handed on (0 = none)
+    unsigned int *xs;            // ExecShared: piece tickets, exited CTAs, per-SM tables; zero between launches
+    int xs_early;                // xs is not touched by the preceding kernel: the SM's CTAs pair up before waiting for it
     double tau;
     float alpha;
     int alpha_is_one;
@@ -75,13 +78,31 @@ struct ExecArgs {
     int c_L;                     // side of C's leaf grid
     int sub2;                    // leaves per super-tile (16; 4 or 1 for tiny trees)
     int nstages;                 // depth of the shared-memory ring
-    int static_first;            // every CTA of the grid is resident: CTA b may take unit b without asking
     int32_t *error_flag;         // plan counts[15]: set when a hand-over wait gives up (never in a correct run)
     uint32_t *clean_ptr;         // the planner's shared state, returned to zero here on behalf of the planner
     int clean_words;             // (spamm_multiply; 0 otherwise)
+    unsigned long long *gates;   // optional (spamm_execute_gates): the 64 gate bits of every task as evaluated HERE
     int dbg;                     // tuning aid (SPAMM_EX_DEBUG): 1 = no copies, 2 = no math
     unsigned long long *trace;   // tuning aid (SPAMM_EX_TRACE): per CTA start / first data / end / units
 };
+
+// ExecShared (uint32 words): [0] piece tickets drawn, [1] CTAs that have run out of work,
+// [2 .. 258) CTAs arrived per SM, [258 .. 514) the piece (+ 1) the CTAs of an SM currently share
+#define XS_TICKET 0
+#define XS_EXITED 1
+#define XS_ARRIVE 2
+#define XS_PIECE 258
+#define XS_WORDS 514
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int *p)
+{
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned int *p, unsigned int v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ unsigned long long global_timer()
 {
@@ -118,7 +139,7 @@ template <bool EXACT, bool FINE>
 #ifndef EX_MIN_BLOCKS
 #define EX_MIN_BLOCKS 2
 #endif
-__global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel(ExecArgs g)
+__global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(ExecArgs g)
 {
     // dynamic shared memory: nstages x (A block + B block), then descriptors and barriers
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -128,21 +149,42 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
     StageDesc *desc = reinterpret_cast<StageDesc *>(smem_raw + (size_t)nstages * 2 * EX_BLOCK_BYTES);
     uint64_t *full_bar = reinterpret_cast<uint64_t *>(desc + EX_MAX_STAGES);
     uint64_t *empty_bar = full_bar + EX_MAX_STAGES;
-    uint64_t *ready_bar = empty_bar + EX_MAX_STAGES;      // fine4: the stage's tasks are classified
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
-    pdl_enter();
-    if (blockIdx.x == 0)
-        for (int x = threadIdx.x; x < g.clean_words; x += blockDim.x) g.clean_ptr[x] = 0u;
+    // everything that does not depend on the preceding kernel comes before the wait for it
     if (threadIdx.x == 0) {
         for (int s = 0; s < nstages; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], EX_CONSUMERS);
-            mbar_init(&ready_bar[s], 1);
         }
         fence_barrier_init();
     }
+    // The CTAs of one SM share a piece.  The first to arrive on an SM draws a piece ticket and
+    // publishes it in the SM's table entry; the others read it there.  Tickets are drawn in order, and
+    // whoever draws a piece starts with its head segment, so the CTA that later waits for that head
+    // (the tail of the next piece, run last) waits for a running CTA: no assumption about residency.
+    uint32_t smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    smid &= 255u;
+    int piece = 0;
+    auto pair_up = [&]() {
+        if (lane == 0) {
+            if (atomicAdd(g.xs + XS_ARRIVE + smid, 1u) == 0u) {
+                piece = (int)atomicAdd(g.xs + XS_TICKET, 1u);
+                st_release_u32(g.xs + XS_PIECE + smid, (unsigned int)piece + 1u);
+            } else {
+                unsigned int v;
+                while ((v = ld_acquire_u32(g.xs + XS_PIECE + smid)) == 0u) __nanosleep(64);
+                piece = (int)v - 1;
+            }
+        }
+        piece = __shfl_sync(FULL_MASK, piece, 0);
+    };
+    if (warp == EX_CONSUMERS && g.xs_early) pair_up();
+    pdl_enter();
+    if (blockIdx.x == 0)
+        for (int x = threadIdx.x; x < g.clean_words; x += blockDim.x) g.clean_ptr[x] = 0u;
     __syncthreads();
     int stage = 0;
     uint32_t phase = 0;
@@ -150,149 +192,132 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
 
     if (warp == EX_CONSUMERS) {
         // ============ producer: stream step records, stage leaf blocks with bulk copies ============
-        // the first unit is read together with the counts (tile_order always has room for one entry per CTA)
-        uint32_t unit_pre = (uint32_t)__ldg(g.tile_order + blockIdx.x);
-        const int ntiles = g.counts[2] ? 0 : g.counts[5];      // an overflowed plan is incomplete: do nothing
-        const int seg_len = g.counts[12];
-        const bool claim_late = ntiles < 16 * (int)gridDim.x;
+        if (!g.xs_early) pair_up();
+        const int npieces = g.counts[2] ? 0 : g.counts[5];      // an overflowed plan is incomplete: do nothing
         const uint32_t *words = reinterpret_cast<const uint32_t *>(g.steps);
-        int tile = 0, units_done = 0;
-        // With the whole grid resident the first unit needs no hand-out: CTA b takes unit b, the counter
-        // hands out the rest.  (Otherwise a unit could wait for a predecessor owned by a CTA that has
-        // not started yet, so every unit is claimed.)
-        tile = (int)blockIdx.x;
-        if (!g.static_first) {
-            if (lane == 0) tile = (int)atomicAdd(g.tile_counter, 1u);
-            tile = __shfl_sync(FULL_MASK, tile, 0);
-        }
-        const int claim_base = g.static_first ? (int)gridDim.x : 0;
-        while (tile < ntiles) {
-            ++units_done;
-            const uint32_t unit = unit_pre;
-            const int node = seg_len ? (int)(unit & ((1u << UNIT_NODE_BITS) - 1u)) : (int)unit;
-            const int seg = seg_len ? (int)((unit >> UNIT_NODE_BITS) & 63u) : 0;
-            int beg = g.tile_off[node], end = g.tile_off[node + 1];
-            bool chain_in = false, chain_out = false;
-            if (seg_len) {      // this unit is one segment of the tile
-                const int ns = end - beg, nseg = (int)(unit >> 26);
-                end = beg + unit_begin(ns, nseg, seg + 1);
-                beg = beg + unit_begin(ns, nseg, seg);
-                chain_in = seg > 0;
-                chain_out = seg + 1 < nseg;
+        const int4 *pieces = reinterpret_cast<const int4 *>(g.pieces);
+        int4 pd = make_int4(0, 0, 0, 0);
+        if (piece < npieces) pd = __ldg(pieces + piece);
+        // Jobs of a piece, in hand-out order: the head segment [me, e), the whole tiles of [mb, me) one by
+        // one, the tail segment [b, mb).  The cursor counts handed-out records in that order.  claim():
+        // the next job of the SM's piece -- or of the piece the SM moves on to -- as records [jb, je).
+        int jb = 0, je = 0, units_done = 0;
+        auto claim = [&]() -> bool {
+            for (;;) {
+                if (piece >= npieces) return false;
+                int got = 0;
+                if (lane == 0) {
+                    const int h = pd.w - pd.z, t = pd.z - pd.y, tl = pd.y - pd.x, total = h + t + tl;
+                    for (;;) {
+                        const int v = ld_acquire_gpu(g.cursor + piece);
+                        if (v >= total) { got = 0; break; }
+                        int nv;
+                        if (v < h) { nv = h; jb = pd.z; je = pd.w; }
+                        else if (v < h + t) {
+                            const int r0 = pd.y + (v - h);
+                            int len = (int)__ldg(words + (size_t)r0 * 16 + 15);      // records of this tile
+                            if (len < 1) len = 1;
+                            if (r0 + len > pd.z) len = pd.z - r0;
+                            nv = v + len; jb = r0; je = r0 + len;
+                        } else { nv = total; jb = pd.x; je = pd.y; }
+                        if (atomicCAS(g.cursor + piece, v, nv) == v) { got = 1; break; }
+                    }
+                }
+                got = __shfl_sync(FULL_MASK, got, 0);
+                if (got) {
+                    jb = __shfl_sync(FULL_MASK, jb, 0);
+                    je = __shfl_sync(FULL_MASK, je, 0);
+                    return true;
+                }
+                // the piece is handed out: join the piece the SM's other CTAs moved on to, or draw the next
+                if (lane == 0) {
+                    const unsigned int cur = ld_acquire_u32(g.xs + XS_PIECE + smid);
+                    if (cur != (unsigned int)piece + 1u) {
+                        piece = (int)cur - 1;
+                    } else {
+                        const int np = (int)atomicAdd(g.xs + XS_TICKET, 1u);
+                        atomicCAS(g.xs + XS_PIECE + smid, (unsigned int)piece + 1u, (unsigned int)np + 1u);
+                        piece = np;      // mine in any case; if the entry had moved meanwhile, I rejoin it afterwards
+                    }
+                }
+                piece = __shfl_sync(FULL_MASK, piece, 0);
+                if (piece < npieces) pd = __ldg(pieces + piece);
             }
-            // With few units per CTA the next unit is claimed late, two records before the
-            // end of this one: its latency still hides behind the staged records, and a CTA never sits
-            // on a whole unit it has not started while others run dry.  With many whole tiles it is
-            // claimed right away.
-            int next_tile = 0;
-            if (lane == 0 && !claim_late) next_tile = (int)atomicAdd(g.tile_counter, 1u) + claim_base;
-            // lane l < 16 holds word l of a record (struct spamm_step)
-            uint32_t w[EX_PREFETCH];
-#pragma unroll
-            for (int x = 0; x < EX_PREFETCH; ++x)
-                w[x] = (lane < 16 && beg + x < end) ? __ldg(words + (size_t)(beg + x) * 16 + lane) : 0u;
-            for (int r = beg; r < end; ++r) {
-                if (lane == 0 && claim_late && (r + 2 == end || (r == beg && r + 2 > end)))
-                    next_tile = (int)atomicAdd(g.tile_counter, 1u) + claim_base;
-                const uint32_t cur = w[0];
-#pragma unroll
-                for (int x = 0; x + 1 < EX_PREFETCH; ++x) w[x] = w[x + 1];
-                w[EX_PREFETCH - 1] =
-                    (lane < 16 && r + EX_PREFETCH < end) ? __ldg(words + (size_t)(r + EX_PREFETCH) * 16 + lane) : 0u;
-                const uint32_t na = __popc(__shfl_sync(FULL_MASK, cur, 5));
-                const uint32_t nb = __popc(__shfl_sync(FULL_MASK, cur, 7));
-                mbar_wait(&empty_bar[stage], phase ^ 1u);
-                uint32_t *d = reinterpret_cast<uint32_t *>(&desc[stage]);
-                if (lane == 1)                                   // flags
-                    d[4] = cur | (chain_in && r == beg ? EX_CHAIN_IN : 0u) | (chain_out && r + 1 == end ? EX_CHAIN_OUT : 0u);
-                if (lane == 13) d[10] = (uint32_t)seg;
-                if (lane == 2) d[5] = cur;                       // c_base
-                if (lane == 12) d[6] = cur;                      // present
-                if (lane == 3) d[9] = cur;                       // tile
-                if (lane == 5) d[7] = cur;                       // a_present
-                if (lane == 7) d[8] = cur;                       // b_present
-                if (lane >= 8 && lane < 12) d[lane - 8] = cur;   // live[kk]
-                __syncwarp();
-                const bool copy = !(g.dbg & 1);
-                if (lane == 0) mbar_arrive_expect_tx(&full_bar[stage], copy ? (na + nb) * SPAMM_REC_BYTES : 0u);
-                __syncwarp();
-                if (copy && lane == 4)
-                    bulk_copy_g2s(sA + (size_t)stage * EX_BLOCK_BYTES, g.a_values_t + (size_t)cur * SPAMM_REC,
-                                  na * SPAMM_REC_BYTES, &full_bar[stage]);
-                if (copy && lane == 6)
-                    bulk_copy_g2s(sB + (size_t)stage * EX_BLOCK_BYTES, g.b_values + (size_t)cur * SPAMM_REC,
-                                  nb * SPAMM_REC_BYTES, &full_bar[stage]);
-                if (++stage == nstages) { stage = 0; phase ^= 1u; }
+        };
+        // cursor over the records of my jobs.  The next job is claimed two records before the cursor
+        // leaves the current one: the claim's latency hides behind the staged records, and no CTA sits
+        // on a job it has not started while its neighbour runs dry.
+        int r = 0, rend = 0, rbeg = 0, nb = 0, ne = 0;
+        bool have_next = false, dry = false, more = true;
+        // fetch: the next record of the cursor -> (word of lane l < 16, meta); meta = rec | first << 30 | last << 31, ~0 = none
+        auto fetch = [&](uint32_t &wd, uint32_t &meta) {
+            for (;;) {
+                if (!more) { wd = 0u; meta = 0xFFFFFFFFu; return; }
+                if (!have_next && !dry && rend - r <= 2) {
+                    have_next = claim();
+                    dry = !have_next;
+                    nb = jb; ne = je;
+                }
+                if (r < rend) break;
+                if (!have_next) { more = false; continue; }
+                r = rbeg = nb; rend = ne;
+                have_next = false;
+                ++units_done;
             }
-            tile = __shfl_sync(FULL_MASK, next_tile, 0);
-            if (tile < ntiles) unit_pre = (uint32_t)g.tile_order[tile];
+            wd = lane < 16 ? __ldg(words + (size_t)r * 16 + lane) : 0u;
+            meta = (uint32_t)r | (r == rbeg ? (1u << 30) : 0u) | (r + 1 == rend ? (1u << 31) : 0u);
+            ++r;
+        };
+        uint32_t w[EX_PREFETCH], m[EX_PREFETCH];
+#pragma unroll
+        for (int x = 0; x < EX_PREFETCH; ++x) fetch(w[x], m[x]);
+        while (m[0] != 0xFFFFFFFFu) {
+            const uint32_t cur = w[0], meta = m[0];
+#pragma unroll
+            for (int x = 0; x + 1 < EX_PREFETCH; ++x) { w[x] = w[x + 1]; m[x] = m[x + 1]; }
+            fetch(w[EX_PREFETCH - 1], m[EX_PREFETCH - 1]);
+            const uint32_t na = __popc(__shfl_sync(FULL_MASK, cur, 5));
+            const uint32_t nb = __popc(__shfl_sync(FULL_MASK, cur, 7));
+            mbar_wait(&empty_bar[stage], phase ^ 1u);
+            uint32_t *d = reinterpret_cast<uint32_t *>(&desc[stage]);
+            if (lane == 1) {                                 // flags: a run that starts or ends inside a tile is chained
+                uint32_t f = cur;
+                if ((meta >> 30 & 1u) && !(cur & STEP_FIRST)) f |= EX_CHAIN_IN;
+                if ((meta >> 31 & 1u) && !(cur & STEP_LAST)) f |= EX_CHAIN_OUT;
+                d[4] = f;
+            }
+            if (lane == 15) d[10] = meta & 0x3FFFFFFFu;      // record index
+            if (lane == 13 || lane == 14) d[lane - 1] = cur; // dead[0..1]
+            if (lane == 2) d[5] = cur;                       // c_base
+            if (lane == 12) d[6] = cur;                      // present
+            if (lane == 3) d[9] = cur;                       // tile
+            if (lane == 5) d[7] = cur;                       // a_present
+            if (lane == 7) d[8] = cur;                       // b_present
+            if (lane >= 8 && lane < 12) d[lane - 8] = cur;   // live[kk]
+            __syncwarp();
+            const bool copy = !(g.dbg & 1);
+            if (lane == 0) mbar_arrive_expect_tx(&full_bar[stage], copy ? (na + nb) * SPAMM_REC_BYTES : 0u);
+            __syncwarp();
+            if (copy && lane == 4)
+                bulk_copy_g2s(sA + (size_t)stage * EX_BLOCK_BYTES, g.a_values_t + (size_t)cur * SPAMM_REC,
+                              na * SPAMM_REC_BYTES, &full_bar[stage]);
+            if (copy && lane == 6)
+                bulk_copy_g2s(sB + (size_t)stage * EX_BLOCK_BYTES, g.b_values + (size_t)cur * SPAMM_REC,
+                              nb * SPAMM_REC_BYTES, &full_bar[stage]);
+            if (++stage == nstages) { stage = 0; phase ^= 1u; }
         }
         mbar_wait(&empty_bar[stage], phase ^ 1u);
         if (lane == 0) {
             desc[stage].flags = EX_EXIT;
             mbar_arrive(&full_bar[stage]);
             if (g.trace) g.trace[blockIdx.x * 4 + 3] = (unsigned long long)units_done;
-            // the last CTA to run out of units leaves both counters at zero for the next launch
-            if (atomicAdd(g.tile_counter + 1, 1u) == gridDim.x - 1) {
-                g.tile_counter[0] = 0u;
-                g.tile_counter[1] = 0u;
-            }
         }
-        return;
-    }
-
-    if (FINE && warp == EX_CONSUMERS + 1) {
-        // ============ classifier warp (fine4) ============
-        // Most tasks away from the band edge run all 64 micro products, and some run none.  Both
-        // cases follow from the extreme sub-block norms of the two leaves: min(subA) * min(subB) >= tau
-        // means every product passes the gate, max(subA) * max(subB) < tau means none does (products
-        // of non-negative floats are exact in double and monotone).  Lane l finds the extremes of
-        // staged leaf l (A block: lanes 0..15, B block: 16..31); consumers then skip the per-lane
-        // gate arithmetic for classified tasks.  A NaN sub-norm leaves the task unclassified.
-        for (;;) {
-            mbar_wait(&full_bar[stage], phase);
-            StageDesc &ds = desc[stage];
-            if (ds.flags & EX_EXIT) {
-                if (lane == 0) mbar_arrive(&ready_bar[stage]);
-                break;
-            }
-            const uint32_t a_present = ds.a_present, b_present = ds.b_present;
-            const uint32_t mine_present = lane < 16 ? a_present : b_present;
-            const float *blk = reinterpret_cast<const float *>((lane < 16 ? sA : sB) + (size_t)stage * EX_BLOCK_BYTES);
-            float mn = 0.0f, mx = 0.0f;
-            bool bad = true;
-            if ((lane & 15u) < (uint32_t)__popc(mine_present) && !(g.dbg & 1)) {
-                const float4 *tl = reinterpret_cast<const float4 *>(blk + (lane & 15u) * SPAMM_REC + 256);
-                const float4 t0 = tl[0], t1 = tl[1], t2 = tl[2], t3 = tl[3];
-                mn = fminf(fminf(fminf(t0.x, t0.y), fminf(t0.z, t0.w)), fminf(fminf(t1.x, t1.y), fminf(t1.z, t1.w)));
-                mn = fminf(mn, fminf(fminf(fminf(t2.x, t2.y), fminf(t2.z, t2.w)), fminf(fminf(t3.x, t3.y), fminf(t3.z, t3.w))));
-                mx = fmaxf(fmaxf(fmaxf(t0.x, t0.y), fmaxf(t0.z, t0.w)), fmaxf(fmaxf(t1.x, t1.y), fmaxf(t1.z, t1.w)));
-                mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(t2.x, t2.y), fmaxf(t2.z, t2.w)), fmaxf(fmaxf(t3.x, t3.y), fmaxf(t3.z, t3.w))));
-                const float sum = ((t0.x + t0.y) + (t0.z + t0.w)) + ((t1.x + t1.y) + (t1.z + t1.w)) +
-                                  ((t2.x + t2.y) + (t2.z + t2.w)) + ((t3.x + t3.y) + (t3.z + t3.w));
-                bad = !(sum == sum) || !(sum - sum == 0.0f);      // a NaN or an infinity among the 16 norms
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int kk = 2 * h + (int)(lane >> 4), pos = (int)(lane & 15u);
-                const int gi = step_pos_di(pos), gj = step_pos_dj(pos);
-                const int ia = __popc(a_present & ((1u << step_pos(gi, kk)) - 1u));
-                const int ib = 16 + __popc(b_present & ((1u << step_pos(kk, gj)) - 1u));
-                const float mna = __shfl_sync(FULL_MASK, mn, ia), mnb = __shfl_sync(FULL_MASK, mn, ib);
-                const float mxa = __shfl_sync(FULL_MASK, mx, ia), mxb = __shfl_sync(FULL_MASK, mx, ib);
-                const int bad_a = __shfl_sync(FULL_MASK, (int)bad, ia), bad_b = __shfl_sync(FULL_MASK, (int)bad, ib);
-                const bool unk = (bad_a | bad_b) != 0;       // both shuffles unconditionally: all lanes take part
-                const bool full = !unk && __dmul_rn((double)mna, (double)mnb) >= g.tau;
-                const bool dead = !unk && __dmul_rn((double)mxa, (double)mxb) < g.tau;
-                const uint32_t fb = __ballot_sync(FULL_MASK, full), db = __ballot_sync(FULL_MASK, dead);
-                if (lane == 0) {
-                    ds.full[h] = fb;
-                    ds.dead[h] = db;
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&ready_bar[stage]);
-            if (++stage == nstages) { stage = 0; phase ^= 1u; }
+        // the last CTA to run out of work leaves the shared state and the cursors at zero for the next launch
+        int last = 0;
+        if (lane == 0) last = atomicAdd(g.xs + XS_EXITED, 1u) == gridDim.x - 1 ? 1 : 0;
+        if (__shfl_sync(FULL_MASK, last, 0)) {
+            for (int x = (int)lane; x < npieces; x += 32) g.cursor[x] = 0;
+            for (int x = (int)lane; x < XS_WORDS; x += 32) g.xs[x] = 0u;
         }
         return;
     }
@@ -310,8 +335,9 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
     uint32_t executed = 0;
     float2 acc2[2][4];     // acc2[h][j] = C sub-block elements (2h, j) and (2h+1, j)
     bool traced = false;
+    bool chained = false;  // the sums of the current tile came (partly) from another CTA
     for (;;) {
-        mbar_wait(FINE ? &ready_bar[stage] : &full_bar[stage], phase);
+        mbar_wait(&full_bar[stage], phase);
         const StageDesc &ds = desc[stage];
         const uint32_t flags = ds.flags;
         if (g.trace && threadIdx.x == 0 && !traced) {
@@ -320,20 +346,22 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
         }
         if (flags & EX_EXIT) break;
         if (flags & STEP_FIRST) {
+            chained = false;
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc2[h][j] = make_float2(0.0f, 0.0f);
         } else if (flags & EX_CHAIN_IN) {
+            chained = true;
             // continue a tile another CTA started: wait for its segment, then take the partial sums
             // from C's value record (written below under EX_CHAIN_OUT); L1 is bypassed
             const uint32_t present_in = ds.present;
             if ((present_in >> mypos) & 1u) {
                 const int64_t cs = (int64_t)ds.c_base + __popc(present_in & ((1u << mypos) - 1u));
-                const int want = (int)ds.seg;
-                // the predecessor was handed out earlier to a running CTA; the bound only turns a
-                // scheduling bug into an error flag instead of a hang
-                for (unsigned spins = 0; ld_acquire_gpu(g.chain + cs) < want; ++spins) {
+                const int want = (int)ds.rec;      // the records before this one are in the partial sums
+                // the predecessor belongs to a CTA that started earlier and runs it first; the bound
+                // only turns a scheduling bug into an error flag instead of a hang
+                for (unsigned spins = 0; ld_acquire_gpu(g.chain + cs) != want; ++spins) {
                     __nanosleep(40);
                     if (spins > (1u << 25)) {
                         if (g.error_flag) *g.error_flag = 1;
@@ -356,14 +384,17 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
         const float *Ablk = reinterpret_cast<const float *>(sA + (size_t)stage * EX_BLOCK_BYTES);
         const float *Bblk = reinterpret_cast<const float *>(sB + (size_t)stage * EX_BLOCK_BYTES);
         const uint4 live4 = *reinterpret_cast<const uint4 *>(ds.live);
-        uint32_t cls_full[2] = {0u, 0u}, cls_dead[2] = {0u, 0u};
+        uint32_t dead01 = 0u, dead23 = 0u;
         if (FINE) {
-            cls_full[0] = ds.full[0]; cls_full[1] = ds.full[1];
-            cls_dead[0] = ds.dead[0]; cls_dead[1] = ds.dead[1];
+            dead01 = ds.dead[0];
+            dead23 = ds.dead[1];
         }
 #pragma unroll     // all four k unrolled: +4-5 % (their addresses become constants), measured
         for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t live = kk == 0 ? live4.x : kk == 1 ? live4.y : kk == 2 ? live4.z : live4.w;
+            const uint32_t lw = kk == 0 ? live4.x : kk == 1 ? live4.y : kk == 2 ? live4.z : live4.w;
+            // fine4: a task the planner found dead runs no micro product (and counts none)
+            const uint32_t dead = FINE ? ((kk < 2 ? dead01 : dead23) >> (16 * (kk & 1))) : 0u;
+            const uint32_t live = lw & 0xFFFFu & ~dead;
             if (!((live >> (2 * warp)) & 3u) || (g.dbg & 2)) continue;
             const bool mine = (live >> mypos) & 1u;
             // leaf (r,c) of a block sits at index popc(present & below(morton4(r,c)))
@@ -371,10 +402,9 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
             const float *Bs = Bblk + __popc(b_present & ((1u << step_pos(kk, dj)) - 1u)) * SPAMM_REC;
             uint32_t on = 0;       // bit r: micro product (p,q,r) of my task runs
             if (FINE) {
-                const uint32_t cbit = 1u << (mypos + 16 * (kk & 1));
-                if (mine && (cls_full[kk >> 1] & cbit)) {
+                if (mine && ((lw >> (16 + mypos)) & 1u)) {
                     on = 15u;
-                } else if (mine && !(cls_dead[kk >> 1] & cbit)) {
+                } else if (mine) {
                     const float4 sa = *reinterpret_cast<const float4 *>(As + 256 + 4 * p);   // subA[p][0..3]
                     const float4 sb = *reinterpret_cast<const float4 *>(Bs + 256 + 4 * q);   // subB[0..3][q]
                     on |= (__dmul_rn((double)sa.x, (double)sb.x) >= g.tau) ? 1u : 0u;
@@ -383,6 +413,14 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
                     on |= (__dmul_rn((double)sa.w, (double)sb.w) >= g.tau) ? 8u : 0u;
                 }
                 executed += __popc(on);
+                if (g.gates && ((lw >> mypos) & 1u)) {
+                    // evidence for the tests: bit r*16 + p*4 + q of the task's word (numeric.py:233-238)
+                    unsigned long long bits = 0ull;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        if ((on >> r) & 1u) bits |= 1ull << (r * 16 + t16);
+                    if (bits) atomicOr(g.gates + ((size_t)ds.rec * 64 + kk * 16 + mypos), bits);
+                }
             } else {
                 on = mine ? 15u : 0u;
             }
@@ -442,7 +480,7 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
             c_base = ds.c_base;
             tile_id = ds.tile;
             present = ds.present;
-            seg_done = ds.seg + 1u;
+            seg_done = ds.rec + 1u;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[stage]);
@@ -508,7 +546,7 @@ __global__ void __launch_bounds__(EX_THREADS_FINE, EX_MIN_BLOCKS) execute_kernel
             cv[256 + q * 4 + p] = sn;
             ct[256 + t16] = sn;
             if (t16 == 0) {
-                if (seg_done > 1u) g.chain[cslot] = 0;      // last reader of the flag: leave it clear
+                if (chained) g.chain[cslot] = 0;            // last reader of the flag: leave it clear
                 g.c_leaf_sq[cslot] = tot;
                 if (g.c_slot) {
                     uint32_t ci, cj;
@@ -537,6 +575,7 @@ int spamm_execute_grid()
     static const ExecTuning tune = exec_tuning();
     return SPAMM_NUM_SMS * tune.ctas_per_sm;
 }
+int spamm_execute_piece_base() { return SPAMM_NUM_SMS; }
 static ExecTuning exec_tuning()
 {
     ExecTuning t{3, 2, 0};
@@ -552,7 +591,8 @@ static ExecTuning exec_tuning()
 int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const spamm_plan_buffers *plan,
                        int64_t nsteps, int64_t nC, double tau, float alpha, int granularity, int exact,
                        float *c_values, float *c_values_t, double *c_leaf_sq, unsigned long long *counters,
-                       const spamm_product_buffers *cgrid, uint32_t *clean_ptr, int clean_words, void *stream)
+                       const spamm_product_buffers *cgrid, uint32_t *clean_ptr, int clean_words, void *stream,
+                       unsigned long long *gates = nullptr)
 {
     if (!a || !b || !plan || nsteps < -1 || nC < -1) return SPAMM_EINVAL;
     if (granularity != SPAMM_FINE4 && granularity != SPAMM_COARSE16) return SPAMM_EINVAL;
@@ -562,14 +602,20 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     g.a_values_t = a->values_t;
     g.b_values = b->values;
     g.steps = plan->steps;
-    g.tile_off = plan->tile_off;
-    g.tile_order = plan->tile_order;
+    g.pieces = plan->tile_order;
+    const int64_t piece_cap = spamm_piece_capacity(plan->leaf_capacity);
+    g.cursor = plan->tile_order + 4 * piece_cap;
     g.counts = plan->counts;
-    g.tile_counter = reinterpret_cast<unsigned int *>(plan->counts + 13);   // [13] hand-out, [14] exited CTAs
+    // the kernel's shared state: in the planner's workspace when the call comes from spamm_multiply
+    // (untouched by the preceding kernel, so the CTAs of an SM can pair up early), else behind the
+    // plan's cursors
+    g.xs = clean_ptr ? clean_ptr + clean_words : reinterpret_cast<unsigned int *>(plan->tile_order + 5 * piece_cap);
+    g.xs_early = clean_ptr ? 1 : 0;
     g.chain = plan->chain;
     g.error_flag = plan->counts + 15;
     g.clean_ptr = clean_ptr;
     g.clean_words = clean_words;
+    g.gates = gates;
     g.tau = tau;
     g.alpha = alpha;
     g.alpha_is_one = (alpha == 1.0f);
@@ -600,7 +646,7 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     g.nstages = tune.stages;
     g.dbg = tune.dbg;
     const int grid = SPAMM_NUM_SMS * tune.ctas_per_sm;
-    const size_t smem = (size_t)tune.stages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 24);
+    const size_t smem = (size_t)tune.stages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16);
     const bool fine = granularity == SPAMM_FINE4;
     void (*kern)(ExecArgs) = exact ? (fine ? execute_kernel<true, true> : execute_kernel<true, false>)
                                    : (fine ? execute_kernel<false, true> : execute_kernel<false, false>);
@@ -609,20 +655,7 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     static const char *trace_path = getenv("SPAMM_EX_TRACE");     // tuning aid: allocates and synchronises
     if (trace_path && cudaMalloc(&g.trace, sizeof(unsigned long long) * 4 * grid) != cudaSuccess) g.trace = nullptr;
     if (g.trace) cudaMemsetAsync(g.trace, 0, sizeof(unsigned long long) * 4 * grid, st);
-    {
-        // is the whole persistent grid resident at once on this device?
-        static int resident[4] = {-1, -1, -1, -1};
-        const int which = (exact ? 2 : 0) + (fine ? 1 : 0);
-        if (resident[which] < 0) {
-            int dev = 0, sms = 0, per_sm = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fine ? EX_THREADS_FINE : EX_THREADS, smem);
-            resident[which] = (long long)per_sm * sms >= grid ? 1 : 0;
-        }
-        g.static_first = resident[which];
-    }
-    if (spamm_launch_pdl(kern, dim3(grid), dim3(fine ? EX_THREADS_FINE : EX_THREADS), smem, st, g) != cudaSuccess)
+    if (spamm_launch_pdl(kern, dim3(grid), dim3(EX_THREADS), smem, st, g) != cudaSuccess)
         return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
     if (g.trace) {
@@ -647,6 +680,19 @@ extern "C" int spamm_execute(const spamm_tree_view *a, const spamm_tree_view *b,
 {
     return spamm_execute_impl(a, b, plan, nsteps, nC, tau, alpha, granularity, exact, c_values, c_values_t, c_leaf_sq,
                               counters, nullptr, nullptr, 0, stream);
+}
+
+// The same run, additionally reporting the gate the kernel evaluated: gates[(record * 64) + kk * 16 +
+// morton4(di,dj)] |= the 64 bits (r*16 + p*4 + q) of that task's micro products that ran.  `gates`
+// holds 64 words per step record and must be zero when the call is enqueued.  Test evidence for the
+// device-side gate (numeric.py:233-238); not used by the product path.
+extern "C" int spamm_execute_gates(const spamm_tree_view *a, const spamm_tree_view *b, const spamm_plan_buffers *plan,
+                                   int64_t nsteps, int64_t nC, double tau, float *c_values, float *c_values_t,
+                                   double *c_leaf_sq, unsigned long long *counters, unsigned long long *gates, void *stream)
+{
+    if (!gates) return SPAMM_EINVAL;
+    return spamm_execute_impl(a, b, plan, nsteps, nC, tau, 1.0f, SPAMM_FINE4, 0, c_values, c_values_t, c_leaf_sq, counters,
+                              nullptr, nullptr, 0, stream, gates);
 }
 
 // ---- beta != 0: union of the old and the produced leaf sets, then _compose ----------------------

@@ -9,13 +9,15 @@
 
 int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
                     const spamm_plan_buffers *out, void *ws, size_t ws_bytes, bool prezeroed,
-                    const spamm_product_buffers *cgrid, uint32_t **clean_ptr, int *clean_words, void *stream);
+                    const spamm_product_buffers *cgrid, uint32_t **clean_ptr, int *clean_words, int fine_weight,
+                    void *stream);
 int spamm_launch_interior(const double *leaf_sq, int depth, float *norm, float *norm_t, double *sq_levels,
                           unsigned int *ticket, cudaStream_t st);
 int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const spamm_plan_buffers *plan,
                        int64_t nsteps, int64_t nC, double tau, float alpha, int granularity, int exact,
                        float *c_values, float *c_values_t, double *c_leaf_sq, unsigned long long *counters,
-                       const spamm_product_buffers *cgrid, uint32_t *clean_ptr, int clean_words, void *stream);
+                       const spamm_product_buffers *cgrid, uint32_t *clean_ptr, int clean_words, void *stream,
+                       unsigned long long *gates = nullptr);
 
 extern "C" int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity, int exact,
                               float alpha, int32_t row0, int32_t row1, const spamm_plan_buffers *plan, void *plan_ws,
@@ -30,7 +32,7 @@ extern "C" int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b
     uint32_t *clean_ptr = nullptr;      // planner state the numeric kernel returns to zero
     int clean_words = 0;
     int rc = spamm_plan_impl(a, b, tau, row0, row1, plan, plan_ws, plan_ws_bytes, true, c, stop == 2 ? nullptr : &clean_ptr,
-                             stop == 2 ? nullptr : &clean_words, stream);
+                             stop == 2 ? nullptr : &clean_words, granularity == SPAMM_FINE4 ? 1 : 0, stream);
     if (rc != SPAMM_OK || stop == 2) return rc;
     // executed micro products are counted in plan->counts[8..9]
     rc = spamm_execute_impl(a, b, plan, -1, -1, tau, alpha, granularity, exact, c->values, c->values_t, c->leaf_sq,

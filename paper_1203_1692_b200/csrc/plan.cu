@@ -20,9 +20,11 @@
 // so the compacted task list comes out already in the order and grouping the numeric phase
 // consumes: ascending k per product leaf (numeric.py:203-217), leaves in Morton order.
 // For n <= 8192 the walk starts densely at the super-tile level (one kernel, no coarser levels).
-// A last kernel sorts the super-tiles into work units for the numeric kernel (longest first, the
-// last ones cut into chained segments), empties C's leaf grids, publishes the counts and returns
-// the workspace to all-zero, so a sequence of plans on one stream needs no memset.
+// A last kernel cuts the record stream into pieces of equal weight for the persistent CTAs of the
+// numeric kernel (a static partition: no hand-out counter, no uneven finish), empties C's leaf grids,
+// publishes the counts and returns the workspace to all-zero, so a sequence of plans on one stream
+// needs no memset.
+#include <stddef.h>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -39,7 +41,6 @@ struct LevelBuf {
     uint32_t *ks;     // contraction indices
 };
 
-#define PLAN_BINS 1024       // super-tiles are binned by their number of step records
 #define PLAN_DENSE_MAX_LEVEL 7   // up to 128 x 128 super-tiles (n <= 8192) the walk starts densely at the tile level
 
 // Lives at the start of the workspace.  The workspace prefix (this struct and the look-back states
@@ -50,8 +51,8 @@ struct PlanShared {
     unsigned int order_ticket;
     unsigned int tile_counter[PLAN_MAX_LEVELS + 1];
     int32_t counts[PLAN_MAX_LEVELS + 1][2];   // (nodes, candidates) per level
-    unsigned int bins[PLAN_BINS];             // histogram of super-tile sizes
-    unsigned int cursor[PLAN_BINS];
+    unsigned int exec_shared[EXEC_SHARED_WORDS];   // the numeric kernel's shared state (ExecShared, execute.cu) when
+                                                   // it runs inside spamm_multiply: zero between launches
 };
 
 // ---- start level: dense enumeration by one block ---------------------------------------
@@ -281,13 +282,16 @@ __device__ __forceinline__ unsigned long long plan_timer()
 
 struct TileArgs {
     unsigned long long *trace;   // tuning aid (SPAMM_PLAN_TRACE): per block 6 timestamps
-    int32_t *tile_class;         // size class of every super-tile node (scratch for the order kernel)
+    unsigned long long *tile_wprefix;   // tasks in the super-tile nodes before each node (one extra entry: all)
+    volatile unsigned long long *tile_state_w;   // look-back states of that prefix
     int all_resident;            // every block of the grid is resident at once (one per SM on this device)
-    int flat_order;              // experiment (SPAMM_ORDER_FLAT): one size class, i.e. hand-out in about Morton order
     const float *norm_a;      // leaf level grid of A, row-major (i,k)
     const float *norm_bt;     // leaf level grid of B transposed (j,k)
     const int32_t *slot_a;    // leaf slots of A (i,k)
     const int32_t *slot_bt;   // leaf slots of B transposed (j,k)
+    const uint32_t *sub_a;    // sub-norm ranges of A's leaves (i,k), see spamm_tree_view.sub; NULL: no classification
+    const uint32_t *sub_bt;   // the same for B, transposed (j,k)
+    int fine_weight;          // balance the numeric kernel's pieces for fine4 gating: dead tasks weigh nothing
     const float *norm_a_t;    // super-tile level grids (dense start only)
     const float *norm_bt_t;
     int St;                   // side of the super-tile level
@@ -300,7 +304,6 @@ struct TileArgs {
     spamm_step *steps;
     uint32_t *c_keys;
     int32_t *tile_off;
-    unsigned int *bins;
     int64_t cap_steps, cap_leaves;
     int32_t *counts;          // plan counts, see spamm_b200.h
     unsigned int *tile_counter;
@@ -313,9 +316,12 @@ struct LaneTests {
     uint32_t live;       // bit morton4(di,dj): task (sub*I+di, k, sub*J+dj) survives
     uint32_t a_here;     // bit di: leaf A(sub*I+di, k) stored
     uint32_t b_here;     // bit dj: leaf B(k, sub*J+dj) stored
+    uint32_t full;       // live tasks whose 64 gated micro products all pass (fine4, numeric.py:233-238)
+    uint32_t dead;       // live tasks of which none passes
 };
 
-struct LaneNorms { float na[4], nb[4]; };      // leaf norms of A(sub*I+d, k) and B(k, sub*J+d); -1 = absent
+// leaf norms of A(sub*I+d, k) and B(k, sub*J+d), -1 = absent; and their sub-norm range words
+struct LaneNorms { float na[4], nb[4]; uint32_t sa[4], sb[4]; };
 
 __device__ __forceinline__ LaneNorms tile_norms(const TileArgs &a, uint32_t I, uint32_t J, uint32_t k, bool valid)
 {
@@ -324,9 +330,14 @@ __device__ __forceinline__ LaneNorms tile_norms(const TileArgs &a, uint32_t I, u
     for (int d = 0; d < 4; ++d) {
         n.na[d] = -1.0f;
         n.nb[d] = -1.0f;
+        n.sa[d] = n.sb[d] = 0xFFFFFFFFu;
         if (valid && d < a.sub) {
             n.na[d] = __ldg(a.norm_a + (int64_t)(a.sub * I + d) * a.L + k);
             n.nb[d] = __ldg(a.norm_bt + (int64_t)(a.sub * J + d) * a.L + k);
+            if (a.sub_a) {
+                n.sa[d] = __ldg(a.sub_a + (int64_t)(a.sub * I + d) * a.L + k);
+                n.sb[d] = __ldg(a.sub_bt + (int64_t)(a.sub * J + d) * a.L + k);
+            }
         }
     }
     return n;
@@ -334,7 +345,7 @@ __device__ __forceinline__ LaneNorms tile_norms(const TileArgs &a, uint32_t I, u
 
 __device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, const LaneNorms &n, uint32_t rowok)
 {
-    LaneTests t{0u, 0u, 0u};
+    LaneTests t{0u, 0u, 0u, 0u, 0u};
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
         t.a_here |= (n.na[d] >= 0.0f) ? (1u << d) : 0u;
@@ -344,7 +355,18 @@ __device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, const LaneNor
     for (int di = 0; di < 4; ++di)
 #pragma unroll
         for (int dj = 0; dj < 4; ++dj)
-            if ((rowok >> di & 1u) && norm_test(n.na[di], n.nb[dj], a.tau)) t.live |= 1u << step_pos(di, dj);
+            if ((rowok >> di & 1u) && norm_test(n.na[di], n.nb[dj], a.tau)) {
+                t.live |= 1u << step_pos(di, dj);
+                if (a.sub_a) {
+                    // lower bounds of the smallest, upper bounds of the largest sub-norm of either leaf
+                    // (NaN for a leaf that cannot be classified: every comparison is then false)
+                    const float mna = __uint_as_float(n.sa[di] << 16), mxa = __uint_as_float(n.sa[di] & 0xFFFF0000u);
+                    const float mnb = __uint_as_float(n.sb[dj] << 16), mxb = __uint_as_float(n.sb[dj] & 0xFFFF0000u);
+                    if (norm_test(mna, mnb, a.tau)) t.full |= 1u << step_pos(di, dj);
+                    else if (mxa >= 0.0f && mxb >= 0.0f && __dmul_rn((double)mxa, (double)mxb) < a.tau)
+                        t.dead |= 1u << step_pos(di, dj);
+                }
+            }
     return t;
 }
 
@@ -357,8 +379,9 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
 {
     pdl_enter();
     __shared__ int s_tile;
-    __shared__ uint32_t s_wsteps[TILE_WARPS], s_wleaves[TILE_WARPS];
+    __shared__ uint32_t s_wsteps[TILE_WARPS], s_wleaves[TILE_WARPS], s_wtasks[TILE_WARPS];
     __shared__ uint32_t s_base_lo, s_base_hi;
+    __shared__ unsigned long long s_base_w;
     __shared__ uint32_t s_ks[DENSE ? TILE_WARPS : 1][DENSE ? (1 << PLAN_DENSE_MAX_LEVEL) : 1];
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
@@ -410,15 +433,19 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
         }
         if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 2] = plan_timer();
         // phase 1: count step records and product leaves of this super-tile
-        uint32_t nsteps = 0, present = 0, ntasks = 0;
+        uint32_t nsteps = 0, present = 0, ntasks = 0, nheavy = 0;
         // the norms of the next pass are fetched before the tests of the current one
         LaneNorms nrm = tile_norms(a, I, J, (s + (int)lane / sub < e) ? sub * ks[s + (int)lane / sub] + kk : 0u,
                                    s + (int)lane / sub < e);
         for (int b = s; b < e; b += per) {
             const int t = b + (int)lane / sub, t2 = t + per;
             const LaneNorms nxt = tile_norms(a, I, J, t2 < e ? sub * ks[t2] + kk : 0u, t2 < e);
-            uint32_t live = 0;
-            if (t < e) live = tile_tests(a, nrm, rowok).live;
+            uint32_t live = 0, heavy = 0;
+            if (t < e) {
+                const LaneTests tt = tile_tests(a, nrm, rowok);
+                live = tt.live;
+                heavy = a.fine_weight ? (tt.live & ~tt.dead) : tt.live;
+            }
             nrm = nxt;
             const uint32_t bal = __ballot_sync(FULL_MASK, live != 0);
             // one record per group of `sub` lanes with any live task
@@ -429,37 +456,46 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
             nsteps += __popc(groups);
             present |= live;
             ntasks += __popc(live);
+            nheavy += __popc(heavy);
         }
         present = __reduce_or_sync(FULL_MASK, present);
         ntasks = __reduce_add_sync(FULL_MASK, ntasks);
+        nheavy = __reduce_add_sync(FULL_MASK, nheavy);
         const uint32_t nleaves = __popc(present);
         if (lane == 0) {
-            s_wsteps[warp] = nsteps; s_wleaves[warp] = nleaves; tasks_total += ntasks;
-            if (valid) {
-                const int cls = a.flat_order ? (nsteps ? 8 : 0) : tile_size_class((int)nsteps, (int)ntasks);
-                a.tile_class[pidx] = cls;
-                atomicAdd(&a.bins[cls], 1u);
-            }
+            s_wsteps[warp] = nsteps; s_wleaves[warp] = nleaves; s_wtasks[warp] = nheavy; tasks_total += ntasks;
         }
         __syncthreads();
         if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 3] = plan_timer();
         // phase 2: block scan + look-back over (records, product leaves)
         if (warp == 0) {
             uint32_t vs = lane < TILE_WARPS ? s_wsteps[lane] : 0u, vl = lane < TILE_WARPS ? s_wleaves[lane] : 0u;
-            uint32_t is = vs, il = vl;          // inclusive scan over the block's warps
+            uint32_t vt = lane < TILE_WARPS ? s_wtasks[lane] : 0u;
+            uint32_t is = vs, il = vl, it = vt;          // inclusive scan over the block's warps
 #pragma unroll
             for (int d = 1; d < TILE_WARPS; d <<= 1) {
                 const uint32_t xs = __shfl_up_sync(FULL_MASK, is, d), xl = __shfl_up_sync(FULL_MASK, il, d);
-                if (lane >= (uint32_t)d) { is += xs; il += xl; }
+                const uint32_t xt = __shfl_up_sync(FULL_MASK, it, d);
+                if (lane >= (uint32_t)d) { is += xs; il += xl; it += xt; }
             }
             const uint32_t rs = __shfl_sync(FULL_MASK, is, TILE_WARPS - 1), rl = __shfl_sync(FULL_MASK, il, TILE_WARPS - 1);
-            if (lane < TILE_WARPS) { s_wsteps[lane] = is - vs; s_wleaves[lane] = il - vl; }
+            const uint32_t rt = __shfl_sync(FULL_MASK, it, TILE_WARPS - 1);
+            if (lane < TILE_WARPS) { s_wsteps[lane] = is - vs; s_wleaves[lane] = il - vl; s_wtasks[lane] = it - vt; }
+            // both aggregates are published before either look-back waits
+            if (lane == 0) lb64_publish(a.tile_state_w, tile, (unsigned long long)rt);
             uint32_t ex_lo, ex_hi;
-            if (fixed_tiles && ntiles <= 128) all_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
-            else lb_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
+            unsigned long long ex_w;
+            if (fixed_tiles && ntiles <= 128) {
+                all_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
+                ex_w = all64_exclusive_warp(a.tile_state_w, tile);
+            } else {
+                lb_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
+                ex_w = lb64_exclusive_warp(a.tile_state_w, tile, (unsigned long long)rt);
+            }
             if (lane == 0) {
                 s_base_lo = ex_lo;
                 s_base_hi = ex_hi;
+                s_base_w = ex_w;
             }
             if (lane == 0 && tile == ntiles - 1) {
                 const int64_t tot_s = (int64_t)ex_lo + rs, tot_l = (int64_t)ex_hi + rl;
@@ -467,12 +503,16 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
                 a.counts[4] = (int32_t)tot_s;
                 a.counts[11] = n_nodes;
                 a.tile_off[n_nodes] = (int32_t)tot_s;
+                a.tile_wprefix[n_nodes] = ex_w + rt;
                 if (tot_s > a.cap_steps || tot_l > a.cap_leaves) a.counts[2] = 1;
             }
         }
         __syncthreads();
         if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 4] = plan_timer();
-        if (valid && lane == 0) a.tile_off[pidx] = (int32_t)(s_base_lo + s_wsteps[warp]);
+        if (valid && lane == 0) {
+            a.tile_off[pidx] = (int32_t)(s_base_lo + s_wsteps[warp]);
+            a.tile_wprefix[pidx] = s_base_w + s_wtasks[warp];
+        }
         if (!valid || nsteps == 0) continue;
         // phase 3: product leaf keys and step records, in ascending K
         int64_t sb = (int64_t)s_base_lo + s_wsteps[warp];
@@ -490,7 +530,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
         for (int b = s; b < e; b += per) {
             const int t = b + (int)lane / sub, t2 = t + per;
             const LaneNorms nxt = tile_norms(a, I, J, t2 < e ? sub * ks[t2] + kk : 0u, t2 < e);
-            LaneTests lt4{0u, 0u, 0u};
+            LaneTests lt4{0u, 0u, 0u, 0u, 0u};
             uint32_t K = 0;
             if (t < e) {
                 K = ks[t];
@@ -498,18 +538,20 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
             }
             nrm = nxt;
             // gather the group's four lanes: live per kk, stored leaves of both blocks
-            uint32_t live4[4] = {0, 0, 0, 0}, a_present = 0, b_present = 0, any = 0;
+            uint32_t live4[4] = {0, 0, 0, 0}, dead4[4] = {0, 0, 0, 0}, a_present = 0, b_present = 0, any = 0;
             // first stored leaf of each block in Morton order and the lane that knows its slot
             int a_best = 16, b_best = 16;
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
                 const int src = (int)grp + (x < sub ? x : 0);
-                const uint32_t lv = __shfl_sync(FULL_MASK, lt4.live, src);
+                const uint32_t lv = __shfl_sync(FULL_MASK, lt4.live | (lt4.full << 16), src);
+                const uint32_t dd = __shfl_sync(FULL_MASK, lt4.dead, src);
                 const uint32_t ah = __shfl_sync(FULL_MASK, lt4.a_here, src);
                 const uint32_t bh = __shfl_sync(FULL_MASK, lt4.b_here, src);
                 if (x < sub) {
                     live4[x] = lv;
-                    any |= lv;
+                    dead4[x] = dd;
+                    any |= lv & 0xFFFFu;
 #pragma unroll
                     for (int d = 0; d < 4; ++d) {
                         if (ah >> d & 1u) { a_present |= 1u << step_pos(d, x); }     // A leaf (di=d, kk=x)
@@ -533,7 +575,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
                 rec[0] = make_uint4(K, flags, (uint32_t)cb, pm);
                 rec[1] = make_uint4(a_first, a_present, b_first, b_present);
                 rec[2] = make_uint4(live4[0], live4[1], live4[2], live4[3]);
-                rec[3] = make_uint4(present, 0u, 0u, 0u);
+                rec[3] = make_uint4(present, dead4[0] | (dead4[1] << 16), dead4[2] | (dead4[3] << 16), nsteps);
             }
             sb += __popc(bal & lead_mask);
         }
@@ -543,18 +585,31 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
     if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 5] = plan_timer();
 }
 
-// Longest-first order of the super-tiles for the numeric kernel's dynamic scheduler: a counting
-// sort by step count (any order inside a bin; the product does not depend on it).
+// Partition of the record stream for the numeric kernel.  The records (tile after tile, in Morton
+// order) are cut into P pieces of equal weight (live tasks + rec_weight per record), one per SM (or a
+// few rounds of them for a large product, so that the SMs work on neighbouring super-tiles at any time
+// and share operand blocks in L2).  A piece is the four record indices (b, mb, me, e): [mb, me) are
+// whole super-tiles, [me, e) is the head of a tile that the next piece finishes (run FIRST, its
+// accumulators are handed on through C's value records), [b, mb) is the tail of a tile the previous
+// piece began (run LAST, when its head is long finished).  A piece inside a single tile has
+// mb = me = e.  The CTAs that are resident on one SM share one piece, tile by tile, through the piece's
+// cursor (execute.cu): two CTAs on an SM do not advance equally, SMs do.  The thread that looks at a
+// tile places the cuts that fall into it: cut g is the first record boundary at which the weight
+// prefix reaches g W / P.
 struct OrderArgs {
     const int32_t *tile_off;
-    const int32_t *tile_class;    // size class per node, from the tiles kernel
+    const unsigned long long *tile_wprefix;
+    const spamm_step *steps;
     int defer_clean;              // the caller's next kernel clears PlanShared (spamm_multiply)
     int32_t *counts;              // the caller's plan counts: written here, all SPAMM_PLAN_COUNTS of them
     PlanShared *shared;
     uint32_t *ws_tail;            // workspace prefix behind PlanShared (look-back states), left zero
     int64_t ws_tail_words;
-    int32_t *tile_order;
-    int unit_target, min_seg, grid_ctas;
+    int32_t *pieces;              // plan.tile_order: 4 ints per piece, then one cursor per piece, then the
+                                  // numeric kernel's shared state (EXEC_SHARED_WORDS, zero between launches)
+    int64_t piece_capacity;
+    int num_sms, piece_records, rec_weight;
+    int fine_weight;              // dead tasks (fine4 classification) weigh nothing
     int32_t *chain;
     int64_t leaf_capacity;
     // optional: C's leaf grids, emptied here for the numeric kernel's epilogue to fill
@@ -568,10 +623,6 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
 {
     const int32_t *__restrict__ tile_off = a.tile_off;
     int32_t *counts = a.shared->res;
-    const unsigned int *__restrict__ bins = a.shared->bins;
-    unsigned int *cursor = a.shared->cursor;
-    int32_t *__restrict__ tile_order = a.tile_order;
-    const int unit_target = a.unit_target, min_seg = a.min_seg, grid_ctas = a.grid_ctas;
     int32_t *__restrict__ chain = a.chain;
     const int64_t leaf_capacity = a.leaf_capacity;
     __shared__ bool s_last;
@@ -590,82 +641,72 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
             a.leaf_sq_grid[x] = 0.0;
         }
     }
-    __shared__ unsigned int s_start[PLAN_BINS];
-    __shared__ unsigned int s_base[256];
-    __shared__ unsigned int s_part[256];
-    // exclusive scan of the bins in DESCENDING size order: 4 bins per thread
     const int t = threadIdx.x;
-    unsigned int v[4], sum = 0;
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-        v[x] = bins[PLAN_BINS - 1 - (4 * t + x)];
-        sum += v[x];
+    const int n_nodes = counts[2] ? 0 : counts[11];
+    const long long R = counts[2] ? 0 : counts[4];
+    const unsigned long long T = a.tile_wprefix[counts[11]];
+    const unsigned long long RW = (unsigned long long)a.rec_weight;
+    const unsigned long long W = T + RW * (unsigned long long)R;
+    // pieces: one per SM, or several rounds of them when the product is large
+    long long rounds = R / ((long long)a.num_sms * a.piece_records);
+    if (rounds < 1) rounds = 1;
+    if (rounds > 64) rounds = 64;
+    if (rounds * a.num_sms > a.piece_capacity) rounds = a.piece_capacity / a.num_sms;
+    const long long P = R > 0 ? (rounds >= 1 ? rounds * a.num_sms : a.piece_capacity) : 0;
+    int32_t *__restrict__ pw = a.pieces;
+    // weight prefix at which cut g is placed (at least 1, so that every cut falls into some tile)
+    auto target_of = [&](long long g) -> unsigned long long {
+        const unsigned long long x = (unsigned long long)((unsigned __int128)g * W / (unsigned long long)P);
+        return x < 1ull ? 1ull : x;
+    };
+    // cursors and the numeric kernel's shared state start at zero
+    for (int64_t x = gtid; x < P; x += gsz) pw[4 * a.piece_capacity + x] = 0;
+    for (int64_t x = gtid; x < EXEC_SHARED_WORDS; x += gsz) pw[5 * a.piece_capacity + x] = 0;
+    if (gtid == 0 && P > 0) {
+        pw[0] = 0;                       // unit 0 begins at record 0, on a tile start
+        pw[1] = 0;
+        pw[4 * (P - 1) + 2] = (int32_t)R;   // the last unit ends with the last record, on a tile end
+        pw[4 * (P - 1) + 3] = (int32_t)R;
     }
-    unsigned int inc = sum;                 // block exclusive scan: warp shuffles + 8 warp totals
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned int y = __shfl_up_sync(FULL_MASK, inc, d);
-        if ((t & 31) >= d) inc += y;
-    }
-    if ((t & 31) == 31) s_part[t >> 5] = inc;
-    __syncthreads();
-    unsigned int run = inc - sum;
-    for (int w = 0; w < (t >> 5); ++w) run += s_part[w];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-        s_start[PLAN_BINS - 1 - (4 * t + x)] = run;
-        run += v[x];
-    }
-    __syncthreads();
-    // Work units.  With many more super-tiles than CTAs every tile is one unit.  Otherwise the tiles
-    // handed out last (the shortest ones, ranks >= whole) are cut into segments of about seg_len
-    // records so that the CTAs of the numeric kernel run dry together; the longer tiles, handed out
-    // first, stay whole (a hand-over costs about a third of a record).  Segment s >= 1 of the cut
-    // tiles follows segment s - 1 of all of them, so unit (tile, s) sits at s_base[s] + rank - whole.
-    const int n_nodes = counts[11];
-    const int n_tiles = n_nodes - (int)bins[0];
-    const int total_steps = counts[4];
-    int seg_len = 0, whole = 0;
-    if (unit_target > 0 && n_tiles > grid_ctas && n_tiles < unit_target && n_nodes <= (1 << UNIT_NODE_BITS)) {
-        seg_len = (total_steps + unit_target - 1) / unit_target;
-        if (seg_len < min_seg) seg_len = min_seg;
-        whole = grid_ctas * (n_tiles / grid_ctas - 1);
-    }
-    unsigned int cnt = 0;                   // cut tiles with more than t segments (t = 0: all tiles)
-    if (t == 0) cnt = (unsigned int)n_tiles;
-    else if (seg_len && t < UNIT_MAX_SEGMENTS && (long long)t * seg_len <= UNIT_SIZE_CLAMP) {
-        const int longer = (int)s_start[t * seg_len * 8 + 7];  // tiles with more than t * seg_len records
-        cnt = longer > whole ? (unsigned int)(longer - whole) : 0u;
-    }
-    __syncthreads();                        // s_part is reused
-    unsigned int inc2 = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const unsigned int y = __shfl_up_sync(FULL_MASK, inc2, d);
-        if ((t & 31) >= d) inc2 += y;
-    }
-    if ((t & 31) == 31) s_part[t >> 5] = inc2;
-    __syncthreads();
-    unsigned int base = inc2 - cnt;
-    for (int w = 0; w < (t >> 5); ++w) base += s_part[w];
-    s_base[t] = base;
-    __shared__ int s_units;
-    if (t == 255) s_units = (int)(base + cnt);      // work units the numeric kernel hands out
-    __syncthreads();
-    for (int idx = blockIdx.x * blockDim.x + t; idx < n_nodes; idx += gridDim.x * blockDim.x) {
-        const int ns = tile_off[idx + 1] - tile_off[idx];
-        if (ns == 0) continue;
-        const int bin = a.tile_class[idx];
-        const int rank = (int)(s_start[bin] + atomicAdd(&cursor[bin], 1u));
-        if (!seg_len) {
-            tile_order[rank] = idx;
-            continue;
+    for (int idx = (int)gtid; idx < n_nodes && P > 1; idx += (int)gsz) {
+        const int ts = tile_off[idx], te = tile_off[idx + 1];
+        if (te == ts) continue;
+        const unsigned long long w0 = a.tile_wprefix[idx] + RW * (unsigned long long)ts;
+        const unsigned long long w1 = a.tile_wprefix[idx + 1] + RW * (unsigned long long)te;
+        // cuts g with w0 < target(g) <= w1 fall into this tile
+        long long g = (long long)((unsigned __int128)w0 * (unsigned long long)P / W);
+        if (g < 1) g = 1;
+        while (g < P && target_of(g) <= w0) ++g;
+        if (g >= P || target_of(g) > w1) continue;
+        unsigned long long acc = w0;
+        bool prev_here = false;
+        for (int r = ts; r < te && g < P; ++r) {
+            const uint4 live = *(reinterpret_cast<const uint4 *>(a.steps + r) + 2);
+            uint32_t d01 = 0u, d23 = 0u;
+            if (a.fine_weight) {
+                const uint4 tail = *(reinterpret_cast<const uint4 *>(a.steps + r) + 3);
+                d01 = tail.y;
+                d23 = tail.z;
+            }
+            acc += RW + __popc(live.x & 0xFFFFu & ~d01) + __popc(live.y & 0xFFFFu & ~(d01 >> 16)) +
+                   __popc(live.z & 0xFFFFu & ~d23) + __popc(live.w & 0xFFFFu & ~(d23 >> 16));
+            while (g < P) {
+                if (target_of(g) > acc) break;
+                const int c = r + 1;
+                const bool clean = c == te;
+                pw[4 * g + 0] = c;                     // b of unit g
+                pw[4 * g + 1] = clean ? c : te;        // mb of unit g (overridden below if it ends in this tile)
+                pw[4 * (g - 1) + 3] = c;               // e of unit g - 1
+                if (prev_here) {                       // unit g - 1 lies inside this tile: one segment
+                    pw[4 * (g - 1) + 1] = c;
+                    pw[4 * (g - 1) + 2] = c;
+                } else {
+                    pw[4 * (g - 1) + 2] = clean ? c : ts;
+                }
+                prev_here = true;
+                ++g;
+            }
         }
-        // hand-out order: first segments of the cut tiles, the whole tiles, then the later segments
-        // (whose predecessors are then long finished)
-        const int nseg = rank >= whole ? unit_segments(ns, seg_len) : 1;
-        tile_order[rank >= whole ? rank - whole : n_tiles - whole + rank] = (int32_t)unit_pack(idx, 0, nseg);
-        for (int sgm = 1; sgm < nseg; ++sgm) tile_order[s_base[sgm] + rank - whole] = (int32_t)unit_pack(idx, sgm, nseg);
     }
     if (a.defer_clean) {
         // the numeric kernel that follows returns the shared planner state to zero (its first block,
@@ -673,8 +714,8 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
         if (blockIdx.x == 0 && t < SPAMM_PLAN_COUNTS) {
             int32_t v = 0;
             if (t == 0 || t == 2 || t == 3 || t == 4 || t == 6 || t == 7 || t == 11) v = counts[t];
-            if (t == 5) v = s_units;
-            if (t == 12) v = seg_len;
+            if (t == 5) v = (int32_t)P;
+            if (t == 12) v = (int32_t)rounds;
             a.counts[t] = v;
         }
         return;
@@ -689,8 +730,8 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
     if (t < SPAMM_PLAN_COUNTS) {
         int32_t v = 0;
         if (t == 0 || t == 2 || t == 3 || t == 4 || t == 6 || t == 7 || t == 11) v = counts[t];
-        if (t == 5) v = s_units;
-        if (t == 12) v = seg_len;
+        if (t == 5) v = (int32_t)P;
+        if (t == 12) v = (int32_t)rounds;
         a.counts[t] = v;
     }
     __syncthreads();
@@ -699,7 +740,7 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
 }
 
 // ---- host side ---------------------------------------------------------------------------------
-int spamm_execute_grid();     // CTAs of the numeric kernel (execute.cu)
+int spamm_execute_piece_base();     // pieces per round = SMs that run the numeric kernel (execute.cu)
 
 static int plan_env(const char *name, int dflt, int lo, int hi)
 {
@@ -712,6 +753,8 @@ static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; 
 struct PlanWorkspace {
     PlanShared *shared;
     unsigned long long *tile_state[PLAN_MAX_LEVELS + 1];   // per parent level
+    unsigned long long *tile_state_w;                      // second look-back of the last stage (task prefix)
+    unsigned long long *tile_wprefix;                      // tasks before each super-tile node
     LevelBuf buf[2];
     size_t zero_bytes;                // prefix of the workspace that must be cleared per plan
     size_t total;
@@ -730,7 +773,11 @@ static PlanWorkspace carve(void *ws, int64_t list_cap, int64_t node_cap)
         w.tile_state[lvl] = reinterpret_cast<unsigned long long *>(p + o);
         o = align_up(o + sizeof(unsigned long long) * (size_t)((nodes + PLAN_WARPS - 1) / PLAN_WARPS + 1), 256);
     }
+    w.tile_state_w = reinterpret_cast<unsigned long long *>(p + o);
+    o = align_up(o + sizeof(unsigned long long) * (size_t)((node_cap + PLAN_WARPS - 1) / PLAN_WARPS + 1), 256);
     w.zero_bytes = o;
+    w.tile_wprefix = reinterpret_cast<unsigned long long *>(p + o);
+    o = align_up(o + sizeof(unsigned long long) * (size_t)(node_cap + 2), 256);
     for (int x = 0; x < 2; ++x) {
         w.buf[x].node = reinterpret_cast<uint32_t *>(p + o);
         o = align_up(o + 4 * (size_t)(node_cap + 1), 256);
@@ -788,7 +835,8 @@ size_t spamm_plan_zero_bytes(int64_t step_capacity, int64_t leaf_capacity)
 // prezeroed: the caller has already cleared that region and out->counts on the stream
 int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
                     const spamm_plan_buffers *out, void *ws, size_t ws_bytes, bool prezeroed,
-                    const spamm_product_buffers *cgrid, uint32_t **clean_ptr, int *clean_words, void *stream)
+                    const spamm_product_buffers *cgrid, uint32_t **clean_ptr, int *clean_words, int fine_weight,
+                    void *stream)
 {
     if (!a || !b || !out || !ws) return SPAMM_EINVAL;
     if (!(tau >= 0.0)) return SPAMM_EINVAL;                       // NaN or negative (symbolic.py:99-100)
@@ -846,6 +894,9 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     t.norm_bt = b->norm_t + spamm_level_offset(depth);
     t.slot_a = a->slot;
     t.slot_bt = b->slot_t;
+    t.sub_a = (a->sub && b->sub_t) ? a->sub : nullptr;
+    t.sub_bt = (a->sub && b->sub_t) ? b->sub_t : nullptr;
+    t.fine_weight = (fine_weight && t.sub_a) ? 1 : 0;
     t.L = 1 << depth;
     t.sub = 1 << (depth - tl);
     t.row0 = row0; t.row1 = row1; t.tau = tau;
@@ -862,11 +913,9 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
         }
         t.all_resident = sms >= tgrid ? 1 : 0;      // 1024 threads x 64 registers: one block per SM
     }
-    static const int flat_env = plan_env("SPAMM_ORDER_FLAT", 0, 0, 1);
-    t.flat_order = flat_env;
     t.tile_off = out->tile_off;
-    t.tile_class = reinterpret_cast<int32_t *>(w.buf[cur ^ 1].node);     // the level buffer not in use any more
-    t.bins = w.shared->bins;
+    t.tile_wprefix = w.tile_wprefix;
+    t.tile_state_w = w.tile_state_w;
     t.cap_steps = out->step_capacity; t.cap_leaves = out->leaf_capacity;
     t.counts = res;
     t.tile_counter = &w.shared->tile_counter[PLAN_MAX_LEVELS];
@@ -875,8 +924,10 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
                          dim3(tgrid), dim3(TILE_THREADS), 0, st, t) != cudaSuccess)
         return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
-    static const int unit_target = plan_env("SPAMM_UNIT_TARGET", 6 * 2 * SPAMM_NUM_SMS, 0, SPAMM_UNIT_EXTRA);
-    static const int min_seg = plan_env("SPAMM_UNIT_MIN_SEG", 2, 1, 1024);
+    // tuning aids: records per piece from which a product is cut into several rounds of pieces,
+    // and the weight of a record (in tasks) in the balance
+    static const int piece_records = plan_env("SPAMM_PIECE_RECORDS", 192, 1, 1 << 20);
+    static const int rec_weight = plan_env("SPAMM_REC_WEIGHT", 6, 1, 64);
     if (t.trace) {
         unsigned long long *h = (unsigned long long *)malloc(8 * 6 * tgrid);
         cudaStreamSynchronize(st);
@@ -894,10 +945,13 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     oa.defer_clean = (cgrid != nullptr && clean_words) ? 1 : 0;
     if (clean_words) {
         *clean_ptr = reinterpret_cast<uint32_t *>(w.shared);
-        *clean_words = oa.defer_clean ? (int)(sizeof(PlanShared) / 4) : 0;
+        // everything before exec_shared: the numeric kernel's CTAs use that part before they wait for
+        // this kernel, and its last CTA to exit leaves it zero
+        *clean_words = oa.defer_clean ? (int)(offsetof(PlanShared, exec_shared) / 4) : 0;
     }
     oa.tile_off = out->tile_off;
-    oa.tile_class = t.tile_class;
+    oa.tile_wprefix = w.tile_wprefix;
+    oa.steps = out->steps;
     oa.counts = out->counts;
     oa.shared = w.shared;
     {
@@ -905,8 +959,10 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
         oa.ws_tail = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(ws) + head);
         oa.ws_tail_words = (int64_t)((w.zero_bytes - head) / 4);
     }
-    oa.tile_order = out->tile_order;
-    oa.unit_target = unit_target; oa.min_seg = min_seg; oa.grid_ctas = spamm_execute_grid();
+    oa.pieces = out->tile_order;
+    oa.piece_capacity = spamm_piece_capacity(out->leaf_capacity);
+    oa.num_sms = spamm_execute_piece_base(); oa.piece_records = piece_records; oa.rec_weight = rec_weight;
+    oa.fine_weight = t.fine_weight;
     oa.chain = out->chain;
     oa.leaf_capacity = out->leaf_capacity;
     oa.cells = 0;
@@ -926,5 +982,6 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
 extern "C" int spamm_plan(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
                           const spamm_plan_buffers *out, void *ws, size_t ws_bytes, void *stream)
 {
-    return spamm_plan_impl(a, b, tau, row0, row1, out, ws, ws_bytes, false, nullptr, nullptr, nullptr, stream);
+    // balanced for the default granularity (fine4, numeric.py:36)
+    return spamm_plan_impl(a, b, tau, row0, row1, out, ws, ws_bytes, false, nullptr, nullptr, nullptr, 1, stream);
 }

@@ -511,6 +511,54 @@ extern "C" int spamm_transpose_records(const float *values, int64_t nleaf, float
     return SPAMM_OK;
 }
 
+// ---- sub-norm ranges (fine4 task classification in the planner) --------------------------------------
+// Per cell of the leaf grid one word: bf16(max sub-norm) rounded up in the high half, bf16(min
+// sub-norm) rounded down in the low half; 0xFFFFFFFF (two NaNs) for an absent leaf or one with a
+// non-finite sub-norm.  With these bounds the planner can tell for most tasks, without reading the
+// leaves, that all 64 gated micro products pass (min * min >= tau) or none does (max * max < tau):
+// products of non-negative floats are monotone in both factors (numeric.py:233-238 is the exact rule).
+__global__ void __launch_bounds__(256) subrange_kernel(const float *__restrict__ values,
+                                                       const int32_t *__restrict__ slot, int L,
+                                                       uint32_t *__restrict__ sub, uint32_t *__restrict__ sub_t)
+{
+    const int64_t cells = (int64_t)L * L;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < cells; x += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t s = slot[x];
+        uint32_t word = 0xFFFFFFFFu;
+        if (s >= 0) {
+            const float4 *tl = reinterpret_cast<const float4 *>(values + (int64_t)s * SPAMM_REC + 256);
+            const float4 t0 = tl[0], t1 = tl[1], t2 = tl[2], t3 = tl[3];
+            float mn = fminf(fminf(fminf(t0.x, t0.y), fminf(t0.z, t0.w)), fminf(fminf(t1.x, t1.y), fminf(t1.z, t1.w)));
+            mn = fminf(mn, fminf(fminf(fminf(t2.x, t2.y), fminf(t2.z, t2.w)), fminf(fminf(t3.x, t3.y), fminf(t3.z, t3.w))));
+            float mx = fmaxf(fmaxf(fmaxf(t0.x, t0.y), fmaxf(t0.z, t0.w)), fmaxf(fmaxf(t1.x, t1.y), fmaxf(t1.z, t1.w)));
+            mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(t2.x, t2.y), fmaxf(t2.z, t2.w)), fmaxf(fmaxf(t3.x, t3.y), fmaxf(t3.z, t3.w))));
+            const float sum = ((t0.x + t0.y) + (t0.z + t0.w)) + ((t1.x + t1.y) + (t1.z + t1.w)) +
+                              ((t2.x + t2.y) + (t2.z + t2.w)) + ((t3.x + t3.y) + (t3.z + t3.w));
+            const bool ok = (sum - sum == 0.0f) && mn >= 0.0f;      // no NaN, no infinity, nothing negative
+            if (ok) {
+                const uint32_t lo = __float_as_uint(mn) >> 16;                       // towards zero
+                const uint32_t hi = (__float_as_uint(mx) + 0xFFFFu) >> 16;           // away from zero
+                word = (hi << 16) | lo;
+            }
+        }
+        sub[x] = word;
+        const int64_t i = x / L, j = x - i * L;
+        sub_t[j * L + i] = word;
+    }
+}
+
+extern "C" int spamm_subrange_grids(const float *values, const int32_t *slot, int depth, uint32_t *sub, uint32_t *sub_t,
+                                    void *stream)
+{
+    if (!slot || !sub || !sub_t || depth < 0 || depth > 15) return SPAMM_EINVAL;
+    const int L = 1 << depth;
+    int64_t blocks = ((int64_t)L * L + 255) / 256;
+    if (blocks > SPAMM_NUM_SMS * 16) blocks = SPAMM_NUM_SMS * 16;
+    subrange_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(values, slot, L, sub, sub_t);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
+}
+
 // Grids of a tree given by packed leaves: clear, then scatter.
 __global__ void clear_grids_kernel(int64_t cells, int32_t *slot, int32_t *slot_t, float *norm, float *norm_t,
                                    double *leaf_sq_grid)

@@ -16,7 +16,7 @@ import torch
 
 from . import _lib
 from .symbolic import MultiplyPlan, build_plan
-from .tree import QuadtreeMatrix, _Span, _stream
+from .tree import QuadtreeMatrix, _Span, _stream, as_device_tree, write_back
 
 GRANULARITIES = ("fine4", "coarse16")
 
@@ -101,16 +101,21 @@ def _check_plan_handles(plan: MultiplyPlan, a: QuadtreeMatrix, b: QuadtreeMatrix
     if plan.n_tasks == 0:
         return
     if plan._tokens != (id(a), a._rev, id(b), b._rev):
-        for side, q, (ka, kb) in (("A", a, (0, 1)), ("B", b, (1, 2))):
-            have = set(q.leaf_keys().tolist()) if q.nleaf else set()
-            if not have:
+        for side, q in (("A", a), ("B", b)):
+            if q.nleaf == 0:
                 raise ValueError(f"plan references leaves but {side} has none (stale handles)")
         raise ValueError("plan was built for other operand revisions (stale handles); rebuild it with build_plan")
 
 
 def execute_plan(plan: MultiplyPlan, a: QuadtreeMatrix, b: QuadtreeMatrix, c: QuadtreeMatrix | None,
                  cfg: MultiplyConfig) -> tuple[QuadtreeMatrix, ExecCounters]:
-    """Run the numeric phase: C = alpha * (planned products) + beta * C (`numeric.py:138-181`)."""
+    """Run the numeric phase: C = alpha * (planned products) + beta * C (`numeric.py:138-181`).
+    Operands and accumulator may be trees of the reference package (copied to the device once per
+    revision; a reference accumulator gets the result written back in place)."""
+    if not isinstance(c, (QuadtreeMatrix, type(None))):
+        dc, counters = execute_plan(plan, a, b, as_device_tree(c), cfg)
+        return write_back(c, dc), counters
+    a, b = as_device_tree(a), as_device_tree(b)
     if plan.tau != cfg.tau:
         raise ValueError(f"plan built for tau={plan.tau}, config has tau={cfg.tau}")
     if a.n_b != b.n_b:
@@ -212,6 +217,10 @@ def multiply(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig | None = 
     synchronisation; the task and leaf counts are read back when first asked for."""
     if cfg is None:
         cfg = MultiplyConfig()
+    if not isinstance(c, (QuadtreeMatrix, type(None))):      # a reference tree as accumulator: mutate it in place
+        dc, plan, counters = multiply(a, b, cfg, as_device_tree(c))
+        return write_back(c, dc), plan, counters
+    a, b = as_device_tree(a), as_device_tree(b)
     merge_old = c is not None and cfg.beta != 0 and c._leaf_bound() > 0
     if not merge_old and cfg.alpha != 0 and a._leaf_bound() > 0 and b._leaf_bound() > 0:
         from .symbolic import _capacity_hint, plan_capacity
@@ -249,10 +258,23 @@ def multiply_async(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig, c:
     if a.n != b.m:
         raise ValueError(f"inner dimensions differ: {a.m}x{a.n} times {b.m}x{b.n}")
     a._require_16()
+    if cfg.beta != 0 and c is not None and c._leaf_bound() > 0:
+        raise ValueError("multiply_async computes C = alpha A B; use multiply() to merge an accumulator (beta != 0)")
     if c is None:
         c = QuadtreeMatrix(a.m, b.n, a.n_b, device=a.device)
     elif (c.m, c.n) != (a.m, b.n) or c.n_b != a.n_b:
         raise ValueError(f"accumulator is {c.m}x{c.n} (n_b={c.n_b}), product needs {a.m}x{b.n} (n_b={a.n_b})")
+    # An operand that is itself the product of a multiply still in flight: its buffers are only final
+    # once its plan is known not to have overflowed (an overflowed multiply computes nothing and is
+    # repeated into new buffers).  Resolve it first -- one read-back -- instead of planning against
+    # storage that may be replaced.
+    for q in (a, b):
+        if q._nleaf is None:
+            q.nleaf
+    if cfg.alpha == 0 or a.nleaf == 0 or b.nleaf == 0:
+        # the reference skips the product pass (numeric.py:173-177): C comes out empty
+        c.clear()
+        return c, build_plan(a, b, cfg.tau, row_range), ExecCounters(0, 0, 0.0)
     lib = _lib.lib()
     dev = a.device
     depth = max(a.depth, b.depth)
@@ -345,9 +367,9 @@ class _AsyncProduct:
         plan, c = self.plan(), self.c()
         if plan is not None:
             target = c if c is not None else QuadtreeMatrix(plan._a.m, plan._b.n, 16, device=plan._a.device)
-            rev = target._rev
+            # the product moved to new buffers: its revision advances, so a plan built from the
+            # old (empty) storage is recognised as stale
             self.bind(plan, target, arena, lay, step_cap, leaf_cap)
-            target._rev = rev
 
     def on_resolved(self, cnt) -> None:
         from .symbolic import remember_capacity

@@ -169,6 +169,62 @@ class MultiplyPlan:
                     out |= live[:, p, q].astype(np.uint64) << np.uint64(r * 16 + p * 4 + q)
         return out
 
+    def device_masks(self) -> np.ndarray:
+        """The same bits as ``masks()``, but as evaluated ON THE DEVICE by the numeric kernel's own gate
+        (planner classification + per-lane products, ``spamm_execute_gates``): one fine4 run into
+        scratch product buffers that records which micro products it executed."""
+        import ctypes as C
+        import torch
+        from .tree import _stream
+        t = self.ikj()
+        if t.shape[0] == 0:
+            return np.zeros(0, np.uint64)
+        a, b = self._a, self._b
+        dev = a.device
+        nC, ns = self.n_cleaves, self.n_steps
+        va, vb = a.view(self.depth), b.view(self.depth, left=False)
+        vals = torch.empty((nC, _lib.REC), dtype=torch.float32, device=dev)
+        vals_t = torch.empty((nC, _lib.REC), dtype=torch.float32, device=dev)
+        leaf_sq = torch.empty((nC,), dtype=torch.float64, device=dev)
+        counters = torch.zeros((2,), dtype=torch.int64, device=dev)
+        gates = torch.zeros((ns * 64,), dtype=torch.int64, device=dev)
+        bufs = self.buffers()
+        _lib.check(_lib.lib().spamm_execute_gates(C.byref(va), C.byref(vb), C.byref(bufs), ns, nC, float(self.tau),
+                                                  vals.data_ptr(), vals_t.data_ptr(), leaf_sq.data_ptr(),
+                                                  counters.data_ptr(), gates.data_ptr(), _stream()), "execute_gates")
+        gh = gates.cpu().numpy().view(np.uint64).reshape(ns, 4, 16)
+        rec = self.step_records()
+        live = rec[:, 8:12].astype(np.int64) & 0xFFFF
+        bits = (live[:, :, None] >> np.arange(16)[None, None, :]) & 1
+        s_idx, kk, pos = np.nonzero(bits)                  # same enumeration as ikj()
+        sub_shift = min(2, self.depth)
+        ti, tj = morton.decode_array(rec[:, 3].astype(np.uint64))
+        i = (ti[s_idx].astype(np.int64) << sub_shift) + _POS_DI[pos]
+        j = (tj[s_idx].astype(np.int64) << sub_shift) + _POS_DJ[pos]
+        k = (rec[:, 0].astype(np.int64)[s_idx] << sub_shift) + kk
+        order = np.lexsort((k, morton.encode_array(i, j)))
+        assert int(counters[0].item()) == int(sum(bin(int(x)).count("1") for x in gh[s_idx, kk, pos]))
+        return gh[s_idx, kk, pos][order]
+
+    def classification(self) -> tuple[np.ndarray, np.ndarray]:
+        """(full, dead) flags per task of ``ikj()``: what the planner decided from the sub-norm ranges
+        (spamm_step.live bits 16..31 and spamm_step.dead)."""
+        rec = self.step_records()
+        live = rec[:, 8:12].astype(np.int64) & 0xFFFF
+        full = (rec[:, 8:12].astype(np.int64) >> 16) & 0xFFFF
+        dead = np.stack([rec[:, 13] & 0xFFFF, rec[:, 13] >> 16, rec[:, 14] & 0xFFFF, rec[:, 14] >> 16], axis=1).astype(np.int64)
+        bits = (live[:, :, None] >> np.arange(16)[None, None, :]) & 1
+        s_idx, kk, pos = np.nonzero(bits)
+        sub_shift = min(2, self.depth)
+        ti, tj = morton.decode_array(rec[:, 3].astype(np.uint64))
+        i = (ti[s_idx].astype(np.int64) << sub_shift) + _POS_DI[pos]
+        j = (tj[s_idx].astype(np.int64) << sub_shift) + _POS_DJ[pos]
+        k = (rec[:, 0].astype(np.int64)[s_idx] << sub_shift) + kk
+        order = np.lexsort((k, morton.encode_array(i, j)))
+        f = ((full[s_idx, kk] >> pos) & 1).astype(bool)[order]
+        d = ((dead[s_idx, kk] >> pos) & 1).astype(bool)[order]
+        return f, d
+
     def _reference_order(self):
         """Tasks in the reference's plan order with their norm products, and the loop
         statistics of `symbolic.py:92-132` (ascending k; A then B by descending norm, ties on
@@ -247,6 +303,8 @@ def build_plan(a: QuadtreeMatrix, b: QuadtreeMatrix, tau: float,
     if a.n != b.m:
         raise ValueError(f"inner dimensions differ: {a.m}x{a.n} times {b.m}x{b.n}")
     _check_tau(tau)
+    from .tree import as_device_tree
+    a, b = as_device_tree(a), as_device_tree(b)      # trees of the reference package are copied once per revision
     a._require_16()
     lib = _lib.lib()
     depth = max(a.depth, b.depth)

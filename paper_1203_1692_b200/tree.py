@@ -56,6 +56,63 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+def pack_reference_leaves(tree) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """Host side of ``QuadtreeMatrix.from_reference``: (int32 keys, (n, 272) float32 leaf records,
+    float64 leaf square sums) of a reference-package tree, in ascending key order.  A record is the
+    256 row-major values followed by the sub-block norms transposed, tail[q*4+p] = sub[p][q]
+    (include/spamm_b200.h); the square sum is float64(leaf norm)^2, whose correctly rounded root is
+    the reference's float32 leaf norm again."""
+    if tree.n_b != DEFAULT_BLOCK:
+        raise ValueError(f"the B200 path stores 16x16 leaves (n_b = 16), got n_b = {tree.n_b}")
+    keys, vals, subs = tree.packed_leaves()
+    n = int(keys.shape[0])
+    rec = np.empty((n, _lib.REC), np.float32)
+    if n == 0:
+        return np.zeros(0, np.int32), rec, np.zeros(0, np.float64)
+    if int(keys.max()) >> 31:
+        raise ValueError("leaf keys beyond 31 bits are not supported (depth <= 15)")
+    norms = np.fromiter((nd.norm for _, nd in tree.leaf_items()), np.float64, n)   # ascending key, as packed_leaves
+    rec[:, :256] = vals.reshape(n, 256)
+    rec[:, 256:] = subs.transpose(0, 2, 1).reshape(n, 16)
+    leaf_sq = norms.astype(np.float32).astype(np.float64) ** 2
+    return keys.astype(np.int64).astype(np.int32), rec, leaf_sq
+
+
+_ingested = None      # reference tree -> (its revision, device copy); weak keys
+
+
+def as_device_tree(x, device=None):
+    """Operands of ``build_plan`` / ``execute_plan`` / ``multiply`` may be trees of the reference
+    package (duck-typed: ``packed_leaves()`` plus ``m, n, n_b``); they are copied to the device once
+    per revision, as `core.py:391-404` caches the packed view by ``_rev``."""
+    global _ingested
+    if x is None or isinstance(x, QuadtreeMatrix):
+        return x
+    if not (hasattr(x, "packed_leaves") and hasattr(x, "leaf_items") and hasattr(x, "n_b")):
+        raise TypeError(f"expected a QuadtreeMatrix, got {type(x).__name__}")
+    if _ingested is None:
+        import weakref
+        _ingested = weakref.WeakKeyDictionary()
+    rev = getattr(x, "_rev", None)
+    hit = _ingested.get(x)
+    if hit is not None and rev is not None and hit[0] == rev:
+        return hit[1]
+    q = QuadtreeMatrix.from_reference(x, device)
+    _ingested[x] = (rev, q)
+    return q
+
+
+def write_back(dst, src: "QuadtreeMatrix"):
+    """Store the leaves of a device tree into a reference-package tree (the accumulator a caller
+    passed in is mutated in place, `numeric.py:165-181`): ``clear`` / ``put_leaf`` / ``compute_norms``."""
+    keys, vals, _ = src.packed_leaves()
+    dst.clear()
+    for k, v in zip(keys.tolist(), vals):
+        dst.put_leaf(int(k), v)
+    dst.compute_norms()
+    return dst
+
+
 class _Span:
     """A typed region of one arena tensor (the single allocation of an asynchronous multiply).
     The kernels only need its address; the tensor view is made when the host first touches it."""
@@ -125,10 +182,11 @@ class TreeNode:
 class _Grids:
     """Slot grids and norm pyramid of a tree indexed at one depth."""
 
-    __slots__ = ("depth", "_slot", "_slot_t", "_norm", "_norm_t")
+    __slots__ = ("depth", "_slot", "_slot_t", "_norm", "_norm_t", "_sub", "_sub_t")
 
     def __init__(self, depth, slot, slot_t, norm, norm_t):
         self.depth, self._slot, self._slot_t, self._norm, self._norm_t = depth, slot, slot_t, norm, norm_t
+        self._sub = self._sub_t = None      # sub-norm range grids, made on the first use as an operand
 
     slot = _lazy_tensor("slot")
     slot_t = _lazy_tensor("slot_t")
@@ -228,6 +286,26 @@ class QuadtreeMatrix:
         q._require_16()
         d = dense.to(device=q.device, dtype=torch.float32, non_blocking=True).contiguous()
         q._build_from_device_dense(d)
+        return q
+
+    @classmethod
+    def from_reference(cls, tree, device=None) -> "QuadtreeMatrix":
+        """Device copy of a tree of the reference package (anything with ``m, n, n_b``,
+        ``packed_leaves()`` and ``leaf_items()``, `core.py:146-405`): the reference's own leaf values,
+        sub-block norms and leaf norms are taken as they are (`core.py:387-405`), so the task set and
+        the gates come out exactly as the reference computes them from that tree.  Interior norms are
+        rebuilt on the device from the leaf norms (they only steer the pruned walk; a parent rebuilt
+        from its children's norms still bounds them, so the task set is the flat rule's)."""
+        q = cls(tree.m, tree.n, tree.n_b, device)
+        keys, rec, leaf_sq = pack_reference_leaves(tree)
+        n = int(keys.shape[0])
+        if n == 0:
+            return q
+        values = torch.from_numpy(rec).to(q.device)
+        values_t = torch.empty_like(values)
+        _lib.check(_lib.lib().spamm_transpose_records(values.data_ptr(), n, values_t.data_ptr(), _stream()),
+                   "transpose_records")
+        q._adopt_packed(torch.from_numpy(keys).to(q.device), values, values_t, torch.from_numpy(leaf_sq).to(q.device), n)
         return q
 
     def _build_from_device_dense(self, d: torch.Tensor) -> None:
@@ -330,10 +408,19 @@ class QuadtreeMatrix:
             _lib.check(_lib.lib().spamm_transpose_records(self.values.data_ptr(), self.values.shape[0], vt.data_ptr(),
                                                           _stream()), "transpose_records")
             self.values_t = vt
+        if nz and g._sub is None and self._values is not None:
+            # range of every leaf's sub-block norms: lets the planner classify fine4 tasks (device only,
+            # from the record tails through the slot grid; no host synchronisation)
+            cells = 1 << (2 * g.depth)
+            g._sub = self._alloc((cells,), torch.int32)
+            g._sub_t = self._alloc((cells,), torch.int32)
+            _lib.check(_lib.lib().spamm_subrange_grids(_ptr(self._values), _ptr(g._slot), g.depth, g._sub.data_ptr(),
+                                                       g._sub_t.data_ptr(), _stream()), "subrange_grids")
         return _lib.TreeView(self.m, self.n, g.depth, self._leaf_bound() if nz else 0,
                              _ptr(self._keys) if nz else None, _ptr(self._values) if nz else None,
                              _ptr(self._values_t) if nz else None,
-                             _ptr(g._slot), _ptr(g._slot_t), _ptr(g._norm), _ptr(g._norm_t))
+                             _ptr(g._slot), _ptr(g._slot_t), _ptr(g._norm), _ptr(g._norm_t),
+                             _ptr(g._sub) if nz else None, _ptr(g._sub_t) if nz else None)
 
     def _flush_guard(self) -> None:
         if self._pending:

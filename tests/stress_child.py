@@ -25,7 +25,8 @@ for gran in ("fine4", "coarse16"):
         assert np.array_equal(c.to_dense().data, want), (gran, it, "values")
         for t in range(oc.depth + 1):
             assert np.array_equal(c.level_norms(t), oc.level_norm(t)), (gran, it, "norms", t)
-    seg = int(plan.counts[12].item())
-    units = int(plan.counts[5].item())
-    print(f"{gran}: units={units} seg_len={seg}")
+    pieces = int(plan.counts[5].item())
+    u = plan.tile_order[: 4 * pieces].cpu().numpy().reshape(pieces, 4)
+    chained = int(np.count_nonzero(u[:, 0] < u[:, 1]))       # pieces that begin inside a super-tile
+    print(f"{gran}: pieces={pieces} rounds={int(plan.counts[12].item())} chained={chained} ")
 print("OK")

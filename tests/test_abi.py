@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 def test_version_and_level_offsets_without_a_gpu():
     from paper_1203_1692_b200 import _lib
     lib = _lib.lib()
-    assert lib.spamm_abi_version() == 1
+    assert lib.spamm_abi_version() == 2
     for t in range(12):
         assert lib.spamm_level_offset_of(t) == _lib.level_offset(t)
         assert _lib.level_offset(t) % 4 == 0 or t == 0

@@ -59,6 +59,13 @@ def test_device_matches_reference(case):
             got = plan.masks()
             want = np.array([omask[(a, b)] for a, b in zip(ka.tolist(), kb.tolist())], np.uint64)
             assert np.array_equal(got, want), "fine4 masks"
+            # the gate as the numeric kernel itself evaluated it (planner classification + per-lane
+            # products in execute_kernel), not a host recomputation
+            assert np.array_equal(plan.device_masks(), want), "fine4 masks evaluated by the device gate"
+            full, dead = plan.classification()
+            assert np.all(want[full] == np.uint64(0xFFFFFFFFFFFFFFFF)), "a task classified 'all pass' has a failing micro product"
+            assert np.all(want[dead] == 0), "a task classified 'none passes' has a passing micro product"
+            assert not np.any(full & dead)
         # ascending k inside every product leaf, leaves in ascending Morton order
         t = plan.ikj()
         if len(plan):

@@ -1,6 +1,6 @@
-"""The numeric kernel's scheduling knobs must never change a bit of the result: chained segments of
-any length (accumulators handed between CTAs), ring depth, CTAs per SM, programmatic dependent
-launch on or off.  Each setting runs in its own process (the knobs are read once per process) and
+"""The numeric kernel's scheduling knobs must never change a bit of the result: pieces of any
+length (accumulators handed between CTAs inside a super-tile), ring depth, CTAs per SM, programmatic
+dependent launch on or off.  Each setting runs in its own process (the knobs are read once per process) and
 repeats the product, so a hand-over race would show up as a mismatch with the oracle."""
 
 import os
@@ -14,14 +14,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 SETTINGS = [
     {},                                                                  # defaults
-    {"SPAMM_EX_CTAS": "1", "SPAMM_UNIT_MIN_SEG": "1"},                   # 148 CTAs: tiles cut into 1-record segments
-    {"SPAMM_EX_CTAS": "1", "SPAMM_UNIT_MIN_SEG": "1", "SPAMM_UNIT_TARGET": "8000"},
-    {"SPAMM_EX_CTAS": "1", "SPAMM_EX_STAGES": "2", "SPAMM_UNIT_MIN_SEG": "3"},
-    {"SPAMM_UNIT_TARGET": "0"},                                          # whole tiles only
-    {"SPAMM_PDL": "0", "SPAMM_EX_CTAS": "1", "SPAMM_UNIT_MIN_SEG": "2"},
-    # a grid larger than what is resident (3 CTAs per SM requested, 2 fit) with chained segments:
-    # every unit must then be claimed dynamically or a wait could starve its predecessor
-    {"SPAMM_EX_CTAS": "3", "SPAMM_UNIT_MIN_SEG": "1", "N": "4096"},
+    {"SPAMM_EX_CTAS": "1", "SPAMM_PIECE_RECORDS": "1"},                  # as many pieces as fit: most are 1-2 records inside one tile
+    {"SPAMM_EX_CTAS": "1", "SPAMM_PIECE_RECORDS": "3", "SPAMM_REC_WEIGHT": "1"},
+    {"SPAMM_EX_CTAS": "1", "SPAMM_EX_STAGES": "2", "SPAMM_PIECE_RECORDS": "2", "SPAMM_REC_WEIGHT": "64"},
+    {"SPAMM_PIECE_RECORDS": "1000000"},                                  # one piece per SM
+    {"SPAMM_PDL": "0", "SPAMM_EX_CTAS": "1", "SPAMM_PIECE_RECORDS": "2"},
+    # a grid larger than what is resident (3 CTAs per SM requested, 2 fit) with chained pieces: a CTA only
+    # waits for the head of a piece that was drawn, and therefore begun, before its own
+    {"SPAMM_EX_CTAS": "3", "SPAMM_PIECE_RECORDS": "1", "N": "4096"},
 ]
 
 
@@ -33,5 +33,5 @@ def test_scheduling_knobs_do_not_change_results(env):
                           "6" if "N" not in env else "3"],
                          env=full, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("OK"), out.stdout[-2000:] + out.stderr[-2000:]
-    if (env.get("SPAMM_EX_CTAS") == "1" or "N" in env) and env.get("SPAMM_UNIT_TARGET") != "0":
-        assert "seg_len=0" not in out.stdout, "this setting is meant to exercise chained segments: " + out.stdout
+    if env.get("SPAMM_EX_CTAS") == "1" or "N" in env:
+        assert "chained=0 " not in out.stdout, "this setting is meant to exercise pieces chained inside super-tiles: " + out.stdout
