@@ -29,7 +29,7 @@ sys.path.insert(0, ROOT)
 
 HEADLINE_TAU = 1e-8
 L2_FLUSH_BYTES = 256 << 20
-NUM_SMS = 148
+NUM_SMS = 148      # B200; replaced by the device's count once a GPU is visible (run_single)
 
 
 def peaks():
@@ -169,9 +169,12 @@ def run_reference(args) -> None:
         "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": name, "n": int(a_d.shape[0]), "tau": tau, "granularity": args.granularity,
-                   "tasks": len(plan), "products4": counters.products4},
+                   "tasks": len(plan), "product_leaves": int(np.unique(plan.c_keys).size), "products4": counters.products4,
+                   "l2": "not applicable (CPU arm)",
+                   "effective_gflops_2n3": 2.0 * float(a_d.shape[0]) ** 3 / sec / 1e9},
         "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"{sample}; C port of the reference algorithm, OpenMP over product leaves"},
+                         "sample": f"{sample}; C port of the reference algorithm, OpenMP over product leaves",
+                         "python_reference": python_reference_time(name, tau, args.granularity)},
         "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -221,6 +224,93 @@ def kernel_time_execute(P, torch, plan, qa, qb, cfg, reps, flush):
         if it >= 2:
             times.append(e0.elapsed_time(e1))
     return float(np.mean(times))
+
+
+def kernel_time_plan(P, torch, plan, qa, qb, tau, reps, flush):
+    """Average duration of the symbolic phase alone (spamm_plan: plan_tiles + plan_order kernels,
+    plus root/expand for deep trees), CUDA events around the C call, L2 flushed."""
+    import ctypes as C
+    from paper_1203_1692_b200 import _lib
+    from paper_1203_1692_b200.symbolic import PlanAlloc
+    lib = _lib.lib()
+    va, vb = qa.view(plan.depth), qb.view(plan.depth, left=False)
+    pb = PlanAlloc(qa.device, plan.depth, max(plan.n_steps, 1) + 64, max(plan.n_cleaves, 1) + 64)
+    st = torch.cuda.current_stream().cuda_stream
+    times = []
+    for it in range(reps + 2):
+        flush.fill_(it)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(lib.spamm_plan(C.byref(va), C.byref(vb), float(tau), 0, 1 << plan.depth, C.byref(pb.struct),
+                                  pb.ws.data_ptr(), pb.ws_bytes, st), "plan")
+        e1.record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            times.append(e0.elapsed_time(e1))
+    assert int(pb.counts[2].item()) == 0 and int(pb.counts[4].item()) == plan.n_steps
+    return float(np.mean(times))
+
+
+def kernel_time_interior(P, torch, c, reps, flush):
+    """Average duration of the interior-norm kernel on the product tree (K4, compute_norms on C)."""
+    from paper_1203_1692_b200 import _lib
+    lib = _lib.lib()
+    depth = c.depth
+    cells, total = 1 << (2 * depth), _lib.level_total(depth)
+    dev = c.device
+    g = c.grids()
+    sq_grid = torch.zeros((cells,), dtype=torch.float64, device=dev)
+    off = _lib.level_offset(depth)
+    leaf_norm = g.norm[off:off + cells].double()
+    sq_grid.copy_(torch.where(leaf_norm >= 0, leaf_norm * leaf_norm, torch.zeros_like(leaf_norm)))
+    norm, norm_t = g.norm.clone(), g.norm_t.clone()
+    sq_levels = torch.empty((total,), dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    times = []
+    for it in range(reps + 2):
+        flush.fill_(it)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(lib.spamm_build_interior(sq_grid.data_ptr(), depth, norm.data_ptr(), norm_t.data_ptr(),
+                                            sq_levels.data_ptr(), 0, st), "build_interior")
+        e1.record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            times.append(e0.elapsed_time(e1))
+    return float(np.mean(times))
+
+
+def time_from_dense(P, torch, dense_dev, reps, flush):
+    """Average duration of QuadtreeMatrix.from_dense on a device-resident dense matrix (K1: leaf and
+    sub-block norms, slot scan, leaf packing in both layouts, interior norms)."""
+    times, q = [], None
+    for it in range(reps + 2):
+        flush.fill_(it)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        q = P.QuadtreeMatrix.from_dense(dense_dev)
+        e1.record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            times.append(e0.elapsed_time(e1))
+        if it < reps + 1:
+            del q
+    return float(np.mean(times)), q
+
+
+def python_reference_time(name: str, tau: float, gran: str):
+    """Seconds per multiply of the unmodified Python reference, measured in the build container by
+    profiles/python_reference_time.py (the reference cannot run on the GPU box)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "python_reference_times.json")) as f:
+            d = json.load(f)
+        r = d["runs"].get(f"{name}:{tau:g}:{gran}")
+        if r:
+            return {"multiply_s": r["multiply_s"], "build_plan_s": r["build_plan_s"], "execute_plan_s": r["execute_plan_s"],
+                    "from_dense_s": r["from_dense_s"], "cores": 1, "where": d["where"], "when": d["when"]}
+    except (OSError, ValueError, KeyError):
+        pass
+    return None
 
 
 def touched_leaves(torch, plan, nleaf_a: int, nleaf_b: int):
@@ -279,8 +369,10 @@ def measure_case(P, torch, qa, qb, tau, gran, flush, fp32_peak, ref64=None, step
 
 def run_single(args, torch, P, local: int) -> None:
     from paper_1203_1692_b200 import _lib, inputs
+    global NUM_SMS
     name = args.workload or "cfg2"
     pk = peaks()
+    NUM_SMS = torch.cuda.get_device_properties(local).multi_processor_count
     fp32_peak = 2 * 128 * NUM_SMS * pk["sm_max_mhz"] * 1e6 / 1e12
     a_d, b_d = inputs.make_operands(name)
     n = a_d.shape[0]
@@ -308,6 +400,23 @@ def run_single(args, torch, P, local: int) -> None:
     ta_hit, tb_hit = touched_leaves(torch, plan, qa.nleaf, qb.nleaf)
     alg_bytes = 1088 * (ta_hit + tb_hit + 2 * plan.n_cleaves) + 64 * plan.n_steps
     n_tasks, n_cleaves = len(plan), plan.n_cleaves
+
+    # ---- the other kernels of the path, each against the roofline that bounds it
+    reps_k = max(5, min(args.steps, 20))
+    k2_ms = kernel_time_plan(P, torch, plan, qa, qb, cfg.tau, reps_k, flush)
+    k4_ms = kernel_time_interior(P, torch, c, reps_k, flush)
+    dense_dev = torch.from_numpy(a_d).cuda()
+    k1_ms, _q = time_from_dense(P, torch, dense_dev, reps_k, flush)
+    del _q, dense_dev
+    n_p = 16 << qa.depth
+    La = 1 << qa.depth
+    # K1: the dense matrix read once, the stored leaves written in both record layouts, the grids and pyramid
+    k1_bytes = 4 * n * n + 2 * 1088 * qa.nleaf + La * La * (4 + 4 + 4 + 4 + 8) * 4 // 3
+    # K2: the leaf norm grids of both operands (and their sub-norm range grids) read once, one record per step written
+    k2_bytes = (4 + 4) * (La * La) * 2 + 64 * plan.n_steps + 4 * 4 * plan.counts[5].item()
+    # K4: C's leaf grid of square sums read, every level of both norm pyramids and the square sums written
+    Lc = 1 << c.depth
+    k4_bytes = Lc * Lc * 8 + Lc * Lc * (4 + 4 + 8) * 4 // 3
 
     # ---- end to end through the public API with host buffers
     host_a = torch.from_numpy(a_d).pin_memory()
@@ -366,7 +475,8 @@ def run_single(args, torch, P, local: int) -> None:
         oflops = 128 * ocnt.products4 if args.granularity == "fine4" else 8192 * len(opl)
         cpu = {"value": oflops / dt / 1e9, "unit": "GFLOP/s", "cores": O.num_threads(), "kind": "port",
                "sample": f"{reps} whole {name} multiplies, {dt * 1e3:.1f} ms each (C port of the reference "
-                         f"algorithm, OpenMP over product leaves)"}
+                         f"algorithm, OpenMP over product leaves)",
+               "python_reference": python_reference_time(name, args.tau, args.granularity)}
         del ta_o, tb_o
 
     # ---- the other BASELINE.json configs on this GPU (time per multiply, GFLOP/s, K3 fraction)
@@ -416,6 +526,15 @@ def run_single(args, torch, P, local: int) -> None:
                      "kernel_ms": k3_ms, "traffic": recorded_traffic(name, args.granularity),
                      "algorithmic_bytes": int(alg_bytes),
                      "hbm_frac_of_measured": alg_bytes / (k3_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
+        "roofline_k1": {"bound": "hbm", "kernel": "from_dense (leaf_norms_dense + slot scan + pack_leaves + interior)",
+                        "achieved": k1_bytes / (k1_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "frac": k1_bytes / (k1_ms * 1e-3) / 1e9 / pk["hbm_gbs"], "ms": k1_ms, "algorithmic_bytes": int(k1_bytes)},
+        "roofline_k2": {"bound": "latency (hbm shown)", "kernel": "spamm_plan (plan_tiles + plan_order)",
+                        "achieved": k2_bytes / (k2_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "frac": k2_bytes / (k2_ms * 1e-3) / 1e9 / pk["hbm_gbs"], "ms": k2_ms, "algorithmic_bytes": int(k2_bytes)},
+        "roofline_k4": {"bound": "latency (hbm shown)", "kernel": "interior_kernel (norms of C)",
+                        "achieved": k4_bytes / (k4_ms * 1e-3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                        "frac": k4_bytes / (k4_ms * 1e-3) / 1e9 / pk["hbm_gbs"], "ms": k4_ms, "algorithmic_bytes": int(k4_bytes)},
         "cpu_baseline": cpu,
         "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

@@ -178,11 +178,19 @@ __device__ __forceinline__ bool mbar_try_wait_hint(uint64_t *bar, uint32_t parit
         : "memory");
     return ok != 0;
 }
+#ifndef MBAR_HINT_NS
+#define MBAR_HINT_NS 20000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     if (mbar_try_wait(bar, parity)) return;
-    while (!mbar_try_wait_hint(bar, parity, 20000u)) {
+#if MBAR_HINT_NS > 0
+    while (!mbar_try_wait_hint(bar, parity, MBAR_HINT_NS)) {
     }
+#else
+    while (!mbar_try_wait(bar, parity)) {
+    }
+#endif
 }
 // 1-D bulk copy global -> shared, completion counted on an mbarrier (SASS: UBLKCP).
 __device__ __forceinline__ void bulk_copy_g2s(void *smem_dst, const void *gmem_src, uint32_t bytes, uint64_t *bar)

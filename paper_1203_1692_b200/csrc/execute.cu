@@ -17,12 +17,15 @@
 // gate and multiply from shared memory; with fine4 the planner has already classified most tasks from
 // the sub-norm ranges of their leaves (all 64 micro products run / none / undecided, spamm_step.live
 // and .dead), so only band-edge tasks pay for per-lane gate arithmetic.  The persistent CTAs (two per SM) run a
-// STATIC partition of the record stream that the planner cut into pieces of equal weight, one per SM
-// (plan.cu, plan_order_kernel); a piece is whole super-tiles plus at most one head and one tail
-// segment of a tile shared with the neighbouring piece, whose accumulators pass from CTA to CTA
-// through C's value records (spamm_b200.h).  The CTAs resident on one SM find each other through
-// %smid and share the SM's piece tile by tile (a compare-and-swap cursor per piece): two CTAs on an SM
-// do not advance equally, SMs do, so all SMs finish together without a global hand-out counter.
+// STATIC partition of the record stream that the planner cut into pieces of equal weight (plan.cu,
+// plan_order_kernel); a piece is whole super-tiles plus at most one head and one tail segment of a
+// tile shared with the neighbouring piece, whose accumulators pass from team to team through C's
+// value records (spamm_b200.h).  One CTA per SM holds TWO TEAMS, each a producer warp, a ring and
+// eight consumer warps; team t owns the warps with (warp & 1) == t, i.e. two of the SM's four warp
+// schedulers to itself.  (Two co-resident CTAs share every scheduler and the hardware favours one of
+// them about 2:1 -- measured -- so equal pieces would not finish together; teams on disjoint schedulers
+// have identical resources.)  A team draws its pieces from one counter in stream order: the first
+// round is in effect a static assignment, a large product continues dynamically.
 // Launched with programmatic dependent launch.
 // Tuning aids: SPAMM_EX_STAGES, SPAMM_EX_CTAS, SPAMM_EX_DEBUG, SPAMM_EX_TRACE (per-CTA time stamps).
 #include <stdio.h>
@@ -33,12 +36,17 @@
 
 #define EX_MAX_STAGES 6
 #define EX_CONSUMERS 8
-#define EX_THREADS (32 * (EX_CONSUMERS + 1))          // consumers + producer
+#ifndef EX_TEAMS
+#define EX_TEAMS 2                                        // teams per CTA; 1 = two independent CTAs per SM instead
+#endif
+#define EX_THREADS (32 * EX_TEAMS * (EX_CONSUMERS + 1))   // per team: consumers + producer
+#define EX_CTAS_PER_SM (EX_TEAMS == 1 ? 2 : 1)
 #define EX_EXIT (1u << 31)
 #define EX_CHAIN_IN (1u << 30)    // first step of a later segment: accumulators come from C's records
 #define EX_CHAIN_OUT (1u << 29)   // last step of a segment that is not the tile's last: hand them on
 #define EX_PREFETCH 4
 #define EX_BLOCK_BYTES (16 * SPAMM_REC_BYTES)     // one 4x4 block of leaf records
+#define EX_TRACE2_RECORDS 96
 
 struct __align__(16) StageDesc {
     uint32_t live[4];      // live tasks per kk (one 16-byte read)
@@ -59,11 +67,10 @@ struct ExecArgs {
     const float *b_values;
     const spamm_step *steps;
     const int32_t *pieces;       // plan.tile_order: (b, mb, me, e) per piece, see plan_order_kernel
-    int32_t *cursor;             // per piece: how far its jobs (head segment, tiles, tail segment) are handed out
     const int32_t *counts;       // plan counts (device): [5] = number of pieces
     int32_t *chain;              // per product leaf: the record up to which its partial sums are handed on (0 = none)
-    unsigned int *xs;            // ExecShared: piece tickets, exited CTAs, per-SM tables; zero between launches
-    int xs_early;                // xs is not touched by the preceding kernel: the SM's CTAs pair up before waiting for it
+    unsigned int *ticket;        // [0] pieces drawn, [1] teams that ran out of work; zero between launches
+    int ticket_early;            // the tickets are not touched by the preceding kernel: draw before waiting for it
     double tau;
     float alpha;
     int alpha_is_one;
@@ -84,25 +91,10 @@ struct ExecArgs {
     unsigned long long *gates;   // optional (spamm_execute_gates): the 64 gate bits of every task as evaluated HERE
     int dbg;                     // tuning aid (SPAMM_EX_DEBUG): 1 = no copies, 2 = no math
     unsigned long long *trace;   // tuning aid (SPAMM_EX_TRACE): per CTA start / first data / end / units
+    long long *trace2;           // tuning aid (SPAMM_EX_TRACE2): SM clock of every warp of team 0 of CTA 0 at the
+                                 // points of its first EX_TRACE2_RECORDS records (consumers: wait begin, data
+                                 // ready, math done; producer: stage free, copies issued)
 };
-
-// ExecShared (uint32 words): [0] piece tickets drawn, [1] CTAs that have run out of work,
-// [2 .. 258) CTAs arrived per SM, [258 .. 514) the piece (+ 1) the CTAs of an SM currently share
-#define XS_TICKET 0
-#define XS_EXITED 1
-#define XS_ARRIVE 2
-#define XS_PIECE 258
-#define XS_WORDS 514
-__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int *p)
-{
-    unsigned int v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned int *p, unsigned int v)
-{
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 __device__ __forceinline__ unsigned long long global_timer()
 {
@@ -135,140 +127,103 @@ __device__ __forceinline__ void mac2(float2 &acc, float2 a, float b)
     }
 }
 
-template <bool EXACT, bool FINE>
-#ifndef EX_MIN_BLOCKS
-#define EX_MIN_BLOCKS 2
-#endif
-__global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(ExecArgs g)
+// DBG: the instantiation with the tuning aids (time stamps, gate evidence, SPAMM_EX_DEBUG switches); the
+// product path runs the one without them, which keeps their state out of the hot loop's registers.
+template <bool EXACT, bool FINE, bool DBG>
+__global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(ExecArgs g)
 {
-    // dynamic shared memory: nstages x (A block + B block), then descriptors and barriers
+    // dynamic shared memory, per team: nstages x (A block + B block), descriptors, barriers
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int nstages = g.nstages;
-    unsigned char *sA = smem_raw;
-    unsigned char *sB = smem_raw + (size_t)nstages * EX_BLOCK_BYTES;
-    StageDesc *desc = reinterpret_cast<StageDesc *>(smem_raw + (size_t)nstages * 2 * EX_BLOCK_BYTES);
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = lane_id();
+    // Teams on disjoint warp schedulers: warp w runs on scheduler w % 4, so the even warps (team 0)
+    // have schedulers 0 and 2 to themselves and the odd warps (team 1) schedulers 1 and 3.
+    const int team = EX_TEAMS == 1 ? 0 : (warp & 1);
+    const int vwarp = EX_TEAMS == 1 ? warp : (warp >> 1);          // 0 .. 7 consumers, 8 = the team's producer
+    const size_t team_bytes = (size_t)nstages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16);
+    unsigned char *tbase = smem_raw + (size_t)team * team_bytes;
+    unsigned char *sA = tbase;
+    unsigned char *sB = tbase + (size_t)nstages * EX_BLOCK_BYTES;
+    StageDesc *desc = reinterpret_cast<StageDesc *>(tbase + (size_t)nstages * 2 * EX_BLOCK_BYTES);
     uint64_t *full_bar = reinterpret_cast<uint64_t *>(desc + EX_MAX_STAGES);
     uint64_t *empty_bar = full_bar + EX_MAX_STAGES;
 
-    const int warp = threadIdx.x >> 5;
-    const uint32_t lane = lane_id();
     // everything that does not depend on the preceding kernel comes before the wait for it
-    if (threadIdx.x == 0) {
+    if (vwarp == EX_CONSUMERS && lane == 0) {
         for (int s = 0; s < nstages; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], EX_CONSUMERS);
         }
         fence_barrier_init();
     }
-    // The CTAs of one SM share a piece.  The first to arrive on an SM draws a piece ticket and
-    // publishes it in the SM's table entry; the others read it there.  Tickets are drawn in order, and
-    // whoever draws a piece starts with its head segment, so the CTA that later waits for that head
-    // (the tail of the next piece, run last) waits for a running CTA: no assumption about residency.
-    uint32_t smid;
-    asm("mov.u32 %0, %%smid;" : "=r"(smid));
-    smid &= 255u;
+    // First piece: pieces are drawn from one counter, in stream order.  A team only ever waits for
+    // partial sums of the piece before one of its own, which was drawn earlier by a team that is
+    // running and begins with the segment in question: no assumption about residency or dispatch order.
     int piece = 0;
-    auto pair_up = [&]() {
-        if (lane == 0) {
-            if (atomicAdd(g.xs + XS_ARRIVE + smid, 1u) == 0u) {
-                piece = (int)atomicAdd(g.xs + XS_TICKET, 1u);
-                st_release_u32(g.xs + XS_PIECE + smid, (unsigned int)piece + 1u);
-            } else {
-                unsigned int v;
-                while ((v = ld_acquire_u32(g.xs + XS_PIECE + smid)) == 0u) __nanosleep(64);
-                piece = (int)v - 1;
-            }
-        }
+    if (vwarp == EX_CONSUMERS && g.ticket_early) {
+        if (lane == 0) piece = (int)atomicAdd(g.ticket, 1u);
         piece = __shfl_sync(FULL_MASK, piece, 0);
-    };
-    if (warp == EX_CONSUMERS && g.xs_early) pair_up();
+    }
     pdl_enter();
     if (blockIdx.x == 0)
         for (int x = threadIdx.x; x < g.clean_words; x += blockDim.x) g.clean_ptr[x] = 0u;
     __syncthreads();
     int stage = 0;
     uint32_t phase = 0;
-    if (g.trace && threadIdx.x == 0) g.trace[blockIdx.x * 4] = global_timer();
+    const int trace_slot = (int)blockIdx.x * EX_TEAMS + team;
+    if (DBG && g.trace && vwarp == 0 && lane == 0) g.trace[trace_slot * 4] = global_timer();
 
-    if (warp == EX_CONSUMERS) {
+    if (vwarp == EX_CONSUMERS) {
         // ============ producer: stream step records, stage leaf blocks with bulk copies ============
-        if (!g.xs_early) pair_up();
+        if (!g.ticket_early) {
+            if (lane == 0) piece = (int)atomicAdd(g.ticket, 1u);
+            piece = __shfl_sync(FULL_MASK, piece, 0);
+        }
         const int npieces = g.counts[2] ? 0 : g.counts[5];      // an overflowed plan is incomplete: do nothing
+        const int first_piece = piece;
         const uint32_t *words = reinterpret_cast<const uint32_t *>(g.steps);
         const int4 *pieces = reinterpret_cast<const int4 *>(g.pieces);
+        // cursor over the records of my pieces: per piece the head segment [me, e), the whole tiles
+        // [mb, me), the tail segment [b, mb).  The next piece is drawn two records before the cursor
+        // leaves the current one, so the latency of the draw hides behind the staged records.
+        int run = -1, r = 0, rend = 0, rbeg = 0, left = 0, units_done = 0, next_piece = 0;
+        bool drawn = false, more = piece < npieces;
         int4 pd = make_int4(0, 0, 0, 0);
-        if (piece < npieces) pd = __ldg(pieces + piece);
-        // Jobs of a piece, in hand-out order: the head segment [me, e), the whole tiles of [mb, me) one by
-        // one, the tail segment [b, mb).  The cursor counts handed-out records in that order.  claim():
-        // the next job of the SM's piece -- or of the piece the SM moves on to -- as records [jb, je).
-        int jb = 0, je = 0, units_done = 0;
-        auto claim = [&]() -> bool {
-            for (;;) {
-                if (piece >= npieces) return false;
-                int got = 0;
-                if (lane == 0) {
-                    const int h = pd.w - pd.z, t = pd.z - pd.y, tl = pd.y - pd.x, total = h + t + tl;
-                    for (;;) {
-                        const int v = ld_acquire_gpu(g.cursor + piece);
-                        if (v >= total) { got = 0; break; }
-                        int nv;
-                        if (v < h) { nv = h; jb = pd.z; je = pd.w; }
-                        else if (v < h + t) {
-                            const int r0 = pd.y + (v - h);
-                            int len = (int)__ldg(words + (size_t)r0 * 16 + 15);      // records of this tile
-                            if (len < 1) len = 1;
-                            if (r0 + len > pd.z) len = pd.z - r0;
-                            nv = v + len; jb = r0; je = r0 + len;
-                        } else { nv = total; jb = pd.x; je = pd.y; }
-                        if (atomicCAS(g.cursor + piece, v, nv) == v) { got = 1; break; }
-                    }
-                }
-                got = __shfl_sync(FULL_MASK, got, 0);
-                if (got) {
-                    jb = __shfl_sync(FULL_MASK, jb, 0);
-                    je = __shfl_sync(FULL_MASK, je, 0);
-                    return true;
-                }
-                // the piece is handed out: join the piece the SM's other CTAs moved on to, or draw the next
-                if (lane == 0) {
-                    const unsigned int cur = ld_acquire_u32(g.xs + XS_PIECE + smid);
-                    if (cur != (unsigned int)piece + 1u) {
-                        piece = (int)cur - 1;
-                    } else {
-                        const int np = (int)atomicAdd(g.xs + XS_TICKET, 1u);
-                        atomicCAS(g.xs + XS_PIECE + smid, (unsigned int)piece + 1u, (unsigned int)np + 1u);
-                        piece = np;      // mine in any case; if the entry had moved meanwhile, I rejoin it afterwards
-                    }
-                }
-                piece = __shfl_sync(FULL_MASK, piece, 0);
-                if (piece < npieces) pd = __ldg(pieces + piece);
-            }
-        };
-        // cursor over the records of my jobs.  The next job is claimed two records before the cursor
-        // leaves the current one: the claim's latency hides behind the staged records, and no CTA sits
-        // on a job it has not started while its neighbour runs dry.
-        int r = 0, rend = 0, rbeg = 0, nb = 0, ne = 0;
-        bool have_next = false, dry = false, more = true;
+        if (more) {
+            pd = __ldg(pieces + piece);
+            left = pd.w - pd.x;
+        }
         // fetch: the next record of the cursor -> (word of lane l < 16, meta); meta = rec | first << 30 | last << 31, ~0 = none
         auto fetch = [&](uint32_t &wd, uint32_t &meta) {
             for (;;) {
                 if (!more) { wd = 0u; meta = 0xFFFFFFFFu; return; }
-                if (!have_next && !dry && rend - r <= 2) {
-                    have_next = claim();
-                    dry = !have_next;
-                    nb = jb; ne = je;
+                if (!drawn && left <= 2) {
+                    if (lane == 0) next_piece = (int)atomicAdd(g.ticket, 1u);
+                    drawn = true;
                 }
                 if (r < rend) break;
-                if (!have_next) { more = false; continue; }
-                r = rbeg = nb; rend = ne;
-                have_next = false;
-                ++units_done;
+                ++run;
+                if (run == 3) {
+                    piece = __shfl_sync(FULL_MASK, next_piece, 0);
+                    drawn = false;
+                    if (piece >= npieces) { more = false; continue; }
+                    pd = __ldg(pieces + piece);
+                    left = pd.w - pd.x;
+                    run = 0;
+                }
+                if (run == 0) { ++units_done; r = pd.z; rend = pd.w; }
+                else if (run == 1) { r = pd.y; rend = pd.z; }
+                else { r = pd.x; rend = pd.y; }
+                rbeg = r;
             }
             wd = lane < 16 ? __ldg(words + (size_t)r * 16 + lane) : 0u;
             meta = (uint32_t)r | (r == rbeg ? (1u << 30) : 0u) | (r + 1 == rend ? (1u << 31) : 0u);
             ++r;
+            --left;
         };
         uint32_t w[EX_PREFETCH], m[EX_PREFETCH];
+        int prec = 0;
 #pragma unroll
         for (int x = 0; x < EX_PREFETCH; ++x) fetch(w[x], m[x]);
         while (m[0] != 0xFFFFFFFFu) {
@@ -278,7 +233,10 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
             fetch(w[EX_PREFETCH - 1], m[EX_PREFETCH - 1]);
             const uint32_t na = __popc(__shfl_sync(FULL_MASK, cur, 5));
             const uint32_t nb = __popc(__shfl_sync(FULL_MASK, cur, 7));
+            const bool t2p = DBG && g.trace2 && blockIdx.x == 0 && team == 0 && prec < EX_TRACE2_RECORDS && lane == 0;
+            if (t2p) g.trace2[(prec * 9 + 8) * 4 + 0] = clock64();
             mbar_wait(&empty_bar[stage], phase ^ 1u);
+            if (t2p) g.trace2[(prec * 9 + 8) * 4 + 1] = clock64();
             uint32_t *d = reinterpret_cast<uint32_t *>(&desc[stage]);
             if (lane == 1) {                                 // flags: a run that starts or ends inside a tile is chained
                 uint32_t f = cur;
@@ -295,7 +253,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
             if (lane == 7) d[8] = cur;                       // b_present
             if (lane >= 8 && lane < 12) d[lane - 8] = cur;   // live[kk]
             __syncwarp();
-            const bool copy = !(g.dbg & 1);
+            const bool copy = !(DBG && (g.dbg & 1));
             if (lane == 0) mbar_arrive_expect_tx(&full_bar[stage], copy ? (na + nb) * SPAMM_REC_BYTES : 0u);
             __syncwarp();
             if (copy && lane == 4)
@@ -304,20 +262,20 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
             if (copy && lane == 6)
                 bulk_copy_g2s(sB + (size_t)stage * EX_BLOCK_BYTES, g.b_values + (size_t)cur * SPAMM_REC,
                               nb * SPAMM_REC_BYTES, &full_bar[stage]);
+            if (t2p) g.trace2[(prec * 9 + 8) * 4 + 2] = clock64();
+            ++prec;
             if (++stage == nstages) { stage = 0; phase ^= 1u; }
         }
         mbar_wait(&empty_bar[stage], phase ^ 1u);
         if (lane == 0) {
             desc[stage].flags = EX_EXIT;
             mbar_arrive(&full_bar[stage]);
-            if (g.trace) g.trace[blockIdx.x * 4 + 3] = (unsigned long long)units_done;
-        }
-        // the last CTA to run out of work leaves the shared state and the cursors at zero for the next launch
-        int last = 0;
-        if (lane == 0) last = atomicAdd(g.xs + XS_EXITED, 1u) == gridDim.x - 1 ? 1 : 0;
-        if (__shfl_sync(FULL_MASK, last, 0)) {
-            for (int x = (int)lane; x < npieces; x += 32) g.cursor[x] = 0;
-            for (int x = (int)lane; x < XS_WORDS; x += 32) g.xs[x] = 0u;
+            if (DBG && g.trace) g.trace[trace_slot * 4 + 3] = (unsigned long long)units_done | ((unsigned long long)first_piece << 32);
+            // the last team to run out of work leaves both counters at zero for the next launch
+            if (atomicAdd(g.ticket + 1, 1u) == gridDim.x * EX_TEAMS - 1) {
+                g.ticket[0] = 0u;
+                g.ticket[1] = 0u;
+            }
         }
         return;
     }
@@ -330,18 +288,22 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
     const int half = (lane >> 2) & 1;
     const int p = ((lane >> 4) & 1) << 1 | ((lane >> 1) & 1), q = ((lane >> 3) & 1) << 1 | (lane & 1);
     const int t16 = p * 4 + q;
-    const int mypos = 2 * warp + half;
+    const int mypos = 2 * vwarp + half;
     const int di = step_pos_di(mypos), dj = step_pos_dj(mypos);
     uint32_t executed = 0;
     float2 acc2[2][4];     // acc2[h][j] = C sub-block elements (2h, j) and (2h+1, j)
     bool traced = false;
     bool chained = false;  // the sums of the current tile came (partly) from another CTA
+    int crec = 0;
     for (;;) {
+        const bool t2c = DBG && g.trace2 && blockIdx.x == 0 && team == 0 && crec < EX_TRACE2_RECORDS && lane == 0;
+        if (t2c) g.trace2[(crec * 9 + vwarp) * 4 + 0] = clock64();
         mbar_wait(&full_bar[stage], phase);
+        if (t2c) g.trace2[(crec * 9 + vwarp) * 4 + 1] = clock64();
         const StageDesc &ds = desc[stage];
         const uint32_t flags = ds.flags;
-        if (g.trace && threadIdx.x == 0 && !traced) {
-            g.trace[blockIdx.x * 4 + 1] = global_timer();
+        if (DBG && g.trace && vwarp == 0 && lane == 0 && !traced) {
+            g.trace[trace_slot * 4 + 1] = global_timer();
             traced = true;
         }
         if (flags & EX_EXIT) break;
@@ -395,7 +357,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
             // fine4: a task the planner found dead runs no micro product (and counts none)
             const uint32_t dead = FINE ? ((kk < 2 ? dead01 : dead23) >> (16 * (kk & 1))) : 0u;
             const uint32_t live = lw & 0xFFFFu & ~dead;
-            if (!((live >> (2 * warp)) & 3u) || (g.dbg & 2)) continue;
+            if (!((live >> (2 * vwarp)) & 3u) || (DBG && (g.dbg & 2))) continue;
             const bool mine = (live >> mypos) & 1u;
             // leaf (r,c) of a block sits at index popc(present & below(morton4(r,c)))
             const float *As = Ablk + __popc(a_present & ((1u << step_pos(di, kk)) - 1u)) * SPAMM_REC;
@@ -413,7 +375,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
                     on |= (__dmul_rn((double)sa.w, (double)sb.w) >= g.tau) ? 8u : 0u;
                 }
                 executed += __popc(on);
-                if (g.gates && ((lw >> mypos) & 1u)) {
+                if (DBG && g.gates && ((lw >> mypos) & 1u)) {
                     // evidence for the tests: bit r*16 + p*4 + q of the task's word (numeric.py:233-238)
                     unsigned long long bits = 0ull;
 #pragma unroll
@@ -483,6 +445,8 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
             seg_done = ds.rec + 1u;
         }
         __syncwarp();
+        if (t2c) g.trace2[(crec * 9 + vwarp) * 4 + 2] = clock64();
+        ++crec;
         if (lane == 0) mbar_arrive(&empty_bar[stage]);
         if (++stage == nstages) { stage = 0; phase ^= 1u; }
         if (flags & EX_CHAIN_OUT) {
@@ -561,7 +525,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_MIN_BLOCKS) execute_kernel(Exec
             }
         }
     }
-    if (g.trace && threadIdx.x == 0) g.trace[blockIdx.x * 4 + 2] = global_timer();
+    if (DBG && g.trace && vwarp == 0 && lane == 0) g.trace[trace_slot * 4 + 2] = global_timer();
     if (FINE) {
         executed = __reduce_add_sync(FULL_MASK, executed);
         if (lane == 0 && executed) atomicAdd(g.counters, (unsigned long long)executed);
@@ -575,10 +539,11 @@ int spamm_execute_grid()
     static const ExecTuning tune = exec_tuning();
     return SPAMM_NUM_SMS * tune.ctas_per_sm;
 }
-int spamm_execute_piece_base() { return SPAMM_NUM_SMS; }
+// teams that draw pieces at the start of the kernel: the planner cuts one round of that many pieces
+int spamm_execute_piece_base() { return spamm_execute_grid() * EX_TEAMS; }
 static ExecTuning exec_tuning()
 {
-    ExecTuning t{3, 2, 0};
+    ExecTuning t{3, EX_CTAS_PER_SM, 0};
     if (const char *e = getenv("SPAMM_EX_STAGES")) t.stages = atoi(e);
     if (const char *e = getenv("SPAMM_EX_CTAS")) t.ctas_per_sm = atoi(e);
     if (const char *e = getenv("SPAMM_EX_DEBUG")) t.dbg = atoi(e);
@@ -603,14 +568,11 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     g.b_values = b->values;
     g.steps = plan->steps;
     g.pieces = plan->tile_order;
-    const int64_t piece_cap = spamm_piece_capacity(plan->leaf_capacity);
-    g.cursor = plan->tile_order + 4 * piece_cap;
     g.counts = plan->counts;
-    // the kernel's shared state: in the planner's workspace when the call comes from spamm_multiply
-    // (untouched by the preceding kernel, so the CTAs of an SM can pair up early), else behind the
-    // plan's cursors
-    g.xs = clean_ptr ? clean_ptr + clean_words : reinterpret_cast<unsigned int *>(plan->tile_order + 5 * piece_cap);
-    g.xs_early = clean_ptr ? 1 : 0;
+    // pieces drawn and teams finished: in the planner's workspace when the call comes from spamm_multiply
+    // (untouched by the preceding kernel, so the first piece can be drawn early), else plan counts [13..14]
+    g.ticket = clean_ptr ? clean_ptr + clean_words : reinterpret_cast<unsigned int *>(plan->counts + 13);
+    g.ticket_early = clean_ptr ? 1 : 0;
     g.chain = plan->chain;
     g.error_flag = plan->counts + 15;
     g.clean_ptr = clean_ptr;
@@ -646,24 +608,42 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     g.nstages = tune.stages;
     g.dbg = tune.dbg;
     const int grid = SPAMM_NUM_SMS * tune.ctas_per_sm;
-    const size_t smem = (size_t)tune.stages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16);
+    const size_t smem = EX_TEAMS * ((size_t)tune.stages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16));
     const bool fine = granularity == SPAMM_FINE4;
-    void (*kern)(ExecArgs) = exact ? (fine ? execute_kernel<true, true> : execute_kernel<true, false>)
-                                   : (fine ? execute_kernel<false, true> : execute_kernel<false, false>);
+    static const char *trace2_path = getenv("SPAMM_EX_TRACE2");   // tuning aids: allocate and synchronise
+    static const char *trace_path = getenv("SPAMM_EX_TRACE");
+    const bool dbg = !exact && (gates || trace_path || trace2_path || tune.dbg);
+    void (*kern)(ExecArgs) = exact ? (fine ? execute_kernel<true, true, false> : execute_kernel<true, false, false>)
+                             : dbg ? (fine ? execute_kernel<false, true, true> : execute_kernel<false, false, true>)
+                                   : (fine ? execute_kernel<false, true, false> : execute_kernel<false, false, false>);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return SPAMM_ECUDA;
     g.trace = nullptr;
-    static const char *trace_path = getenv("SPAMM_EX_TRACE");     // tuning aid: allocates and synchronises
-    if (trace_path && cudaMalloc(&g.trace, sizeof(unsigned long long) * 4 * grid) != cudaSuccess) g.trace = nullptr;
-    if (g.trace) cudaMemsetAsync(g.trace, 0, sizeof(unsigned long long) * 4 * grid, st);
+    g.trace2 = nullptr;
+    const size_t trace2_words = (size_t)EX_TRACE2_RECORDS * 9 * 4;
+    if (trace2_path && cudaMalloc(&g.trace2, 8 * trace2_words) == cudaSuccess) cudaMemsetAsync(g.trace2, 0, 8 * trace2_words, st);
+    const int nslots = grid * EX_TEAMS;
+    if (trace_path && cudaMalloc(&g.trace, sizeof(unsigned long long) * 4 * nslots) != cudaSuccess) g.trace = nullptr;
+    if (g.trace) cudaMemsetAsync(g.trace, 0, sizeof(unsigned long long) * 4 * nslots, st);
     if (spamm_launch_pdl(kern, dim3(grid), dim3(EX_THREADS), smem, st, g) != cudaSuccess)
         return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
-    if (g.trace) {
-        unsigned long long *h = (unsigned long long *)malloc(sizeof(unsigned long long) * 4 * grid);
+    if (g.trace2) {
+        long long *h = (long long *)malloc(8 * trace2_words);
         cudaStreamSynchronize(st);
-        cudaMemcpy(h, g.trace, sizeof(unsigned long long) * 4 * grid, cudaMemcpyDeviceToHost);
+        cudaMemcpy(h, g.trace2, 8 * trace2_words, cudaMemcpyDeviceToHost);
+        if (FILE *f = fopen(trace2_path, "w")) {
+            for (size_t x = 0; x < trace2_words; x += 4) fprintf(f, "%zu %zu %lld %lld %lld\n", x / 36, (x / 4) % 9, h[x], h[x + 1], h[x + 2]);
+            fclose(f);
+        }
+        free(h);
+        cudaFree(g.trace2);
+    }
+    if (g.trace) {
+        unsigned long long *h = (unsigned long long *)malloc(sizeof(unsigned long long) * 4 * nslots);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, g.trace, sizeof(unsigned long long) * 4 * nslots, cudaMemcpyDeviceToHost);
         if (FILE *f = fopen(trace_path, "w")) {
-            for (int x = 0; x < grid; ++x)
+            for (int x = 0; x < nslots; ++x)
                 fprintf(f, "%d %llu %llu %llu %llu\n", x, h[4 * x], h[4 * x + 1], h[4 * x + 2], h[4 * x + 3]);
             fclose(f);
         }

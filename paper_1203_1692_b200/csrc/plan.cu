@@ -51,8 +51,8 @@ struct PlanShared {
     unsigned int order_ticket;
     unsigned int tile_counter[PLAN_MAX_LEVELS + 1];
     int32_t counts[PLAN_MAX_LEVELS + 1][2];   // (nodes, candidates) per level
-    unsigned int exec_shared[EXEC_SHARED_WORDS];   // the numeric kernel's shared state (ExecShared, execute.cu) when
-                                                   // it runs inside spamm_multiply: zero between launches
+    unsigned int exec_ticket[2];              // the numeric kernel's pieces drawn / teams finished when it runs
+                                              // inside spamm_multiply: zero between launches
 };
 
 // ---- start level: dense enumeration by one block ---------------------------------------
@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
     const uint32_t kk = lane % sub;              // my k inside the block
     const uint32_t grp = (lane / sub) * sub;     // first lane of my group
     unsigned long long tasks_total = 0;
+    uint32_t tiles_total = 0;            // super-tiles with at least one record
     if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6] = plan_timer();
     // dense start with no more tiles than blocks: block b takes tile b, no hand-out counter
     const bool fixed_tiles = DENSE && a.all_resident && ntiles <= (int)gridDim.x;
@@ -464,6 +465,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
         const uint32_t nleaves = __popc(present);
         if (lane == 0) {
             s_wsteps[warp] = nsteps; s_wleaves[warp] = nleaves; s_wtasks[warp] = nheavy; tasks_total += ntasks;
+            tiles_total += nsteps > 0 ? 1u : 0u;
         }
         __syncthreads();
         if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 3] = plan_timer();
@@ -581,21 +583,31 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
         }
     }
     if (lane == 0 && tasks_total) atomicAdd(reinterpret_cast<unsigned long long *>(a.counts + 6), tasks_total);
+    if (lane == 0 && tiles_total) atomicAdd(a.counts + 1, (int32_t)tiles_total);
     __syncthreads();
     if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 5] = plan_timer();
 }
 
-// Partition of the record stream for the numeric kernel.  The records (tile after tile, in Morton
-// order) are cut into P pieces of equal weight (live tasks + rec_weight per record), one per SM (or a
-// few rounds of them for a large product, so that the SMs work on neighbouring super-tiles at any time
-// and share operand blocks in L2).  A piece is the four record indices (b, mb, me, e): [mb, me) are
-// whole super-tiles, [me, e) is the head of a tile that the next piece finishes (run FIRST, its
-// accumulators are handed on through C's value records), [b, mb) is the tail of a tile the previous
-// piece began (run LAST, when its head is long finished).  A piece inside a single tile has
-// mb = me = e.  The CTAs that are resident on one SM share one piece, tile by tile, through the piece's
-// cursor (execute.cu): two CTAs on an SM do not advance equally, SMs do.  The thread that looks at a
-// tile places the cuts that fall into it: cut g is the first record boundary at which the weight
-// prefix reaches g W / P.
+// Work units of the numeric kernel, claimed by its teams from one counter in the order given here.
+// The records (tile after tile, in Morton order) form two regions.
+//   Region A, the bulk: P pieces of equal weight (live tasks + rec_weight per record), one per team
+//   (or a few rounds of them for a large product, so that the teams work on neighbouring super-tiles
+//   at any time and share operand blocks in L2).  A piece is the four record indices (b, mb, me, e):
+//   [mb, me) are whole super-tiles, [me, e) is the head of a tile that the next piece finishes (run
+//   FIRST, its accumulators are handed on through C's value records), [b, mb) is the tail of a tile
+//   the previous piece began (run LAST, when its head is long finished).  A piece inside a single
+//   tile has mb = me = e.  This is McNaughton's wrap-around rule for preemptive scheduling, with the
+//   split tile's two parts at opposite ends of the two teams' time lines so that the ascending-k
+//   order of a tile's records is kept.  The thread that looks at a tile places the cuts that fall into
+//   it: cut g is the first record boundary at which the weight prefix reaches g W_A / P.
+//   Region B, the last tiles (about a quarter of the work, at least 1.25 tiles per team): no model of
+//   a team's speed is exact, so the teams do not finish their pieces together; the tiles of B are cut
+//   into a long first segment and up to two short ones, handed out in LAYERS -- all first segments,
+//   then all second ones, then all third ones -- so that a segment's predecessor was claimed a
+//   whole layer earlier and is finished when its successor starts.  The same (b, mb, me, e) form:
+//   a first segment is a head (or a whole tile), a later one a tail.
+#define ORDER_MAX_B_NODES 4096      // region B: at most this many super-tile nodes (block 0 lays them out)
+#define ORDER_MAX_SEGS 3
 struct OrderArgs {
     const int32_t *tile_off;
     const unsigned long long *tile_wprefix;
@@ -605,10 +617,11 @@ struct OrderArgs {
     PlanShared *shared;
     uint32_t *ws_tail;            // workspace prefix behind PlanShared (look-back states), left zero
     int64_t ws_tail_words;
-    int32_t *pieces;              // plan.tile_order: 4 ints per piece, then one cursor per piece, then the
-                                  // numeric kernel's shared state (EXEC_SHARED_WORDS, zero between launches)
+    int32_t *pieces;              // plan.tile_order: 4 ints per piece
     int64_t piece_capacity;
-    int num_sms, piece_records, rec_weight;
+    int num_teams, piece_records, rec_weight;
+    int tail_records;             // region B: records per short segment (0: no region B)
+    int tail_percent;             // region B: its share of the work (at least 1.25 tiles per team anyway)
     int fine_weight;              // dead tasks (fine4 classification) weigh nothing
     int32_t *chain;
     int64_t leaf_capacity;
@@ -647,34 +660,67 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
     const unsigned long long T = a.tile_wprefix[counts[11]];
     const unsigned long long RW = (unsigned long long)a.rec_weight;
     const unsigned long long W = T + RW * (unsigned long long)R;
-    // pieces: one per SM, or several rounds of them when the product is large
-    long long rounds = R / ((long long)a.num_sms * a.piece_records);
+    // ---- region B: where it begins (every block finds the same answer)
+    __shared__ int s_lo, s_hi;
+    const int n_tiles = counts[2] ? 0 : counts[1];
+    auto wnode = [&](int i) -> unsigned long long { return a.tile_wprefix[i] + RW * (unsigned long long)tile_off[i]; };
+    int idxB = n_nodes;
+    // room in the plan: half of the unit slots for region A, the rest for up to three units per node of B
+    const int max_b_nodes = (int)(a.piece_capacity / 6 < ORDER_MAX_B_NODES ? a.piece_capacity / 6 : ORDER_MAX_B_NODES);
+    if (a.tail_records > 0 && n_tiles > 0 && R > 0 && max_b_nodes > 0) {
+        unsigned long long wB = (unsigned long long)((unsigned __int128)W * (unsigned long long)a.tail_percent / 100ull);
+        const unsigned long long wmin = (unsigned long long)((unsigned __int128)W * (unsigned long long)(a.num_teams + a.num_teams / 4) /
+                                                             (unsigned long long)n_tiles);
+        if (wB < wmin) wB = wmin;
+        const unsigned long long targetA = wB >= W ? 0ull : W - wB;
+        // largest node index whose weight prefix is <= targetA: 256-ary search over the monotone prefix
+        int lo = 0, hi = n_nodes;              // answer in [lo, hi]
+        while (hi - lo > 1) {
+            const long long span = hi - lo;
+            const int probe = lo + (int)((span * (t + 1)) / 257);
+            const bool le = probe > lo && probe < hi && wnode(probe) <= targetA;
+            __syncthreads();
+            if (t == 0) { s_lo = lo; s_hi = hi; }
+            __syncthreads();
+            if (probe > lo && probe < hi) {
+                if (le) atomicMax(&s_lo, probe);
+                else atomicMin(&s_hi, probe);
+            }
+            __syncthreads();
+            lo = s_lo; hi = s_hi;
+            if (span <= 257) break;             // every interior point was probed
+        }
+        idxB = lo;
+        if (n_nodes - idxB > max_b_nodes) idxB = n_nodes - max_b_nodes;
+    }
+    const long long RA = idxB < n_nodes ? tile_off[idxB] : R;        // records of region A
+    const unsigned long long WA = idxB < n_nodes ? wnode(idxB) : W;
+    // ---- region A: pieces, one per team, or several rounds of them when the product is large
+    long long rounds = RA / ((long long)a.num_teams * a.piece_records);
     if (rounds < 1) rounds = 1;
     if (rounds > 64) rounds = 64;
-    if (rounds * a.num_sms > a.piece_capacity) rounds = a.piece_capacity / a.num_sms;
-    const long long P = R > 0 ? (rounds >= 1 ? rounds * a.num_sms : a.piece_capacity) : 0;
+    const int64_t cap_a = a.piece_capacity - (int64_t)ORDER_MAX_SEGS * max_b_nodes;
+    if (rounds * a.num_teams > cap_a) rounds = cap_a / a.num_teams;
+    const long long P = RA > 0 ? (rounds >= 1 ? rounds * a.num_teams : cap_a) : 0;
     int32_t *__restrict__ pw = a.pieces;
     // weight prefix at which cut g is placed (at least 1, so that every cut falls into some tile)
     auto target_of = [&](long long g) -> unsigned long long {
-        const unsigned long long x = (unsigned long long)((unsigned __int128)g * W / (unsigned long long)P);
+        const unsigned long long x = (unsigned long long)((unsigned __int128)g * WA / (unsigned long long)P);
         return x < 1ull ? 1ull : x;
     };
-    // cursors and the numeric kernel's shared state start at zero
-    for (int64_t x = gtid; x < P; x += gsz) pw[4 * a.piece_capacity + x] = 0;
-    for (int64_t x = gtid; x < EXEC_SHARED_WORDS; x += gsz) pw[5 * a.piece_capacity + x] = 0;
     if (gtid == 0 && P > 0) {
-        pw[0] = 0;                       // unit 0 begins at record 0, on a tile start
+        pw[0] = 0;                       // piece 0 begins at record 0, on a tile start
         pw[1] = 0;
-        pw[4 * (P - 1) + 2] = (int32_t)R;   // the last unit ends with the last record, on a tile end
-        pw[4 * (P - 1) + 3] = (int32_t)R;
+        pw[4 * (P - 1) + 2] = (int32_t)RA;  // the last piece ends with the last record of region A, on a tile end
+        pw[4 * (P - 1) + 3] = (int32_t)RA;
     }
-    for (int idx = (int)gtid; idx < n_nodes && P > 1; idx += (int)gsz) {
+    for (int idx = (int)gtid; idx < idxB && P > 1; idx += (int)gsz) {
         const int ts = tile_off[idx], te = tile_off[idx + 1];
         if (te == ts) continue;
         const unsigned long long w0 = a.tile_wprefix[idx] + RW * (unsigned long long)ts;
         const unsigned long long w1 = a.tile_wprefix[idx + 1] + RW * (unsigned long long)te;
         // cuts g with w0 < target(g) <= w1 fall into this tile
-        long long g = (long long)((unsigned __int128)w0 * (unsigned long long)P / W);
+        long long g = (long long)((unsigned __int128)w0 * (unsigned long long)P / WA);
         if (g < 1) g = 1;
         while (g < P && target_of(g) <= w0) ++g;
         if (g >= P || target_of(g) > w1) continue;
@@ -694,10 +740,10 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
                 if (target_of(g) > acc) break;
                 const int c = r + 1;
                 const bool clean = c == te;
-                pw[4 * g + 0] = c;                     // b of unit g
-                pw[4 * g + 1] = clean ? c : te;        // mb of unit g (overridden below if it ends in this tile)
-                pw[4 * (g - 1) + 3] = c;               // e of unit g - 1
-                if (prev_here) {                       // unit g - 1 lies inside this tile: one segment
+                pw[4 * g + 0] = c;                     // b of piece g
+                pw[4 * g + 1] = clean ? c : te;        // mb of piece g (overridden below if it ends in this tile)
+                pw[4 * (g - 1) + 3] = c;               // e of piece g - 1
+                if (prev_here) {                       // piece g - 1 lies inside this tile: one segment
                     pw[4 * (g - 1) + 1] = c;
                     pw[4 * (g - 1) + 2] = c;
                 } else {
@@ -708,18 +754,64 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
             }
         }
     }
+    // ---- region B: layered segments, laid out by block 0
+    __shared__ int s_layer[ORDER_MAX_SEGS + 1], s_hist[ORDER_MAX_SEGS + 1], s_cur[ORDER_MAX_SEGS + 1];
+    __shared__ long long s_units;
+    if (t <= ORDER_MAX_SEGS) { s_hist[t] = 0; s_cur[t] = 0; }
+    __syncthreads();
+    if (blockIdx.x == 0) {
+        const int sl = a.tail_records > 0 ? a.tail_records : 1;
+        // segments of a tile of ns records: ns <= sl: 1; ns <= 2 sl: 2 (ns - sl, sl); else 3 (ns - 2 sl, sl, sl)
+        auto segs_of = [&](int ns) -> int { return ns <= 0 ? 0 : (ns <= sl ? 1 : (ns <= 2 * sl ? 2 : 3)); };
+        for (int idx = idxB + t; idx < n_nodes; idx += blockDim.x) atomicAdd(&s_hist[segs_of(tile_off[idx + 1] - tile_off[idx])], 1);
+        __syncthreads();
+        if (t == 0) {
+            // layer l holds the tiles with more than l segments; inside a layer tiles are ranked by
+            // segment count, most first, so that those tiles are a prefix of the ranking
+            int base = 0;
+            for (int l = 0; l < ORDER_MAX_SEGS; ++l) {
+                int cnt = 0;
+                for (int n = l + 1; n <= ORDER_MAX_SEGS; ++n) cnt += s_hist[n];
+                s_layer[l] = base;
+                base += cnt;
+            }
+            s_layer[ORDER_MAX_SEGS] = base;
+            int start = 0;
+            for (int n = ORDER_MAX_SEGS; n >= 1; --n) { s_cur[n] = start; start += s_hist[n]; }
+        }
+        __syncthreads();
+        for (int idx = idxB + t; idx < n_nodes; idx += blockDim.x) {
+            const int ts = tile_off[idx], te = tile_off[idx + 1], ns = te - ts;
+            const int nseg = segs_of(ns);
+            if (nseg == 0) continue;
+            const int rank = atomicAdd(&s_cur[nseg], 1);
+            int sb = ts;
+            for (int l = 0; l < nseg; ++l) {
+                const int se = l + 1 == nseg ? te : (l == 0 ? te - (nseg - 1) * sl : sb + sl);
+                int32_t *u = pw + 4 * (P + s_layer[l] + rank);
+                if (l == 0) { u[0] = sb; u[1] = sb; u[2] = nseg == 1 ? se : sb; u[3] = se; }   // whole tile, or head [me, e)
+                else { u[0] = sb; u[1] = se; u[2] = se; u[3] = se; }                           // tail [b, mb)
+                sb = se;
+            }
+        }
+        if (t == 0) s_units = P + s_layer[ORDER_MAX_SEGS];
+    }
+    __syncthreads();
+    const long long units = blockIdx.x == 0 ? s_units : 0;
     if (a.defer_clean) {
         // the numeric kernel that follows returns the shared planner state to zero (its first block,
         // once this kernel has completed); the counts are final already, block 0 publishes them
         if (blockIdx.x == 0 && t < SPAMM_PLAN_COUNTS) {
             int32_t v = 0;
-            if (t == 0 || t == 2 || t == 3 || t == 4 || t == 6 || t == 7 || t == 11) v = counts[t];
-            if (t == 5) v = (int32_t)P;
-            if (t == 12) v = (int32_t)rounds;
+            if (t == 0 || t == 1 || t == 2 || t == 3 || t == 4 || t == 6 || t == 7 || t == 11) v = counts[t];
+            if (t == 5) v = (int32_t)units;
+            if (t == 12) v = (int32_t)P;
             a.counts[t] = v;
         }
         return;
     }
+    // block 0 knows the number of units: it leaves it where the last block finds it
+    if (blockIdx.x == 0 && t == 0) counts[5] = (int32_t)units, counts[12] = (int32_t)P;
     // the last block publishes the counts and leaves the shared planner state zero for the next plan
     __threadfence();
     __syncthreads();
@@ -729,9 +821,7 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
     __threadfence();
     if (t < SPAMM_PLAN_COUNTS) {
         int32_t v = 0;
-        if (t == 0 || t == 2 || t == 3 || t == 4 || t == 6 || t == 7 || t == 11) v = counts[t];
-        if (t == 5) v = (int32_t)P;
-        if (t == 12) v = (int32_t)rounds;
+        if (t == 0 || t == 1 || t == 2 || t == 3 || t == 4 || t == 5 || t == 6 || t == 7 || t == 11 || t == 12) v = counts[t];
         a.counts[t] = v;
     }
     __syncthreads();
@@ -740,7 +830,7 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
 }
 
 // ---- host side ---------------------------------------------------------------------------------
-int spamm_execute_piece_base();     // pieces per round = SMs that run the numeric kernel (execute.cu)
+int spamm_execute_piece_base();     // pieces per round = teams of the numeric kernel (execute.cu)
 
 static int plan_env(const char *name, int dflt, int lo, int hi)
 {
@@ -927,7 +1017,9 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     // tuning aids: records per piece from which a product is cut into several rounds of pieces,
     // and the weight of a record (in tasks) in the balance
     static const int piece_records = plan_env("SPAMM_PIECE_RECORDS", 192, 1, 1 << 20);
-    static const int rec_weight = plan_env("SPAMM_REC_WEIGHT", 6, 1, 64);
+    static const int rec_weight = plan_env("SPAMM_REC_WEIGHT", 32, 1, 256);
+    static const int tail_records = plan_env("SPAMM_TAIL_RECORDS", 3, 0, 64);
+    static const int tail_percent = plan_env("SPAMM_TAIL_PERCENT", 25, 0, 100);
     if (t.trace) {
         unsigned long long *h = (unsigned long long *)malloc(8 * 6 * tgrid);
         cudaStreamSynchronize(st);
@@ -945,9 +1037,9 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     oa.defer_clean = (cgrid != nullptr && clean_words) ? 1 : 0;
     if (clean_words) {
         *clean_ptr = reinterpret_cast<uint32_t *>(w.shared);
-        // everything before exec_shared: the numeric kernel's CTAs use that part before they wait for
-        // this kernel, and its last CTA to exit leaves it zero
-        *clean_words = oa.defer_clean ? (int)(offsetof(PlanShared, exec_shared) / 4) : 0;
+        // everything before exec_ticket: the numeric kernel's teams draw their first piece from it before
+        // they wait for this kernel, and the last team to finish leaves it zero
+        *clean_words = oa.defer_clean ? (int)(offsetof(PlanShared, exec_ticket) / 4) : 0;
     }
     oa.tile_off = out->tile_off;
     oa.tile_wprefix = w.tile_wprefix;
@@ -961,7 +1053,9 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     }
     oa.pieces = out->tile_order;
     oa.piece_capacity = spamm_piece_capacity(out->leaf_capacity);
-    oa.num_sms = spamm_execute_piece_base(); oa.piece_records = piece_records; oa.rec_weight = rec_weight;
+    oa.num_teams = spamm_execute_piece_base(); oa.piece_records = piece_records; oa.rec_weight = rec_weight;
+    oa.tail_records = tail_records;
+    oa.tail_percent = tail_percent;
     oa.fine_weight = t.fine_weight;
     oa.chain = out->chain;
     oa.leaf_capacity = out->leaf_capacity;

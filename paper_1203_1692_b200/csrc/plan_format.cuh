@@ -51,11 +51,8 @@ __host__ __device__ __forceinline__ uint32_t step_colmask(int dj)
     return dj == 0 ? 0x0505u : dj == 1 ? 0x0A0Au : dj == 2 ? 0x5050u : 0xA0A0u;
 }
 
-// plan.tile_order holds, in ints: 4 per piece (b, mb, me, e) for piece_capacity pieces, then one cursor per
-// piece, then EXEC_SHARED_WORDS words of state shared by the CTAs of the numeric kernel (ExecShared,
-// execute.cu).  Everything behind the pieces is zero between launches.
-#define EXEC_SHARED_WORDS 1024
+// plan.tile_order holds 4 ints per piece (b, mb, me, e), see plan_order_kernel
 __host__ __device__ __forceinline__ int64_t spamm_piece_capacity(int64_t leaf_capacity)
 {
-    return (leaf_capacity + SPAMM_UNIT_EXTRA - EXEC_SHARED_WORDS) / 5;
+    return (leaf_capacity + SPAMM_UNIT_EXTRA) / 4;
 }

@@ -21,3 +21,9 @@ fl = 128 * k.products4 if gran == "fine4" else 8192 * len(plan)
 print(json.dumps({"env": {k_: v for k_, v in os.environ.items() if k_.startswith("SPAMM_")}, "workload": name, "n": int(a.shape[0]), "tau": tau,
                   "gran": gran, "steps": plan.n_steps, "tasks": len(plan), "kernel_ms": round(ms, 4),
                   "tflops": round(fl / ms / 1e9, 2), "frac": round(fl / ms / 1e9 / 74.45, 3)}))
+if os.environ.get("SPAMM_EX_TRACE"):
+    # for the weight model of the planner's partition: the pieces and per-record work of this plan
+    units = int(plan.counts[5].item())
+    pieces = plan.tile_order[: 4 * units].cpu().numpy().reshape(units, 4)
+    rec = plan.step_records()
+    np.savez(os.environ["SPAMM_EX_TRACE"] + ".plan.npz", pieces=pieces, rec=rec)

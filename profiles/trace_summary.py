@@ -3,7 +3,7 @@ import sys
 import numpy as np
 d = np.loadtxt(sys.argv[1], dtype=np.int64)
 t0 = d[:, 1].min()
-start, first, end, units = d[:, 1] - t0, d[:, 2] - t0, d[:, 3] - t0, d[:, 4]
+start, first, end, units = d[:, 1] - t0, d[:, 2] - t0, d[:, 3] - t0, d[:, 4] & 0xFFFFFFFF
 print(f"CTAs {len(d)}  units/CTA min {units.min()} mean {units.mean():.2f} max {units.max()}")
 print(f"start   : max {start.max() / 1e3:.1f} us")
 print(f"1st data: mean {first.mean() / 1e3:.1f} us  max {first.max() / 1e3:.1f} us")

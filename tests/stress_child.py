@@ -28,5 +28,5 @@ for gran in ("fine4", "coarse16"):
     pieces = int(plan.counts[5].item())
     u = plan.tile_order[: 4 * pieces].cpu().numpy().reshape(pieces, 4)
     chained = int(np.count_nonzero(u[:, 0] < u[:, 1]))       # pieces that begin inside a super-tile
-    print(f"{gran}: pieces={pieces} rounds={int(plan.counts[12].item())} chained={chained} ")
+    print(f"{gran}: units={pieces} pieces={int(plan.counts[12].item())} chained={chained} ")
 print("OK")

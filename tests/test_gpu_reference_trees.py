@@ -32,7 +32,7 @@ class RefLikeTree:
         ln = t.leaf_norm
         for x, k in enumerate(t.keys.tolist()):
             ii, jj = (int(i[x]), int(j[x])) if i is not None else _decode(k)
-            q._leaves[int(k)] = (t.values[x].copy(), t.subnorms[x].copy(), float(ln[ii, jj]))
+            q._leaves[int(k)] = (t.values[x].reshape(16, 16).copy(), t.subnorms[x].reshape(4, 4).copy(), float(ln[ii, jj]))
         return q
 
     def packed_leaves(self):
@@ -50,7 +50,7 @@ class RefLikeTree:
         self._rev += 1
 
     def put_leaf(self, key, values):
-        self._leaves[int(key)] = (np.ascontiguousarray(values, np.float32), None, 0.0)
+        self._leaves[int(key)] = (np.ascontiguousarray(values, np.float32), np.zeros((4, 4), np.float32), 0.0)
         self._rev += 1
 
     def compute_norms(self):

@@ -17,9 +17,9 @@ SETTINGS = [
     {"SPAMM_EX_CTAS": "1", "SPAMM_PIECE_RECORDS": "1"},                  # as many pieces as fit: most are 1-2 records inside one tile
     {"SPAMM_EX_CTAS": "1", "SPAMM_PIECE_RECORDS": "3", "SPAMM_REC_WEIGHT": "1"},
     {"SPAMM_EX_CTAS": "1", "SPAMM_EX_STAGES": "2", "SPAMM_PIECE_RECORDS": "2", "SPAMM_REC_WEIGHT": "64"},
-    {"SPAMM_PIECE_RECORDS": "1000000"},                                  # one piece per SM
+    {"SPAMM_PIECE_RECORDS": "1000000"},                                  # one piece per team
     {"SPAMM_PDL": "0", "SPAMM_EX_CTAS": "1", "SPAMM_PIECE_RECORDS": "2"},
-    # a grid larger than what is resident (3 CTAs per SM requested, 2 fit) with chained pieces: a CTA only
+    # a grid larger than what is resident (3 CTAs per SM requested, 1 fits) with chained pieces: a team only
     # waits for the head of a piece that was drawn, and therefore begun, before its own
     {"SPAMM_EX_CTAS": "3", "SPAMM_PIECE_RECORDS": "1", "N": "4096"},
 ]
