@@ -598,15 +598,20 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
 
     mine_tree = parallel.tree_from_shard(m, n, mine)       # the resident form of the local rows, as at N = 1
 
+    # the headline step: everything about the exchange that needs the host is prepared once (ShardedMultiply);
+    # the step is exchange (asynchronous) + interior rows meanwhile + the remaining rows afterwards
+    chosen = "auto" if args.exchange == "auto" else args.exchange
+    sm = parallel.ShardedMultiply(mine, None, (m, n), (m, n), cfg, splits=splits, exchange=chosen, overlap=True,
+                                  a_tree=mine_tree)
+
     def step_resident():
-        return parallel.multiply_sharded(mine, None, (m, n), (m, n), cfg, exchange=args.exchange, splits=splits,
-                                         a_tree=mine_tree)
+        return sm.run()
 
     host_out = {}
 
     def step_e2e():
         shard = parallel.shard_from_dense_rows(host_rows, r0)
-        c, plan, counters = parallel.multiply_sharded(shard, None, (m, n), (m, n), cfg, exchange=args.exchange,
+        c, plan, counters = parallel.multiply_sharded(shard, None, (m, n), (m, n), cfg, exchange=sm.exchange,
                                                       splits=splits)
         nc = c.nleaf                         # this rank's product leaves, read back as packed leaves
         if host_out.get("vals") is None or host_out["vals"].shape[0] < nc:
@@ -636,10 +641,21 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
 
     l0 = _lib.launch_count()
     with ClockSampler(local) as clocks:
-        ms, (c, plan, counters) = timed(step_resident, args.steps, args.warmup)
+        ms, parts = timed(step_resident, args.steps, args.warmup)
     launches = (_lib.launch_count() - l0) * args.steps // (args.steps + args.warmup)
-    work = torch.tensor([float(counters.products4), float(len(plan)), float(r1 - r0), float(c.nleaf)],
-                        dtype=torch.float64, device="cuda")
+    work = torch.tensor([float(sum(k.products4 for _, _, _, k in parts)), float(sum(len(p) for _, _, p, _ in parts)),
+                         float(r1 - r0), float(sum(c.nleaf for _, c, _, _ in parts))], dtype=torch.float64, device="cuda")
+
+    # the alternatives beside it, each prepared the same way (N > 1 only: with one rank they coincide)
+    variants = {}
+    if world > 1:
+        for label, ex, ov in (("allgather", "all", False), ("allgather_overlap", "all", True),
+                              ("needed", "needed", False), ("needed_overlap", "needed", True)):
+            alt = parallel.ShardedMultiply(mine, None, (m, n), (m, n), cfg, splits=splits, exchange=ex, overlap=ov,
+                                           a_tree=mine_tree)
+            t_alt, _ = timed(alt.run, max(2, min(args.steps, 10)), 3)
+            variants[label] = {"ms_per_step": t_alt}
+            del alt
     per_rank = [torch.zeros_like(work) for _ in range(world)]
     dist.all_gather(per_rank, work)
     tot_p4 = sum(float(w[0]) for w in per_rank)
@@ -662,7 +678,12 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
             "config": {"workload": name, "n": m, "tau": args.tau, "granularity": args.granularity,
                        "tasks": int(tot_tasks), "products4": int(tot_p4),
                        "parallelism": f"row blocks of A and C x{world} cut by task count; exchange of B inside the timed "
-                                      f"region: {'all-gather' if args.exchange == 'all' else 'needed leaf rows only'} (NCCL)",
+                                      f"region: {'all-gather' if sm.exchange == 'all' else 'needed leaf rows only'} (NCCL, "
+                                      f"{'chosen automatically, ' if args.exchange == 'auto' else ''}rank 0 needs "
+                                      f"{sm.need_fraction:.2f} of B's leaf rows), interior rows {sm.interior} of {sm.rows} "
+                                      "multiplied while the exchange is in flight",
+                       "with_exchange": {"ms_per_step": ms, "exchange": sm.exchange, "overlap": True},
+                       "exchange_variants": variants,
                        "without_exchange": {"ms_per_step": local_ms, "value": flops / (local_ms * 1e-3) / 1e9,
                                             "note": "B already replicated, trees prebuilt: the local multiply alone"},
                        "tasks_per_rank": [int(w[1]) for w in per_rank],
@@ -715,8 +736,9 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
-    ap.add_argument("--exchange", default=os.environ.get("SPAMM_EXCHANGE", "all"), choices=("all", "needed"),
-                    help="N > 1: bring all of B to every rank (all-gather) or only the leaf rows it reaches")
+    ap.add_argument("--exchange", default=os.environ.get("SPAMM_EXCHANGE", "auto"), choices=("auto", "all", "needed"),
+                    help="N > 1: bring all of B to every rank (all-gather), only the leaf rows it reaches, or decide "
+                         "by the share of B the rank needs (auto: needed when below half)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -193,7 +193,7 @@ typedef struct {
  * [12] records per segment (0: every unit is a whole super-tile), [13..14] the numeric kernel's
  * hand-out and exit counters (zero between launches), [15] set by the numeric kernel if a wait for
  * a chained segment ever gives up (a scheduling bug, never in a correct run): results invalid */
-#define SPAMM_PLAN_COUNTS 16
+#define SPAMM_PLAN_COUNTS 32
 typedef struct {
     spamm_step *steps;       /* [step_capacity]                                   */
     uint32_t *c_keys;        /* [leaf_capacity] product leaf keys, ascending      */
@@ -309,6 +309,19 @@ int spamm_compose(const float *prod_values, const float *old_values,
                   const int32_t *idx_prod, const int32_t *idx_old, int64_t nout,
                   float alpha, float beta, int alpha_is_one, int beta_is_one,
                   float *out_values, void *stream);
+
+/* ---- multi-GPU: the exchange step of the row-block split (no counterpart in the reference) ---- */
+
+/* Every rank holds the stored leaves of its block of leaf rows; C's rows are split like A's and every
+ * product leaf has one owner, so the only exchange is bringing B's leaves to the rank.  This is the
+ * all-gather form: each rank contributes `cap` slots (its leaves first, unused slots carry the key
+ * 0xFFFFFFFF) of keys, 272-float records and leaf square sums; rank r's part lands at slot r * cap of
+ * the outputs, on which spamm_index_leaves + spamm_build_interior then build the tree of B, and
+ * spamm_multiply with the rank's rows of A (or row0, row1) yields the rank's rows of C.  nccl_comm is
+ * the caller's ncclComm_t; NCCL is looked up in the running process, not linked. */
+int spamm_exchange_allgather(void *nccl_comm, const uint32_t *keys, const float *records,
+                             const double *leaf_sq, int64_t cap, uint32_t *out_keys, float *out_records,
+                             double *out_leaf_sq, void *stream);
 
 #ifdef __cplusplus
 }

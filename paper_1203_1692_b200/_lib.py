@@ -53,7 +53,7 @@ class ArenaLayout(C.Structure):
 
 REC = 272           # floats per stored leaf record: 256 values + 16 sub-block norms
 STEP_WORDS = 16     # uint32 words per step record (struct spamm_step)
-PLAN_COUNTS = 16
+PLAN_COUNTS = 32
 UNIT_EXTRA = 8192   # SPAMM_UNIT_EXTRA: tile_order holds leaf_capacity + UNIT_EXTRA units, then the chain flags
 
 
@@ -87,6 +87,7 @@ SIGNATURES = {
     "spamm_multiply_arena_layout": (C.c_int, [C.c_int, C.c_int, i64, i64, C.POINTER(ArenaLayout)]),
     "spamm_multiply_arena": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, C.c_int, C.c_int, f32, i32, i32,
                                        C.c_int, i64, i64, vp, sz, vp, sz, vp]),
+    "spamm_exchange_allgather": (C.c_int, [vp, vp, vp, vp, i64, vp, vp, vp, vp]),
     "spamm_union_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp, sz, vp]),
     "spamm_compose": (C.c_int, [vp, vp, vp, vp, i64, f32, f32, C.c_int, C.c_int, vp, vp]),
 }

@@ -48,26 +48,25 @@
 #define EX_BLOCK_BYTES (16 * SPAMM_REC_BYTES)     // one 4x4 block of leaf records
 #define EX_TRACE2_RECORDS 96
 
+// A stage's descriptor: the step record as it is in the plan (one store per lane of the producer), the
+// shared-memory addresses of the staged leaves, and what the producer adds (run flags, record index).
 struct __align__(16) StageDesc {
-    uint32_t live[4];      // live tasks per kk (one 16-byte read)
-    uint32_t flags;        // STEP_FIRST | STEP_LAST | EX_EXIT | EX_CHAIN_*
-    uint32_t c_base;
-    uint32_t present;      // product leaves of the super-tile
-    uint32_t a_present;    // stored leaves of the staged A block, bit morton4(di,kk)
-    uint32_t b_present;    // stored leaves of the staged B block, bit morton4(kk,dj)
-    uint32_t tile;         // Morton index of the super-tile
-    uint32_t rec;          // index of the record in the plan
-    uint32_t pad;
-    uint32_t dead[2];      // fine4: live tasks none of whose micro products runs (spamm_step.dead)
-    uint32_t pad2[2];
+    spamm_step rec;        // kblock, flags, c_base, tile, a_first, a_present, b_first, b_present, live[4], present, dead[2], len|pos
+    // shared-memory addresses (32-bit, shared window) of the staged leaves, written by the producer so that
+    // the consumers do no index arithmetic: a_leaf[di][kk] = leaf A(di, kk), b_leaf[dj][kk] = leaf B(kk, dj)
+    uint32_t a_leaf[4][4];
+    uint32_t b_leaf[4][4];
+    uint32_t flags;        // rec.flags | EX_EXIT | EX_CHAIN_*
+    uint32_t index;        // index of the record in the plan
+    uint32_t pad[2];
 };
 
 struct ExecArgs {
     const float *a_values_t;
     const float *b_values;
     const spamm_step *steps;
-    const int32_t *pieces;       // plan.tile_order: (b, mb, me, e) per piece, see plan_order_kernel
-    const int32_t *counts;       // plan counts (device): [5] = number of pieces
+    const int32_t *pieces;       // plan.tile_order: the work units (b, e), see plan_order_kernel
+    const int32_t *counts;       // plan counts (device): [12] pieces of region A, [16..21] ranges of region B
     int32_t *chain;              // per product leaf: the record up to which its partial sums are handed on (0 = none)
     unsigned int *ticket;        // [0] pieces drawn, [1] teams that ran out of work; zero between launches
     int ticket_early;            // the tickets are not touched by the preceding kernel: draw before waiting for it
@@ -113,6 +112,12 @@ __device__ __forceinline__ double ex_row_sq(float4 v)
     return r;
 }
 
+// generic pointer to a 32-bit shared-window address
+__device__ __forceinline__ const float *shared_ptr(uint32_t addr)
+{
+    return reinterpret_cast<const float *>(__cvta_shared_to_generic((size_t)addr));
+}
+
 // Two C elements of one column (rows 2h, 2h+1) advance together: packed FP32 (sm_100 FFMA2 with a
 // broadcast scalar operand) halves the issue slots the multiply-accumulates take.  EXACT rounds the
 // product and the sum separately (numeric.py:252-259) with scalar FMUL + FADD.
@@ -142,6 +147,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
     const int team = EX_TEAMS == 1 ? 0 : (warp & 1);
     const int vwarp = EX_TEAMS == 1 ? warp : (warp >> 1);          // 0 .. 7 consumers, 8 = the team's producer
     const size_t team_bytes = (size_t)nstages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16);
+    static_assert(sizeof(StageDesc) == 208 && sizeof(spamm_step) == 64, "StageDesc layout");
     unsigned char *tbase = smem_raw + (size_t)team * team_bytes;
     unsigned char *sA = tbase;
     unsigned char *sB = tbase + (size_t)nstages * EX_BLOCK_BYTES;
@@ -180,41 +186,86 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
             if (lane == 0) piece = (int)atomicAdd(g.ticket, 1u);
             piece = __shfl_sync(FULL_MASK, piece, 0);
         }
-        const int npieces = g.counts[2] ? 0 : g.counts[5];      // an overflowed plan is incomplete: do nothing
+        const bool plan_ok = g.counts[2] == 0;                  // an overflowed plan is incomplete: do nothing
+        // unit slots: region A's pieces [0, P), then region B's five ranges, range x at P + x * stride with nr[x] in use
+        const int P = plan_ok ? g.counts[12] : 0, stride = g.counts[21];
+        int nr[5];
+#pragma unroll
+        for (int x = 0; x < 5; ++x) nr[x] = plan_ok ? g.counts[16 + x] : 0;
         const int first_piece = piece;
         const uint32_t *words = reinterpret_cast<const uint32_t *>(g.steps);
-        const int4 *pieces = reinterpret_cast<const int4 *>(g.pieces);
-        // cursor over the records of my pieces: per piece the head segment [me, e), the whole tiles
-        // [mb, me), the tail segment [b, mb).  The next piece is drawn two records before the cursor
-        // leaves the current one, so the latency of the draw hides behind the staged records.
-        int run = -1, r = 0, rend = 0, rbeg = 0, left = 0, units_done = 0, next_piece = 0;
-        bool drawn = false, more = piece < npieces;
-        int4 pd = make_int4(0, 0, 0, 0);
-        if (more) {
-            pd = __ldg(pieces + piece);
-            left = pd.w - pd.x;
-        }
+        const int2 *units = reinterpret_cast<const int2 *>(g.pieces);
+        auto slot_of = [&](int t) -> int {          // claim number -> unit slot, -1 = no work left
+            if (t < P) return t;
+            t -= P;
+#pragma unroll
+            for (int x = 0; x < 5; ++x) {
+                if (t < nr[x]) return P + x * stride + t;
+                t -= nr[x];
+            }
+            return -1;
+        };
+        // Cursor over the records of my units.  A unit [b, e) is run as: the head segment [me, e) of a tile
+        // that the next unit finishes, the whole tiles [mb, me), the tail segment [b, mb) of a tile another
+        // unit began; mb and me follow from the first and the last record's tile length and position.
+        // The next unit is claimed in three steps while the last three records of the current one are
+        // fetched (counter, unit, its end records), so that none of the latencies is exposed.
+        int run = 2, r = 0, rend = 0, rbeg = 0, left = 0, units_done = 0;
+        int ub = 0, umb = 0, ume = 0, ue = 0;
+        int cstate = 1, tk = piece;               // 0: nothing claimed, 1: counter drawn, 2: unit loaded, 3: end records loaded, 4: no work left
+        int2 nu = make_int2(0, 0);
+        uint32_t wf = 0, wl = 0;
+        bool more = true;
+        auto claim_step = [&]() {
+            if (cstate == 0) {
+                if (lane == 0) tk = (int)atomicAdd(g.ticket, 1u);
+                cstate = 1;
+            } else if (cstate == 1) {
+                const int slot = slot_of(__shfl_sync(FULL_MASK, tk, 0));
+                if (slot < 0) cstate = 4;
+                else { nu = __ldg(units + slot); cstate = 2; }
+            } else if (cstate == 2) {
+                if (nu.y > nu.x) {
+                    wf = __ldg(words + (size_t)nu.x * 16 + 15);
+                    wl = __ldg(words + (size_t)(nu.y - 1) * 16 + 15);
+                }
+                cstate = 3;
+            }
+        };
         // fetch: the next record of the cursor -> (word of lane l < 16, meta); meta = rec | first << 30 | last << 31, ~0 = none
         auto fetch = [&](uint32_t &wd, uint32_t &meta) {
+            if (left > 3 && r + 1 < rend) {        // the common case: well inside a run, nothing to claim yet
+                wd = lane < 16 ? __ldg(words + (size_t)r * 16 + lane) : 0u;
+                meta = (uint32_t)r | (r == rbeg ? (1u << 30) : 0u);
+                ++r;
+                --left;
+                return;
+            }
             for (;;) {
                 if (!more) { wd = 0u; meta = 0xFFFFFFFFu; return; }
-                if (!drawn && left <= 2) {
-                    if (lane == 0) next_piece = (int)atomicAdd(g.ticket, 1u);
-                    drawn = true;
-                }
+                if (cstate < 3 && left <= 3 - cstate) claim_step();
                 if (r < rend) break;
                 ++run;
                 if (run == 3) {
-                    piece = __shfl_sync(FULL_MASK, next_piece, 0);
-                    drawn = false;
-                    if (piece >= npieces) { more = false; continue; }
-                    pd = __ldg(pieces + piece);
-                    left = pd.w - pd.x;
+                    while (cstate < 3) claim_step();
+                    if (cstate == 4) { more = false; continue; }
+                    ub = nu.x; ue = nu.y;
+                    umb = ub; ume = ue;
+                    if (ue > ub) {
+                        const int pos_b = (int)(wf >> 16), len_b = (int)(wf & 0xFFFFu);
+                        const int pos_l = (int)(wl >> 16), len_l = (int)(wl & 0xFFFFu);
+                        const int ts_l = ue - 1 - pos_l;
+                        umb = pos_b == 0 ? ub : min(ub - pos_b + len_b, ue);
+                        ume = ts_l + len_l == ue ? ue : max(ts_l, umb);
+                    }
+                    left = ue - ub;
+                    cstate = 0;
                     run = 0;
+                    ++units_done;
                 }
-                if (run == 0) { ++units_done; r = pd.z; rend = pd.w; }
-                else if (run == 1) { r = pd.y; rend = pd.z; }
-                else { r = pd.x; rend = pd.y; }
+                if (run == 0) { r = ume; rend = ue; }
+                else if (run == 1) { r = umb; rend = ume; }
+                else { r = ub; rend = umb; }
                 rbeg = r;
             }
             wd = lane < 16 ? __ldg(words + (size_t)r * 16 + lane) : 0u;
@@ -231,29 +282,31 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
 #pragma unroll
             for (int x = 0; x + 1 < EX_PREFETCH; ++x) { w[x] = w[x + 1]; m[x] = m[x + 1]; }
             fetch(w[EX_PREFETCH - 1], m[EX_PREFETCH - 1]);
-            const uint32_t na = __popc(__shfl_sync(FULL_MASK, cur, 5));
-            const uint32_t nb = __popc(__shfl_sync(FULL_MASK, cur, 7));
+            const uint32_t ap = __shfl_sync(FULL_MASK, cur, 5), bp = __shfl_sync(FULL_MASK, cur, 7);   // a_present, b_present
             const bool t2p = DBG && g.trace2 && blockIdx.x == 0 && team == 0 && prec < EX_TRACE2_RECORDS && lane == 0;
             if (t2p) g.trace2[(prec * 9 + 8) * 4 + 0] = clock64();
             mbar_wait(&empty_bar[stage], phase ^ 1u);
             if (t2p) g.trace2[(prec * 9 + 8) * 4 + 1] = clock64();
             uint32_t *d = reinterpret_cast<uint32_t *>(&desc[stage]);
+            if (lane < 16) d[lane] = cur;                    // the record itself
             if (lane == 1) {                                 // flags: a run that starts or ends inside a tile is chained
                 uint32_t f = cur;
                 if ((meta >> 30 & 1u) && !(cur & STEP_FIRST)) f |= EX_CHAIN_IN;
                 if ((meta >> 31 & 1u) && !(cur & STEP_LAST)) f |= EX_CHAIN_OUT;
-                d[4] = f;
+                d[48] = f;
+                d[49] = meta & 0x3FFFFFFFu;                  // record index
             }
-            if (lane == 15) d[10] = meta & 0x3FFFFFFFu;      // record index
-            if (lane == 13 || lane == 14) d[lane - 1] = cur; // dead[0..1]
-            if (lane == 2) d[5] = cur;                       // c_base
-            if (lane == 12) d[6] = cur;                      // present
-            if (lane == 3) d[9] = cur;                       // tile
-            if (lane == 5) d[7] = cur;                       // a_present
-            if (lane == 7) d[8] = cur;                       // b_present
-            if (lane >= 8 && lane < 12) d[lane - 8] = cur;   // live[kk]
+            {
+                // leaf (r,c) of a block sits at index popc(present & below(morton4(r,c)))
+                const int x = (int)(lane & 15u) >> 2, kk = (int)(lane & 3u);
+                const uint32_t idx = lane < 16 ? __popc(ap & ((1u << step_pos(x, kk)) - 1u))
+                                               : __popc(bp & ((1u << step_pos(kk, x)) - 1u));
+                const unsigned char *base = (lane < 16 ? sA : sB) + (size_t)stage * EX_BLOCK_BYTES;
+                d[16 + lane] = smem_u32(base) + idx * SPAMM_REC_BYTES;
+            }
             __syncwarp();
             const bool copy = !(DBG && (g.dbg & 1));
+            const uint32_t na = __popc(ap), nb = __popc(bp);
             if (lane == 0) mbar_arrive_expect_tx(&full_bar[stage], copy ? (na + nb) * SPAMM_REC_BYTES : 0u);
             __syncwarp();
             if (copy && lane == 4)
@@ -317,10 +370,10 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
             chained = true;
             // continue a tile another CTA started: wait for its segment, then take the partial sums
             // from C's value record (written below under EX_CHAIN_OUT); L1 is bypassed
-            const uint32_t present_in = ds.present;
+            const uint32_t present_in = ds.rec.present;
             if ((present_in >> mypos) & 1u) {
-                const int64_t cs = (int64_t)ds.c_base + __popc(present_in & ((1u << mypos) - 1u));
-                const int want = (int)ds.rec;      // the records before this one are in the partial sums
+                const int64_t cs = (int64_t)ds.rec.c_base + __popc(present_in & ((1u << mypos) - 1u));
+                const int want = (int)ds.index;    // the records before this one are in the partial sums
                 // the predecessor belongs to a CTA that started earlier and runs it first; the bound
                 // only turns a scheduling bug into an error flag instead of a hang
                 for (unsigned spins = 0; ld_acquire_gpu(g.chain + cs) != want; ++spins) {
@@ -342,14 +395,14 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
                 }
             }
         }
-        const uint32_t a_present = ds.a_present, b_present = ds.b_present;
-        const float *Ablk = reinterpret_cast<const float *>(sA + (size_t)stage * EX_BLOCK_BYTES);
-        const float *Bblk = reinterpret_cast<const float *>(sB + (size_t)stage * EX_BLOCK_BYTES);
-        const uint4 live4 = *reinterpret_cast<const uint4 *>(ds.live);
+        // where my A leaves (row di) and B leaves (column dj) of the four k sit in shared memory
+        const uint4 a_at = *reinterpret_cast<const uint4 *>(ds.a_leaf[di]);
+        const uint4 b_at = *reinterpret_cast<const uint4 *>(ds.b_leaf[dj]);
+        const uint4 live4 = *reinterpret_cast<const uint4 *>(ds.rec.live);
         uint32_t dead01 = 0u, dead23 = 0u;
         if (FINE) {
-            dead01 = ds.dead[0];
-            dead23 = ds.dead[1];
+            dead01 = ds.rec.dead[0];
+            dead23 = ds.rec.dead[1];
         }
 #pragma unroll     // all four k unrolled: +4-5 % (their addresses become constants), measured
         for (int kk = 0; kk < 4; ++kk) {
@@ -359,9 +412,8 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
             const uint32_t live = lw & 0xFFFFu & ~dead;
             if (!((live >> (2 * vwarp)) & 3u) || (DBG && (g.dbg & 2))) continue;
             const bool mine = (live >> mypos) & 1u;
-            // leaf (r,c) of a block sits at index popc(present & below(morton4(r,c)))
-            const float *As = Ablk + __popc(a_present & ((1u << step_pos(di, kk)) - 1u)) * SPAMM_REC;
-            const float *Bs = Bblk + __popc(b_present & ((1u << step_pos(kk, dj)) - 1u)) * SPAMM_REC;
+            const float *As = shared_ptr(kk == 0 ? a_at.x : kk == 1 ? a_at.y : kk == 2 ? a_at.z : a_at.w);
+            const float *Bs = shared_ptr(kk == 0 ? b_at.x : kk == 1 ? b_at.y : kk == 2 ? b_at.z : b_at.w);
             uint32_t on = 0;       // bit r: micro product (p,q,r) of my task runs
             if (FINE) {
                 if (mine && ((lw >> (16 + mypos)) & 1u)) {
@@ -381,7 +433,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
 #pragma unroll
                     for (int r = 0; r < 4; ++r)
                         if ((on >> r) & 1u) bits |= 1ull << (r * 16 + t16);
-                    if (bits) atomicOr(g.gates + ((size_t)ds.rec * 64 + kk * 16 + mypos), bits);
+                    if (bits) atomicOr(g.gates + ((size_t)ds.index * 64 + kk * 16 + mypos), bits);
                 }
             } else {
                 on = mine ? 15u : 0u;
@@ -389,7 +441,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
             // Fast path (the common case away from the band edge): every lane runs all four r or
             // none, so the 16 k of the task form one branch-free block and the compiler overlaps the
             // shared-memory reads of r+1 with the multiplies of r.
-            if (__all_sync(FULL_MASK, on == 15u || on == 0u)) {
+            if (!FINE || __all_sync(FULL_MASK, on == 15u || on == 0u)) {
                 if (on) {
 #pragma unroll
                     for (int r = 0; r < 4; ++r) {
@@ -439,10 +491,10 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
         }
         uint32_t c_base = 0, present = 0, tile_id = 0, seg_done = 0;
         if (flags & (STEP_LAST | EX_CHAIN_OUT)) {
-            c_base = ds.c_base;
-            tile_id = ds.tile;
-            present = ds.present;
-            seg_done = ds.rec + 1u;
+            c_base = ds.rec.c_base;
+            tile_id = ds.rec.tile;
+            present = ds.rec.present;
+            seg_done = ds.index + 1u;
         }
         __syncwarp();
         if (t2c) g.trace2[(crec * 9 + vwarp) * 4 + 2] = clock64();

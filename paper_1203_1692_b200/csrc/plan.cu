@@ -305,7 +305,16 @@ struct TileArgs {
     uint32_t *c_keys;
     int32_t *tile_off;
     int64_t cap_steps, cap_leaves;
-    int32_t *counts;          // plan counts, see spamm_b200.h
+    int32_t *counts;          // plan counts, see spamm_b200.h (accumulated in the workspace)
+    int32_t *out_counts;      // the caller's plan counts
+    // cleared here, while the first loads of the walk are in flight: the numeric kernel's per-leaf hand-over
+    // flags and (optional) C's leaf grids, which its epilogue fills
+    int32_t *chain;
+    int64_t chain_words;
+    int64_t cells;
+    int32_t *c_slot, *c_slot_t;
+    float *c_norm, *c_norm_t;
+    double *c_leaf_sq_grid;
     unsigned int *tile_counter;
     volatile unsigned long long *tile_state;
 };
@@ -320,8 +329,8 @@ struct LaneTests {
     uint32_t dead;       // live tasks of which none passes
 };
 
-// leaf norms of A(sub*I+d, k) and B(k, sub*J+d), -1 = absent; and their sub-norm range words
-struct LaneNorms { float na[4], nb[4]; uint32_t sa[4], sb[4]; };
+// leaf norms of A(sub*I+d, k) and B(k, sub*J+d), -1 = absent
+struct LaneNorms { float na[4], nb[4]; };
 
 __device__ __forceinline__ LaneNorms tile_norms(const TileArgs &a, uint32_t I, uint32_t J, uint32_t k, bool valid)
 {
@@ -330,20 +339,19 @@ __device__ __forceinline__ LaneNorms tile_norms(const TileArgs &a, uint32_t I, u
     for (int d = 0; d < 4; ++d) {
         n.na[d] = -1.0f;
         n.nb[d] = -1.0f;
-        n.sa[d] = n.sb[d] = 0xFFFFFFFFu;
         if (valid && d < a.sub) {
             n.na[d] = __ldg(a.norm_a + (int64_t)(a.sub * I + d) * a.L + k);
             n.nb[d] = __ldg(a.norm_bt + (int64_t)(a.sub * J + d) * a.L + k);
-            if (a.sub_a) {
-                n.sa[d] = __ldg(a.sub_a + (int64_t)(a.sub * I + d) * a.L + k);
-                n.sb[d] = __ldg(a.sub_bt + (int64_t)(a.sub * J + d) * a.L + k);
-            }
         }
     }
     return n;
 }
 
-__device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, const LaneNorms &n, uint32_t rowok)
+// WITH_SUB: also classify the live tasks from the sub-norm ranges of their leaves (loaded here, only by
+// lanes that have a live task; not prefetched -- the registers are better spent on the norms)
+template <bool WITH_SUB>
+__device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, const LaneNorms &n, uint32_t rowok, uint32_t I = 0,
+                                                uint32_t J = 0, uint32_t k = 0)
 {
     LaneTests t{0u, 0u, 0u, 0u, 0u};
 #pragma unroll
@@ -355,18 +363,31 @@ __device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, const LaneNor
     for (int di = 0; di < 4; ++di)
 #pragma unroll
         for (int dj = 0; dj < 4; ++dj)
-            if ((rowok >> di & 1u) && norm_test(n.na[di], n.nb[dj], a.tau)) {
-                t.live |= 1u << step_pos(di, dj);
-                if (a.sub_a) {
+            if ((rowok >> di & 1u) && norm_test(n.na[di], n.nb[dj], a.tau)) t.live |= 1u << step_pos(di, dj);
+    if (WITH_SUB && a.sub_a && t.live) {
+        uint32_t sa[4], sb[4];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+            sa[d] = sb[d] = 0xFFFFFFFFu;
+            if (d < a.sub) {
+                sa[d] = __ldg(a.sub_a + (int64_t)(a.sub * I + d) * a.L + k);
+                sb[d] = __ldg(a.sub_bt + (int64_t)(a.sub * J + d) * a.L + k);
+            }
+        }
+#pragma unroll
+        for (int di = 0; di < 4; ++di)
+#pragma unroll
+            for (int dj = 0; dj < 4; ++dj)
+                if (t.live >> step_pos(di, dj) & 1u) {
                     // lower bounds of the smallest, upper bounds of the largest sub-norm of either leaf
                     // (NaN for a leaf that cannot be classified: every comparison is then false)
-                    const float mna = __uint_as_float(n.sa[di] << 16), mxa = __uint_as_float(n.sa[di] & 0xFFFF0000u);
-                    const float mnb = __uint_as_float(n.sb[dj] << 16), mxb = __uint_as_float(n.sb[dj] & 0xFFFF0000u);
+                    const float mna = __uint_as_float(sa[di] << 16), mxa = __uint_as_float(sa[di] & 0xFFFF0000u);
+                    const float mnb = __uint_as_float(sb[dj] << 16), mxb = __uint_as_float(sb[dj] & 0xFFFF0000u);
                     if (norm_test(mna, mnb, a.tau)) t.full |= 1u << step_pos(di, dj);
                     else if (mxa >= 0.0f && mxb >= 0.0f && __dmul_rn((double)mxa, (double)mxb) < a.tau)
                         t.dead |= 1u << step_pos(di, dj);
                 }
-            }
+    }
     return t;
 }
 
@@ -392,6 +413,20 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
     const uint32_t grp = (lane / sub) * sub;     // first lane of my group
     unsigned long long tasks_total = 0;
     uint32_t tiles_total = 0;            // super-tiles with at least one record
+    if (blockIdx.x == 0 && threadIdx.x < 8) a.out_counts[16 + threadIdx.x] = 0;     // accumulated by plan_order_kernel
+    {
+        const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gsz = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t x = gtid; x < a.chain_words; x += gsz) a.chain[x] = 0;
+        if (a.c_slot) {
+            for (int64_t x = gtid; x < a.cells; x += gsz) {
+                a.c_slot[x] = -1;
+                a.c_slot_t[x] = -1;
+                a.c_norm[x] = -1.0f;
+                a.c_norm_t[x] = -1.0f;
+                a.c_leaf_sq_grid[x] = 0.0;
+            }
+        }
+    }
     if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6] = plan_timer();
     // dense start with no more tiles than blocks: block b takes tile b, no hand-out counter
     const bool fixed_tiles = DENSE && a.all_resident && ntiles <= (int)gridDim.x;
@@ -437,15 +472,14 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
         uint32_t nsteps = 0, present = 0, ntasks = 0, nheavy = 0;
         // the norms of the next pass are fetched before the tests of the current one
         LaneNorms nrm = tile_norms(a, I, J, (s + (int)lane / sub < e) ? sub * ks[s + (int)lane / sub] + kk : 0u,
-                                   s + (int)lane / sub < e);
+                                          s + (int)lane / sub < e);
         for (int b = s; b < e; b += per) {
             const int t = b + (int)lane / sub, t2 = t + per;
             const LaneNorms nxt = tile_norms(a, I, J, t2 < e ? sub * ks[t2] + kk : 0u, t2 < e);
             uint32_t live = 0, heavy = 0;
             if (t < e) {
-                const LaneTests tt = tile_tests(a, nrm, rowok);
-                live = tt.live;
-                heavy = a.fine_weight ? (tt.live & ~tt.dead) : tt.live;
+                const LaneTests tt = tile_tests<false>(a, nrm, rowok);
+                live = heavy = tt.live;
             }
             nrm = nxt;
             const uint32_t bal = __ballot_sync(FULL_MASK, live != 0);
@@ -536,7 +570,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
             uint32_t K = 0;
             if (t < e) {
                 K = ks[t];
-                lt4 = tile_tests(a, nrm, rowok);
+                lt4 = tile_tests<true>(a, nrm, rowok, I, J, (uint32_t)sub * K + kk);
             }
             nrm = nxt;
             // gather the group's four lanes: live per kk, stored leaves of both blocks
@@ -577,7 +611,10 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
                 rec[0] = make_uint4(K, flags, (uint32_t)cb, pm);
                 rec[1] = make_uint4(a_first, a_present, b_first, b_present);
                 rec[2] = make_uint4(live4[0], live4[1], live4[2], live4[3]);
-                rec[3] = make_uint4(present, dead4[0] | (dead4[1] << 16), dead4[2] | (dead4[3] << 16), nsteps);
+                // last word: records of this tile | position of this record in it << 16 (tiles have at
+                // most L/4 <= 8192 records), from which the numeric kernel finds the tile's ends
+                rec[3] = make_uint4(present, dead4[0] | (dead4[1] << 16), dead4[2] | (dead4[3] << 16),
+                                    nsteps | ((uint32_t)(x - s_first) << 16));
             }
             sb += __popc(bal & lead_mask);
         }
@@ -589,72 +626,56 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
 }
 
 // Work units of the numeric kernel, claimed by its teams from one counter in the order given here.
+// A unit is a run [b, e) of consecutive step records (two ints in plan.tile_order).  Where a run
+// begins or ends inside a super-tile, the tile's accumulators pass from team to team through C's
+// value records; the numeric kernel works out from the records themselves (tile length and position,
+// last word of spamm_step) which part of a unit is the head of a tile that the next unit finishes
+// (run FIRST), which are whole tiles, and which is the tail of a tile another unit began (run LAST).
 // The records (tile after tile, in Morton order) form two regions.
 //   Region A, the bulk: P pieces of equal weight (live tasks + rec_weight per record), one per team
 //   (or a few rounds of them for a large product, so that the teams work on neighbouring super-tiles
-//   at any time and share operand blocks in L2).  A piece is the four record indices (b, mb, me, e):
-//   [mb, me) are whole super-tiles, [me, e) is the head of a tile that the next piece finishes (run
-//   FIRST, its accumulators are handed on through C's value records), [b, mb) is the tail of a tile
-//   the previous piece began (run LAST, when its head is long finished).  A piece inside a single
-//   tile has mb = me = e.  This is McNaughton's wrap-around rule for preemptive scheduling, with the
-//   split tile's two parts at opposite ends of the two teams' time lines so that the ascending-k
-//   order of a tile's records is kept.  The thread that looks at a tile places the cuts that fall into
-//   it: cut g is the first record boundary at which the weight prefix reaches g W_A / P.
+//   at any time and share operand blocks in L2).  This is McNaughton's wrap-around rule for
+//   preemptive scheduling, with the split tile's two parts at opposite ends of the two teams' time
+//   lines so that the ascending-k order of a tile's records is kept.  One warp looks at one tile and
+//   places the cuts that fall into it: cut g is the first record boundary at which the weight prefix
+//   reaches g W_A / P.
 //   Region B, the last tiles (about a quarter of the work, at least 1.25 tiles per team): no model of
 //   a team's speed is exact, so the teams do not finish their pieces together; the tiles of B are cut
 //   into a long first segment and up to two short ones, handed out in LAYERS -- all first segments,
 //   then all second ones, then all third ones -- so that a segment's predecessor was claimed a
-//   whole layer earlier and is finished when its successor starts.  The same (b, mb, me, e) form:
-//   a first segment is a head (or a whole tile), a later one a tail.
-#define ORDER_MAX_B_NODES 4096      // region B: at most this many super-tile nodes (block 0 lays them out)
+//   whole layer earlier and is finished when its successor starts.  Five ranges of unit slots, range x
+//   at P + x * stride with counts[16 + x] slots in use (counts[21] = stride): the first segments of the
+//   tiles with three, with two segments and the whole tiles (longest first), the second segments, the
+//   third segments; the numeric kernel maps its claim numbers onto the slots in use.
+#define ORDER_MAX_B_NODES 4096      // region B: at most this many super-tile nodes
 #define ORDER_MAX_SEGS 3
 struct OrderArgs {
     const int32_t *tile_off;
     const unsigned long long *tile_wprefix;
     const spamm_step *steps;
     int defer_clean;              // the caller's next kernel clears PlanShared (spamm_multiply)
-    int32_t *counts;              // the caller's plan counts: written here, all SPAMM_PLAN_COUNTS of them
+    int32_t *counts;              // the caller's plan counts: written here
     PlanShared *shared;
     uint32_t *ws_tail;            // workspace prefix behind PlanShared (look-back states), left zero
     int64_t ws_tail_words;
-    int32_t *pieces;              // plan.tile_order: 4 ints per piece
-    int64_t piece_capacity;
+    int32_t *units;               // plan.tile_order: 2 ints per unit
+    int64_t unit_capacity;
     int num_teams, piece_records, rec_weight;
     int tail_records;             // region B: records per short segment (0: no region B)
     int tail_percent;             // region B: its share of the work (at least 1.25 tiles per team anyway)
-    int fine_weight;              // dead tasks (fine4 classification) weigh nothing
-    int32_t *chain;
-    int64_t leaf_capacity;
-    // optional: C's leaf grids, emptied here for the numeric kernel's epilogue to fill
-    int64_t cells;
-    int32_t *slot, *slot_t;
-    float *norm, *norm_t;
-    double *leaf_sq_grid;
 };
 
 __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
 {
     const int32_t *__restrict__ tile_off = a.tile_off;
     int32_t *counts = a.shared->res;
-    int32_t *__restrict__ chain = a.chain;
-    const int64_t leaf_capacity = a.leaf_capacity;
     __shared__ bool s_last;
     pdl_enter();
-    // the numeric kernel's per-leaf hand-over flags start clear; the planner's look-back states are
-    // done with and go back to zero; C's leaf grids start empty
+    // the planner's look-back states are done with and go back to zero
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gsz = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t x = gtid; x < leaf_capacity; x += gsz) chain[x] = 0;
     for (int64_t x = gtid; x < a.ws_tail_words; x += gsz) a.ws_tail[x] = 0u;
-    if (a.slot) {
-        for (int64_t x = gtid; x < a.cells; x += gsz) {
-            a.slot[x] = -1;
-            a.slot_t[x] = -1;
-            a.norm[x] = -1.0f;
-            a.norm_t[x] = -1.0f;
-            a.leaf_sq_grid[x] = 0.0;
-        }
-    }
     const int t = threadIdx.x;
+    const uint32_t lane = lane_id();
     const int n_nodes = counts[2] ? 0 : counts[11];
     const long long R = counts[2] ? 0 : counts[4];
     const unsigned long long T = a.tile_wprefix[counts[11]];
@@ -666,15 +687,20 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
     auto wnode = [&](int i) -> unsigned long long { return a.tile_wprefix[i] + RW * (unsigned long long)tile_off[i]; };
     int idxB = n_nodes;
     // room in the plan: half of the unit slots for region A, the rest for up to three units per node of B
-    const int max_b_nodes = (int)(a.piece_capacity / 6 < ORDER_MAX_B_NODES ? a.piece_capacity / 6 : ORDER_MAX_B_NODES);
-    if (a.tail_records > 0 && n_tiles > 0 && R > 0 && max_b_nodes > 0) {
-        unsigned long long wB = (unsigned long long)((unsigned __int128)W * (unsigned long long)a.tail_percent / 100ull);
-        const unsigned long long wmin = (unsigned long long)((unsigned __int128)W * (unsigned long long)(a.num_teams + a.num_teams / 4) /
-                                                             (unsigned long long)n_tiles);
+    const int max_b_nodes = (int)(a.unit_capacity / 10 < ORDER_MAX_B_NODES ? a.unit_capacity / 10 : ORDER_MAX_B_NODES);
+    // measured (B200): with a piece of several tiles per team the static split alone finishes within a few
+    // per cent; the layered tail is worth its hand-overs only when a team's share is shorter than a tile
+    const int tail_records = a.tail_records >= 0 ? a.tail_records : (R < 8ll * a.num_teams ? 3 : 0);
+    if (tail_records > 0 && n_tiles > 0 && R > 0 && max_b_nodes > 0) {
+        // (64-bit products: a plan's weight stays far below 2^48 -- at most 2^31 records of at most 96 -- and
+        // the factors here below 2^15)
+        unsigned long long wB = W * (unsigned long long)a.tail_percent / 100ull;
+        const unsigned long long wmin = W * (unsigned long long)(a.num_teams + a.num_teams / 4) / (unsigned long long)n_tiles;
         if (wB < wmin) wB = wmin;
         const unsigned long long targetA = wB >= W ? 0ull : W - wB;
         // largest node index whose weight prefix is <= targetA: 256-ary search over the monotone prefix
-        int lo = 0, hi = n_nodes;              // answer in [lo, hi]
+        int lo = n_nodes > max_b_nodes ? n_nodes - max_b_nodes : 0, hi = n_nodes;   // answer in [lo, hi]
+        if (wnode(lo) > targetA) hi = lo;                                           // region B is capped: starts at lo
         while (hi - lo > 1) {
             const long long span = hi - lo;
             const int probe = lo + (int)((span * (t + 1)) / 257);
@@ -691,7 +717,6 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
             if (span <= 257) break;             // every interior point was probed
         }
         idxB = lo;
-        if (n_nodes - idxB > max_b_nodes) idxB = n_nodes - max_b_nodes;
     }
     const long long RA = idxB < n_nodes ? tile_off[idxB] : R;        // records of region A
     const unsigned long long WA = idxB < n_nodes ? wnode(idxB) : W;
@@ -699,119 +724,106 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
     long long rounds = RA / ((long long)a.num_teams * a.piece_records);
     if (rounds < 1) rounds = 1;
     if (rounds > 64) rounds = 64;
-    const int64_t cap_a = a.piece_capacity - (int64_t)ORDER_MAX_SEGS * max_b_nodes;
+    const int64_t cap_a = a.unit_capacity - 5ll * max_b_nodes;
     if (rounds * a.num_teams > cap_a) rounds = cap_a / a.num_teams;
     const long long P = RA > 0 ? (rounds >= 1 ? rounds * a.num_teams : cap_a) : 0;
-    int32_t *__restrict__ pw = a.pieces;
+    int32_t *__restrict__ uw = a.units;
     // weight prefix at which cut g is placed (at least 1, so that every cut falls into some tile)
     auto target_of = [&](long long g) -> unsigned long long {
-        const unsigned long long x = (unsigned long long)((unsigned __int128)g * WA / (unsigned long long)P);
+        const unsigned long long x = (unsigned long long)g * WA / (unsigned long long)P;
         return x < 1ull ? 1ull : x;
     };
     if (gtid == 0 && P > 0) {
-        pw[0] = 0;                       // piece 0 begins at record 0, on a tile start
-        pw[1] = 0;
-        pw[4 * (P - 1) + 2] = (int32_t)RA;  // the last piece ends with the last record of region A, on a tile end
-        pw[4 * (P - 1) + 3] = (int32_t)RA;
+        uw[0] = 0;                              // piece 0 begins at record 0
+        uw[2 * (P - 1) + 1] = (int32_t)RA;      // the last piece ends with region A
     }
-    for (int idx = (int)gtid; idx < idxB && P > 1; idx += (int)gsz) {
+    // one warp per tile: the records' weights in parallel, a warp scan, every lane places the cuts that
+    // fall behind its record (cut g = boundary after the first record at which the prefix reaches target(g))
+    const int64_t gwarp = gtid >> 5, nwarps = gsz >> 5;
+    for (int64_t idx = gwarp; idx < idxB && P > 1; idx += nwarps) {
         const int ts = tile_off[idx], te = tile_off[idx + 1];
         if (te == ts) continue;
         const unsigned long long w0 = a.tile_wprefix[idx] + RW * (unsigned long long)ts;
         const unsigned long long w1 = a.tile_wprefix[idx + 1] + RW * (unsigned long long)te;
-        // cuts g with w0 < target(g) <= w1 fall into this tile
-        long long g = (long long)((unsigned __int128)w0 * (unsigned long long)P / WA);
-        if (g < 1) g = 1;
-        while (g < P && target_of(g) <= w0) ++g;
-        if (g >= P || target_of(g) > w1) continue;
-        unsigned long long acc = w0;
-        bool prev_here = false;
-        for (int r = ts; r < te && g < P; ++r) {
-            const uint4 live = *(reinterpret_cast<const uint4 *>(a.steps + r) + 2);
-            uint32_t d01 = 0u, d23 = 0u;
-            if (a.fine_weight) {
-                const uint4 tail = *(reinterpret_cast<const uint4 *>(a.steps + r) + 3);
-                d01 = tail.y;
-                d23 = tail.z;
+        long long g0 = (long long)(w0 * (unsigned long long)P / WA);
+        if (g0 < 1) g0 = 1;
+        while (g0 < P && target_of(g0) <= w0) ++g0;          // first cut behind w0
+        if (g0 >= P || target_of(g0) > w1) continue;         // no cut in this tile
+        unsigned long long run = w0;
+        for (int base = ts; base < te; base += 32) {
+            const int r = base + (int)lane;
+            unsigned long long wr = 0;
+            if (r < te) {
+                const uint4 live = *(reinterpret_cast<const uint4 *>(a.steps + r) + 2);
+                wr = RW + __popc(live.x & 0xFFFFu) + __popc(live.y & 0xFFFFu) + __popc(live.z & 0xFFFFu) + __popc(live.w & 0xFFFFu);
             }
-            acc += RW + __popc(live.x & 0xFFFFu & ~d01) + __popc(live.y & 0xFFFFu & ~(d01 >> 16)) +
-                   __popc(live.z & 0xFFFFu & ~d23) + __popc(live.w & 0xFFFFu & ~(d23 >> 16));
-            while (g < P) {
-                if (target_of(g) > acc) break;
-                const int c = r + 1;
-                const bool clean = c == te;
-                pw[4 * g + 0] = c;                     // b of piece g
-                pw[4 * g + 1] = clean ? c : te;        // mb of piece g (overridden below if it ends in this tile)
-                pw[4 * (g - 1) + 3] = c;               // e of piece g - 1
-                if (prev_here) {                       // piece g - 1 lies inside this tile: one segment
-                    pw[4 * (g - 1) + 1] = c;
-                    pw[4 * (g - 1) + 2] = c;
-                } else {
-                    pw[4 * (g - 1) + 2] = clean ? c : ts;
+            unsigned long long inc = wr;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned long long y = __shfl_up_sync(FULL_MASK, inc, d);
+                if (lane >= (uint32_t)d) inc += y;
+            }
+            const unsigned long long hi_w = run + inc, lo_w = hi_w - wr;      // prefix after / before my record
+            if (r < te && wr > 0) {
+                long long g = (long long)(lo_w * (unsigned long long)P / WA);
+                if (g < 1) g = 1;
+                while (g < P && target_of(g) <= lo_w) ++g;
+                for (; g < P && target_of(g) <= hi_w; ++g) {
+                    uw[2 * g] = r + 1;                 // b of piece g
+                    uw[2 * (g - 1) + 1] = r + 1;       // e of piece g - 1
                 }
-                prev_here = true;
-                ++g;
             }
+            run += __shfl_sync(FULL_MASK, inc, 31);
         }
     }
-    // ---- region B: layered segments, laid out by block 0
-    __shared__ int s_layer[ORDER_MAX_SEGS + 1], s_hist[ORDER_MAX_SEGS + 1], s_cur[ORDER_MAX_SEGS + 1];
-    __shared__ long long s_units;
-    if (t <= ORDER_MAX_SEGS) { s_hist[t] = 0; s_cur[t] = 0; }
-    __syncthreads();
-    if (blockIdx.x == 0) {
-        const int sl = a.tail_records > 0 ? a.tail_records : 1;
+    // ---- region B: layered segments; every warp takes 32 nodes at a time, slots by one atomic per warp and range.
+    // Five ranges of unit slots, each nB long, handed out in this order: first segments of the tiles with 3,
+    // with 2 segments, whole tiles (longest first inside the first layer), then second, then third segments.
+    const int nB = n_nodes - idxB;                   // range stride
+    if (nB > 0) {
+        const int sl = tail_records > 0 ? tail_records : 1;
         // segments of a tile of ns records: ns <= sl: 1; ns <= 2 sl: 2 (ns - sl, sl); else 3 (ns - 2 sl, sl, sl)
-        auto segs_of = [&](int ns) -> int { return ns <= 0 ? 0 : (ns <= sl ? 1 : (ns <= 2 * sl ? 2 : 3)); };
-        for (int idx = idxB + t; idx < n_nodes; idx += blockDim.x) atomicAdd(&s_hist[segs_of(tile_off[idx + 1] - tile_off[idx])], 1);
-        __syncthreads();
-        if (t == 0) {
-            // layer l holds the tiles with more than l segments; inside a layer tiles are ranked by
-            // segment count, most first, so that those tiles are a prefix of the ranking
-            int base = 0;
-            for (int l = 0; l < ORDER_MAX_SEGS; ++l) {
-                int cnt = 0;
-                for (int n = l + 1; n <= ORDER_MAX_SEGS; ++n) cnt += s_hist[n];
-                s_layer[l] = base;
-                base += cnt;
-            }
-            s_layer[ORDER_MAX_SEGS] = base;
-            int start = 0;
-            for (int n = ORDER_MAX_SEGS; n >= 1; --n) { s_cur[n] = start; start += s_hist[n]; }
-        }
-        __syncthreads();
-        for (int idx = idxB + t; idx < n_nodes; idx += blockDim.x) {
-            const int ts = tile_off[idx], te = tile_off[idx + 1], ns = te - ts;
-            const int nseg = segs_of(ns);
-            if (nseg == 0) continue;
-            const int rank = atomicAdd(&s_cur[nseg], 1);
+        for (int64_t base = idxB + gwarp * 32; base < n_nodes; base += nwarps * 32) {
+            const int64_t idx = base + lane;
+            int ts = 0, te = 0;
+            if (idx < n_nodes) { ts = tile_off[idx]; te = tile_off[idx + 1]; }
+            const int ns = te - ts;
+            const int nseg = ns <= 0 ? 0 : (ns <= sl ? 1 : (ns <= 2 * sl ? 2 : 3));
             int sb = ts;
-            for (int l = 0; l < nseg; ++l) {
-                const int se = l + 1 == nseg ? te : (l == 0 ? te - (nseg - 1) * sl : sb + sl);
-                int32_t *u = pw + 4 * (P + s_layer[l] + rank);
-                if (l == 0) { u[0] = sb; u[1] = sb; u[2] = nseg == 1 ? se : sb; u[3] = se; }   // whole tile, or head [me, e)
-                else { u[0] = sb; u[1] = se; u[2] = se; u[3] = se; }                           // tail [b, mb)
-                sb = se;
+#pragma unroll
+            for (int x = 0; x < 5; ++x) {
+                // range x: segment index l of the tiles with the given number of segments
+                const int l = x < 3 ? 0 : x - 2;
+                const bool in = x < 3 ? nseg == 3 - x : nseg > l;
+                const uint32_t m = __ballot_sync(FULL_MASK, in);
+                if (m == 0) continue;
+                int slot0 = 0;
+                if (lane == (uint32_t)(__ffs(m) - 1)) slot0 = atomicAdd(&a.counts[16 + x], __popc(m));
+                slot0 = __shfl_sync(FULL_MASK, slot0, __ffs(m) - 1);
+                if (in) {
+                    const int se = l + 1 == nseg ? te : (l == 0 ? te - (nseg - 1) * sl : sb + sl);
+                    int32_t *u = uw + 2 * (P + (long long)x * nB + slot0 + __popc(m & lanemask_lt()));
+                    u[0] = sb;
+                    u[1] = se;
+                    sb = se;
+                }
             }
         }
-        if (t == 0) s_units = P + s_layer[ORDER_MAX_SEGS];
     }
-    __syncthreads();
-    const long long units = blockIdx.x == 0 ? s_units : 0;
     if (a.defer_clean) {
         // the numeric kernel that follows returns the shared planner state to zero (its first block,
-        // once this kernel has completed); the counts are final already, block 0 publishes them
-        if (blockIdx.x == 0 && t < SPAMM_PLAN_COUNTS) {
+        // once this kernel has completed); the counts are final already, block 0 publishes them (the
+        // layer counts [16..18] are accumulated in place by all blocks)
+        if (blockIdx.x == 0 && t < 16) {
             int32_t v = 0;
             if (t == 0 || t == 1 || t == 2 || t == 3 || t == 4 || t == 6 || t == 7 || t == 11) v = counts[t];
-            if (t == 5) v = (int32_t)units;
+            if (t == 5) v = (int32_t)(P + 5ll * nB);     // unit slots; [16..20] say how many of region B's are in use
             if (t == 12) v = (int32_t)P;
             a.counts[t] = v;
         }
+        if (blockIdx.x == 0 && t == 0) a.counts[21] = nB;
         return;
     }
-    // block 0 knows the number of units: it leaves it where the last block finds it
-    if (blockIdx.x == 0 && t == 0) counts[5] = (int32_t)units, counts[12] = (int32_t)P;
     // the last block publishes the counts and leaves the shared planner state zero for the next plan
     __threadfence();
     __syncthreads();
@@ -819,11 +831,14 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    if (t < SPAMM_PLAN_COUNTS) {
+    if (t < 16) {
         int32_t v = 0;
-        if (t == 0 || t == 1 || t == 2 || t == 3 || t == 4 || t == 5 || t == 6 || t == 7 || t == 11 || t == 12) v = counts[t];
+        if (t == 0 || t == 1 || t == 2 || t == 3 || t == 4 || t == 6 || t == 7 || t == 11) v = counts[t];
+        if (t == 5) v = (int32_t)(P + 5ll * nB);
+        if (t == 12) v = (int32_t)P;
         a.counts[t] = v;
     }
+    if (t == 0) a.counts[21] = nB;
     __syncthreads();
     uint32_t *sh = reinterpret_cast<uint32_t *>(a.shared);
     for (int x = t; x < (int)(sizeof(PlanShared) / 4); x += blockDim.x) sh[x] = 0u;
@@ -986,7 +1001,8 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     t.slot_bt = b->slot_t;
     t.sub_a = (a->sub && b->sub_t) ? a->sub : nullptr;
     t.sub_bt = (a->sub && b->sub_t) ? b->sub_t : nullptr;
-    t.fine_weight = (fine_weight && t.sub_a) ? 1 : 0;
+    (void)fine_weight;       // the pieces are balanced by live tasks whatever the gating (the layered tail absorbs the rest)
+    t.fine_weight = 0;
     t.L = 1 << depth;
     t.sub = 1 << (depth - tl);
     t.row0 = row0; t.row1 = row1; t.tau = tau;
@@ -1008,6 +1024,18 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     t.tile_state_w = w.tile_state_w;
     t.cap_steps = out->step_capacity; t.cap_leaves = out->leaf_capacity;
     t.counts = res;
+    t.out_counts = out->counts;
+    t.chain = out->chain;
+    t.chain_words = out->leaf_capacity;
+    t.cells = 0;
+    t.c_slot = t.c_slot_t = nullptr; t.c_norm = t.c_norm_t = nullptr; t.c_leaf_sq_grid = nullptr;
+    if (cgrid) {
+        const int64_t off = spamm_level_offset(cgrid->depth);
+        t.cells = int64_t(1) << (2 * cgrid->depth);
+        t.c_slot = cgrid->slot; t.c_slot_t = cgrid->slot_t;
+        t.c_norm = cgrid->norm + off; t.c_norm_t = cgrid->norm_t + off;
+        t.c_leaf_sq_grid = cgrid->leaf_sq_grid;
+    }
     t.tile_counter = &w.shared->tile_counter[PLAN_MAX_LEVELS];
     t.tile_state = w.tile_state[PLAN_MAX_LEVELS];
     if (spamm_launch_pdl(dense ? plan_tiles_kernel<true> : plan_tiles_kernel<false>,
@@ -1018,7 +1046,9 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     // and the weight of a record (in tasks) in the balance
     static const int piece_records = plan_env("SPAMM_PIECE_RECORDS", 192, 1, 1 << 20);
     static const int rec_weight = plan_env("SPAMM_REC_WEIGHT", 32, 1, 256);
-    static const int tail_records = plan_env("SPAMM_TAIL_RECORDS", 3, 0, 64);
+    // region B (the layered tail) pays only when the pieces would otherwise be shorter than a super-tile
+    // (SPAMM_TAIL_RECORDS = -1: decide by the size of the plan; 0: never; n: always, n records per short segment)
+    static const int tail_records = plan_env("SPAMM_TAIL_RECORDS", -1, -1, 64);
     static const int tail_percent = plan_env("SPAMM_TAIL_PERCENT", 25, 0, 100);
     if (t.trace) {
         unsigned long long *h = (unsigned long long *)malloc(8 * 6 * tgrid);
@@ -1051,23 +1081,11 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
         oa.ws_tail = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(ws) + head);
         oa.ws_tail_words = (int64_t)((w.zero_bytes - head) / 4);
     }
-    oa.pieces = out->tile_order;
-    oa.piece_capacity = spamm_piece_capacity(out->leaf_capacity);
+    oa.units = out->tile_order;
+    oa.unit_capacity = spamm_unit_capacity(out->leaf_capacity);
     oa.num_teams = spamm_execute_piece_base(); oa.piece_records = piece_records; oa.rec_weight = rec_weight;
     oa.tail_records = tail_records;
     oa.tail_percent = tail_percent;
-    oa.fine_weight = t.fine_weight;
-    oa.chain = out->chain;
-    oa.leaf_capacity = out->leaf_capacity;
-    oa.cells = 0;
-    oa.slot = oa.slot_t = nullptr; oa.norm = oa.norm_t = nullptr; oa.leaf_sq_grid = nullptr;
-    if (cgrid) {
-        const int64_t off = spamm_level_offset(cgrid->depth);
-        oa.cells = int64_t(1) << (2 * cgrid->depth);
-        oa.slot = cgrid->slot; oa.slot_t = cgrid->slot_t;
-        oa.norm = cgrid->norm + off; oa.norm_t = cgrid->norm_t + off;
-        oa.leaf_sq_grid = cgrid->leaf_sq_grid;
-    }
     if (spamm_launch_pdl(plan_order_kernel, dim3(SPAMM_NUM_SMS), dim3(256), 0, st, oa) != cudaSuccess) return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;

@@ -22,7 +22,7 @@ for kk in range(4):
     for w in range(8):
         passes += ((live >> (2 * w)) & 3) != 0
 cr, ct, cp = (np.concatenate([[0], np.cumsum(x)]) for x in (np.ones(R, np.int64), tasks, passes))
-b, e = pieces[:, 0], pieces[:, 3]
+b, e = pieces[:, 0], pieces[:, -1]
 if len(pieces) != len(tr):
     print("pieces", len(pieces), "teams", len(tr), ": fit needs one round (one piece per team)")
     sys.exit(0)

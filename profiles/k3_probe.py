@@ -22,8 +22,8 @@ print(json.dumps({"env": {k_: v for k_, v in os.environ.items() if k_.startswith
                   "gran": gran, "steps": plan.n_steps, "tasks": len(plan), "kernel_ms": round(ms, 4),
                   "tflops": round(fl / ms / 1e9, 2), "frac": round(fl / ms / 1e9 / 74.45, 3)}))
 if os.environ.get("SPAMM_EX_TRACE"):
-    # for the weight model of the planner's partition: the pieces and per-record work of this plan
-    units = int(plan.counts[5].item())
-    pieces = plan.tile_order[: 4 * units].cpu().numpy().reshape(units, 4)
+    # for the weight model of the planner's partition: the pieces (region A units) and per-record work of this plan
+    npieces = int(plan.counts[12].item())
+    pieces = plan.tile_order[: 2 * npieces].cpu().numpy().reshape(npieces, 2)
     rec = plan.step_records()
     np.savez(os.environ["SPAMM_EX_TRACE"] + ".plan.npz", pieces=pieces, rec=rec)

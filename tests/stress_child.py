@@ -25,8 +25,10 @@ for gran in ("fine4", "coarse16"):
         assert np.array_equal(c.to_dense().data, want), (gran, it, "values")
         for t in range(oc.depth + 1):
             assert np.array_equal(c.level_norms(t), oc.level_norm(t)), (gran, it, "norms", t)
-    pieces = int(plan.counts[5].item())
-    u = plan.tile_order[: 4 * pieces].cpu().numpy().reshape(pieces, 4)
-    chained = int(np.count_nonzero(u[:, 0] < u[:, 1]))       # pieces that begin inside a super-tile
-    print(f"{gran}: units={pieces} pieces={int(plan.counts[12].item())} chained={chained} ")
+    cnt = plan.counts.cpu().numpy()
+    npieces = int(cnt[12])
+    u = plan.tile_order[: 2 * npieces].cpu().numpy().reshape(npieces, 2)
+    flags = plan.step_records()[:, 1]
+    chained = int(np.count_nonzero((flags[u[u[:, 1] > u[:, 0], 0]] & (1 << 16)) == 0))     # pieces that begin inside a super-tile
+    print(f"{gran}: pieces={npieces} ranges={cnt[16:21].tolist()} chained={chained + int(cnt[19]) + int(cnt[20])} ")
 print("OK")

@@ -16,9 +16,13 @@ STEP_FIRST, STEP_LAST = 1 << 16, 1 << 17
 
 
 def _units(plan):
+    """(pieces of region A, [segments of layer 0, 1, 2 of region B], step records) of a device plan."""
     cnt = plan.counts.cpu().numpy()
-    U, P = int(cnt[5]), int(cnt[12])
-    return plan.tile_order[: 4 * U].cpu().numpy().reshape(U, 4).astype(np.int64), P, int(cnt[4])
+    P, n, stride = int(cnt[12]), [int(x) for x in cnt[16:21]], int(cnt[21])
+    raw = plan.tile_order[: 2 * (P + 5 * stride)].cpu().numpy().reshape(-1, 2).astype(np.int64)
+    rng = [raw[P + x * stride: P + x * stride + n[x]] for x in range(5)]
+    # ranges 0..2: first segments of the tiles with 3, 2, 1 segments; 3: second segments; 4: third segments
+    return raw[:P], [np.concatenate(rng[:3]), rng[3], rng[4]], int(cnt[4])
 
 
 @pytest.mark.parametrize("n,tau", [(256, 1e-6), (1024, 1e-6), (2048, 1e-8), (4096, 1e-8), (4096, 1e-4)])
@@ -29,63 +33,53 @@ def test_units_cover_the_plan(n, tau):
     a = inputs.exponential_decay(n, 0.95, seed=0)
     qa = P.QuadtreeMatrix.from_dense(a)
     plan = P.build_plan(qa, qa, tau)
-    units, npieces, R = _units(plan)
-    assert R == plan.n_steps and len(units) >= 1
+    pa, layers, R = _units(plan)
+    assert R == plan.n_steps
     rec = plan.step_records()
     flags = rec[:, 1]
-    b, mb, me, e = units.T
-    assert np.all(b <= mb) and np.all(mb <= me) and np.all(me <= e)
+    units = np.concatenate([pa] + layers)
+    b, e = units.T
+    assert np.all(b <= e)
     # the units tile the record stream: region A's pieces in stream order, then region B's segments
     order = np.lexsort((e, b))
     nz = (e > b)[order]
     bs, es = b[order][nz], e[order][nz]
     assert bs[0] == 0 and es[-1] == R and np.array_equal(es[:-1], bs[1:]), "units must tile the record stream"
-    pa = units[:npieces]
+    npieces = len(pa)
     if npieces:
-        assert pa[0, 0] == 0 and np.array_equal(pa[:-1, 3], pa[1:, 0]), "pieces of region A are contiguous"
-    RA = int(pa[-1, 3]) if npieces else 0
+        assert pa[0, 0] == 0 and np.array_equal(pa[:-1, 1], pa[1:, 0]), "pieces of region A are contiguous"
+    RA = int(pa[-1, 1]) if npieces else 0
     first = np.concatenate([(flags & STEP_FIRST) != 0, [True]])     # index R counts as a tile start
     assert first[RA], "region B begins on a tile boundary"
-    # whole-tile range: begins and ends on tile boundaries
-    nzw = mb < me
-    assert np.all(first[mb[nzw]]) and np.all(first[me[nzw]])
-    # a head segment begins on a tile start and does not reach the tile's end
-    hd = me < e
-    assert np.all(first[me[hd]]) and not np.any(flags[e[hd] - 1] & STEP_LAST)
-    # a tail segment begins inside a tile; it ends with the tile unless the whole unit lies inside one tile
-    tl = b < mb
-    assert not np.any(first[b[tl]])
-    ends_tile = (flags[mb[tl] - 1] & STEP_LAST) != 0
-    single = (mb[tl] == me[tl]) & (me[tl] == e[tl])
-    assert np.all(ends_tile | single)
-    # no record of a segment crosses a tile boundary
-    for lo, hi in list(zip(me[hd], e[hd])) + list(zip(b[tl], mb[tl])):
-        assert not np.any(flags[lo + 1:hi] & STEP_FIRST)
-    # every record knows how many records its tile has
+    # every record knows how many records its tile has and where in the tile it sits
     starts = np.flatnonzero(flags & STEP_FIRST)
     lens = np.diff(np.concatenate([starts, [R]]))
-    assert np.array_equal(rec[:, 15], np.repeat(lens, lens))
-    # region A: equal weights; weight = live tasks that are not known dead + rec_weight per record (default 32)
+    assert np.array_equal(rec[:, 15] & 0xFFFF, np.repeat(lens, lens))
+    assert np.array_equal(rec[:, 15] >> 16, np.concatenate([np.arange(x) for x in lens]))
+    # region A: equal weights; weight = live tasks + rec_weight per record (default 32)
     w = np.zeros(R, np.int64)
-    dead = [rec[:, 13] & 0xFFFF, rec[:, 13] >> 16, rec[:, 14] & 0xFFFF, rec[:, 14] >> 16]
     for kk in range(4):
-        w += np.array([bin(int(x) & 0xFFFF & ~int(d)).count("1") for x, d in zip(rec[:, 8 + kk], dead[kk])], np.int64)
+        w += np.array([bin(int(x) & 0xFFFF).count("1") for x in rec[:, 8 + kk]], np.int64)
     w += 32
     cw = np.concatenate([[0], np.cumsum(w)])
     if npieces:
-        pw = cw[pa[:, 3]] - cw[pa[:, 0]]
+        pw = cw[pa[:, 1]] - cw[pa[:, 0]]
         assert npieces % (2 * torch.cuda.get_device_properties(0).multi_processor_count) == 0
         assert pw.max() <= cw[RA] / npieces + w.max() + 1, "a piece exceeds its share by more than one record"
-    # region B: layered segments of its tiles -- every later segment is the short kind (2 records),
-    # and a tile's segments appear in the unit list in ascending order, a whole layer apart
-    ub = units[npieces:]
-    later = ub[ub[:, 0] < ub[:, 1]]
-    assert np.all(later[:, 1] - later[:, 0] == 2)
-    nB = int(np.count_nonzero(ub[:, 0] == ub[:, 1]))          # first segments = tiles of region B
-    firsts = ub[:nB]
-    assert np.all(firsts[:, 0] == firsts[:, 1]), "layer 0 holds exactly the first segments"
-    pos = {int(x[0]): i for i, x in enumerate(ub)}              # unit that starts at a record
-    for i, u in enumerate(ub):
-        if u[3] < R and not first[u[3]]:                         # the tile continues: its next segment comes later
-            assert pos[int(u[3])] > i
-    assert cw[R] - cw[RA] >= min(cw[R], cw[R] // 4) - w.max() * 16
+    # region B: every tile is cut into a first segment (layer 0) and up to two short ones of 3 records
+    # (layers 1, 2); a tile's segments sit in consecutive layers
+    l0, l1, l2 = layers
+    assert np.all(first[l0[:, 0]]), "layer 0 holds the first segments"
+    assert len(l0) == int(np.count_nonzero(first[RA:R])), "one first segment per tile of region B"
+    for later in (l1, l2):
+        assert np.all(later[:, 1] - later[:, 0] == 3) and not np.any(first[later[:, 0]])
+    ends0 = set(l0[:, 1].tolist())
+    assert set(l1[:, 0].tolist()) <= ends0 and set(l2[:, 0].tolist()) <= set(l1[:, 1].tolist())
+    for seg in units[npieces:]:
+        assert not np.any(flags[seg[0] + 1:seg[1]] & STEP_FIRST), "a segment stays inside its tile"
+    # region B exists only when a team's share of the records is shorter than a super-tile (8 records)
+    teams = 2 * torch.cuda.get_device_properties(0).multi_processor_count
+    if R < 8 * teams:
+        assert cw[R] - cw[RA] >= min(cw[R], cw[R] // 4) - w.max() * 16
+    else:
+        assert RA == R and not len(l0)

@@ -164,3 +164,81 @@ def test_two_rank_split_reproduces_single_process_product(tmp_path):
     ref = np.stack([plan.ti, plan.tk, plan.tj], axis=1)
     assert np.array_equal(allt[np.lexsort(allt.T[::-1])], ref[np.lexsort(ref.T[::-1])])
     assert p4 == k_ref.products4
+
+
+def test_interior_rows_need_nothing_from_other_ranks():
+    """ShardedMultiply's overlap: the tasks of the interior rows of a rank's block only touch rows of B
+    the rank holds itself (checked against the oracle's task list), and the run is maximal."""
+    n, tau = 1024, 1e-6
+    a = inputs.exponential_decay(n, 0.8, seed=4)
+    full = O.tree_from_dense(a)
+    plan = O.build_plan(full, full, tau)
+    nrows = n // 16
+    whole = _shard_of_oracle_tree(full, 0, nrows)
+    rowmax = parallel.row_max_norms(whole, nrows)
+    assert np.array_equal(rowmax.numpy(), np.where(full.leaf_norm.max(axis=1) > 0, full.leaf_norm.max(axis=1), 0).astype(np.float32))
+    for world in (2, 3):
+        splits = parallel.even_row_split(nrows, world)
+        for rank, (r0, r1) in enumerate(splits):
+            mine = _shard_of_oracle_tree(full, r0, r1)
+            reach = parallel.reaching_leaves(mine, rowmax, tau)
+            # exactly the stored leaves of A that occur in a task
+            mi, mk = morton.decode_array(mine.keys.numpy().astype(np.uint64))
+            in_task = set(zip(plan.ti.tolist(), plan.tk.tolist()))
+            assert [(int(i), int(k)) in in_task for i, k in zip(mi, mk)] == reach.tolist()
+            i0, i1 = parallel.interior_rows(mine, (r0, r1), splits[rank], reach)
+            assert r0 <= i0 <= i1 <= r1 and i0 % parallel.ROW_ALIGN == 0 and (i1 % parallel.ROW_ALIGN == 0 or i1 == r1)
+            assert i1 > i0, "a banded matrix has interior rows"
+            sel = (plan.ti >= i0) & (plan.ti < i1)
+            assert plan.tk[sel].min() >= r0 and plan.tk[sel].max() < r1
+            # maximal: the aligned groups just outside the run have a task that reaches a foreign row
+            for g0 in (i0 - parallel.ROW_ALIGN, i1):
+                if r0 <= g0 and g0 + parallel.ROW_ALIGN <= r1:
+                    sel = (plan.ti >= g0) & (plan.ti < g0 + parallel.ROW_ALIGN)
+                    assert plan.tk[sel].min() < r0 or plan.tk[sel].max() >= r1
+            # the band-limited exchange asks for exactly the (aligned) rows of B the tasks touch
+            need = parallel.needed_rows(mine, nrows, reach).numpy()
+            sel = (plan.ti >= r0) & (plan.ti < r1)
+            want = np.zeros(nrows, bool)
+            want[np.unique(plan.tk[sel])] = True
+            want = want.reshape(-1, parallel.ROW_ALIGN).any(axis=1).repeat(parallel.ROW_ALIGN)
+            assert np.array_equal(need, want)
+
+
+def _layout_worker(rank: int, world: int, port: int, n: int):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = inputs.exponential_decay(n, 0.9, seed=3)
+        full = O.tree_from_dense(a)
+        nrows = -(-n // 16)
+        splits = parallel.even_row_split(nrows, world)
+        r0, r1 = splits[rank]
+        mine = _shard_of_oracle_tree(full, r0, r1)
+        # the prepared (host-sync-free) forms move exactly what the one-shot forms move, and can be reused
+        want = parallel.allgather_shards(mine)
+        lay = parallel.gather_layout(mine)
+        for _ in range(2):
+            got = parallel.allgather_with_layout(mine, lay)
+            assert torch.equal(got.keys, want.keys) and torch.equal(got.leaf_sq, want.leaf_sq)
+            used = want.keys != parallel.HOLE
+            assert torch.equal(got.records[used], want.records[used])
+        got, works = parallel.allgather_with_layout(mine, lay, async_op=True)
+        for w in works:
+            w.wait()
+        assert torch.equal(got.keys, want.keys)
+        need = parallel.needed_rows(mine, nrows)
+        want = parallel.exchange_needed_rows(mine, need, splits)
+        nl = parallel.needed_layout(mine, need, splits)
+        for _ in range(2):
+            got = parallel.exchange_with_layout(mine, nl)
+            assert torch.equal(got.keys, want.keys) and torch.equal(got.records, want.records)
+            assert torch.equal(got.leaf_sq, want.leaf_sq)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_prepared_exchanges_match_the_one_shot_ones():
+    mp.spawn(_layout_worker, args=(2, _free_port(), 384), nprocs=2, join=True)
