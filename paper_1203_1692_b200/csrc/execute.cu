@@ -84,6 +84,7 @@ struct ExecArgs {
     int c_L;                     // side of C's leaf grid
     int sub2;                    // leaves per super-tile (16; 4 or 1 for tiny trees)
     int nstages;                 // depth of the shared-memory ring
+    uint32_t producer_nap_ns;    // pause between the producer's polls for a free stage (SPAMM_EX_NAP, ns)
     int32_t *error_flag;         // plan counts[15]: set when a hand-over wait gives up (never in a correct run)
     uint32_t *clean_ptr;         // the planner's shared state, returned to zero here on behalf of the planner
     int clean_words;             // (spamm_multiply; 0 otherwise)
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
             const uint32_t ap = __shfl_sync(FULL_MASK, cur, 5), bp = __shfl_sync(FULL_MASK, cur, 7);   // a_present, b_present
             const bool t2p = DBG && g.trace2 && blockIdx.x == 0 && team == 0 && prec < EX_TRACE2_RECORDS && lane == 0;
             if (t2p) g.trace2[(prec * 9 + 8) * 4 + 0] = clock64();
-            mbar_wait(&empty_bar[stage], phase ^ 1u);
+            mbar_wait_relaxed(&empty_bar[stage], phase ^ 1u, g.producer_nap_ns);
             if (t2p) g.trace2[(prec * 9 + 8) * 4 + 1] = clock64();
             uint32_t *d = reinterpret_cast<uint32_t *>(&desc[stage]);
             if (lane < 16) d[lane] = cur;                    // the record itself
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
             ++prec;
             if (++stage == nstages) { stage = 0; phase ^= 1u; }
         }
-        mbar_wait(&empty_bar[stage], phase ^ 1u);
+        mbar_wait_relaxed(&empty_bar[stage], phase ^ 1u, g.producer_nap_ns);
         if (lane == 0) {
             desc[stage].flags = EX_EXIT;
             mbar_arrive(&full_bar[stage]);
@@ -584,7 +585,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
     }
 }
 
-struct ExecTuning { int stages, ctas_per_sm, dbg; };
+struct ExecTuning { int stages, ctas_per_sm, dbg, nap; };
 static ExecTuning exec_tuning();
 int spamm_execute_grid()
 {
@@ -595,10 +596,12 @@ int spamm_execute_grid()
 int spamm_execute_piece_base() { return spamm_execute_grid() * EX_TEAMS; }
 static ExecTuning exec_tuning()
 {
-    ExecTuning t{3, EX_CTAS_PER_SM, 0};
+    ExecTuning t{3, EX_CTAS_PER_SM, 0, 256};
     if (const char *e = getenv("SPAMM_EX_STAGES")) t.stages = atoi(e);
     if (const char *e = getenv("SPAMM_EX_CTAS")) t.ctas_per_sm = atoi(e);
     if (const char *e = getenv("SPAMM_EX_DEBUG")) t.dbg = atoi(e);
+    if (const char *e = getenv("SPAMM_EX_NAP")) t.nap = atoi(e);
+    if (t.nap < 0) t.nap = 0;
     if (t.stages < 2) t.stages = 2;
     if (t.stages > EX_MAX_STAGES) t.stages = EX_MAX_STAGES;
     if (t.ctas_per_sm < 1) t.ctas_per_sm = 1;
@@ -658,6 +661,7 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     // the kernel leaves them clear again
     static const ExecTuning tune = exec_tuning();
     g.nstages = tune.stages;
+    g.producer_nap_ns = (uint32_t)tune.nap;
     g.dbg = tune.dbg;
     const int grid = SPAMM_NUM_SMS * tune.ctas_per_sm;
     const size_t smem = EX_TEAMS * ((size_t)tune.stages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16));
