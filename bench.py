@@ -715,6 +715,8 @@ def run_own(args) -> None:
         if not dist.is_initialized():
             if "MASTER_ADDR" not in os.environ:
                 os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": "29531", "RANK": "0", "WORLD_SIZE": "1"})
+            if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+                os.environ["NCCL_DEBUG"] = "WARN"       # the version banner goes to stdout; the line below must be the only one
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         try:
             run_sharded(args, torch, dist, P, local)

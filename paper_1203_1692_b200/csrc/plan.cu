@@ -349,9 +349,25 @@ __device__ __forceinline__ LaneNorms tile_norms(const TileArgs &a, uint32_t I, u
 
 // WITH_SUB: also classify the live tasks from the sub-norm ranges of their leaves (loaded here, only by
 // lanes that have a live task; not prefetched -- the registers are better spent on the norms)
+// sub-norm range words of the leaves A(sub*I+d, k) and B(k, sub*J+d) (spamm_tree_view.sub)
+struct SubWords { uint32_t sa[4], sb[4]; };
+__device__ __forceinline__ SubWords tile_subs(const TileArgs &a, uint32_t I, uint32_t J, uint32_t k, bool valid)
+{
+    SubWords w;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+        w.sa[d] = w.sb[d] = 0xFFFFFFFFu;
+        if (valid && a.sub_a && d < a.sub) {
+            w.sa[d] = __ldg(a.sub_a + (int64_t)(a.sub * I + d) * a.L + k);
+            w.sb[d] = __ldg(a.sub_bt + (int64_t)(a.sub * J + d) * a.L + k);
+        }
+    }
+    return w;
+}
+
 template <bool WITH_SUB>
 __device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, const LaneNorms &n, uint32_t rowok, uint32_t I = 0,
-                                                uint32_t J = 0, uint32_t k = 0)
+                                                uint32_t J = 0, uint32_t k = 0, const SubWords *pre = nullptr)
 {
     LaneTests t{0u, 0u, 0u, 0u, 0u};
 #pragma unroll
@@ -366,13 +382,13 @@ __device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, const LaneNor
             if ((rowok >> di & 1u) && norm_test(n.na[di], n.nb[dj], a.tau)) t.live |= 1u << step_pos(di, dj);
     if (WITH_SUB && a.sub_a && t.live) {
         uint32_t sa[4], sb[4];
+        if (pre) {
 #pragma unroll
-        for (int d = 0; d < 4; ++d) {
-            sa[d] = sb[d] = 0xFFFFFFFFu;
-            if (d < a.sub) {
-                sa[d] = __ldg(a.sub_a + (int64_t)(a.sub * I + d) * a.L + k);
-                sb[d] = __ldg(a.sub_bt + (int64_t)(a.sub * J + d) * a.L + k);
-            }
+            for (int d = 0; d < 4; ++d) { sa[d] = pre->sa[d]; sb[d] = pre->sb[d]; }
+        } else {
+            const SubWords w = tile_subs(a, I, J, k, true);
+#pragma unroll
+            for (int d = 0; d < 4; ++d) { sa[d] = w.sa[d]; sb[d] = w.sb[d]; }
         }
 #pragma unroll
         for (int di = 0; di < 4; ++di)
@@ -690,7 +706,7 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
     const int max_b_nodes = (int)(a.unit_capacity / 10 < ORDER_MAX_B_NODES ? a.unit_capacity / 10 : ORDER_MAX_B_NODES);
     // measured (B200): with a piece of several tiles per team the static split alone finishes within a few
     // per cent; the layered tail is worth its hand-overs only when a team's share is shorter than a tile
-    const int tail_records = a.tail_records >= 0 ? a.tail_records : (R < 8ll * a.num_teams ? 3 : 0);
+    const int tail_records = a.tail_records >= 0 ? a.tail_records : (R < 3ll * a.num_teams ? 3 : 0);
     if (tail_records > 0 && n_tiles > 0 && R > 0 && max_b_nodes > 0) {
         // (64-bit products: a plan's weight stays far below 2^48 -- at most 2^31 records of at most 96 -- and
         // the factors here below 2^15)
