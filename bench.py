@@ -419,32 +419,53 @@ def run_single(args, torch, P, local: int) -> None:
     k4_bytes = Lc * Lc * 8 + Lc * Lc * (4 + 4 + 8) * 4 // 3
 
     # ---- end to end through the public API with host buffers
-    host_a = torch.from_numpy(a_d).pin_memory()
-    host_b = host_a if b_d is None else torch.from_numpy(b_d).pin_memory()
-    # the result comes back as the product tree's packed leaves (keys + 272-float leaf records: the
-    # reference's packed_leaves() form, `core.py:387-405`), not as a zero-filled dense matrix
+    # The operands are host trees in the reference's packed form (keys + 16x16 leaf blocks, the arrays
+    # of packed_leaves(), `core.py:387-405`: what the reference arm's timed region starts from as well);
+    # the result comes back as the product tree's packed leaves (keys + 272-float leaf records), not as
+    # a zero-filled dense matrix.  The variant that starts from a dense host matrix is reported beside it.
     cap = plan.n_cleaves
     host_vals = torch.empty((cap, _lib.REC), dtype=torch.float32).pin_memory()
     host_keys = torch.empty((cap,), dtype=torch.int32).pin_memory()
-    d2h = 0
-    e2e_times = []
-    for it in range(2 + max(3, min(args.steps, 20) // 2)):
-        flush.fill_(it)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+
+    def packed_host(q):
+        k, v, _s = q.packed_leaves()
+        return torch.from_numpy(k.astype(np.int32)).pin_memory(), torch.from_numpy(v.reshape(-1, 256)).pin_memory()
+
+    pk_a = packed_host(qa)
+    pk_b = pk_a if b_d is None else packed_host(qb)
+    host_a = torch.from_numpy(a_d).pin_memory()
+    host_b = host_a if b_d is None else torch.from_numpy(b_d).pin_memory()
+
+    def e2e_time(make):
+        times, d2h_bytes = [], 0
+        for it in range(2 + max(3, min(args.steps, 20) // 2)):
+            flush.fill_(it)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ta, tb = make()
+            cc, _, _ = P.multiply(ta, tb, cfg)
+            nc = cc.nleaf                       # reads the counts back (the one synchronisation of the step)
+            host_vals[:nc].copy_(cc.values[:nc], non_blocking=True)
+            host_keys[:nc].copy_(cc.keys[:nc], non_blocking=True)
+            d2h_bytes = nc * (_lib.REC * 4 + 4)
+            e1.record()
+            torch.cuda.synchronize()
+            if it >= 2:
+                times.append(e0.elapsed_time(e1))
+        return float(np.mean(times)), d2h_bytes
+
+    def make_packed():
+        ta = P.QuadtreeMatrix.from_packed(n, n, pk_a[0], pk_a[1])
+        return ta, (ta if b_d is None else P.QuadtreeMatrix.from_packed(n, n, pk_b[0], pk_b[1]))
+
+    def make_dense():
         ta = P.QuadtreeMatrix.from_dense(host_a)
-        tb = ta if b_d is None else P.QuadtreeMatrix.from_dense(host_b)
-        cc, _, _ = P.multiply(ta, tb, cfg)
-        nc = cc.nleaf                       # reads the counts back (the one synchronisation of the step)
-        host_vals[:nc].copy_(cc.values[:nc], non_blocking=True)
-        host_keys[:nc].copy_(cc.keys[:nc], non_blocking=True)
-        d2h = nc * (_lib.REC * 4 + 4)
-        e1.record()
-        torch.cuda.synchronize()
-        if it >= 2:
-            e2e_times.append(e0.elapsed_time(e1))
-    e2e_ms = float(np.mean(e2e_times))
-    h2d = a_d.nbytes * (1 if b_d is None else 2)
+        return ta, (ta if b_d is None else P.QuadtreeMatrix.from_dense(host_b))
+
+    e2e_ms, d2h = e2e_time(make_packed)
+    e2e_dense_ms, _ = e2e_time(make_dense)
+    h2d = sum(int(t.numel()) * t.element_size() for t in pk_a) * (1 if b_d is None else 2)
+    h2d_dense = a_d.nbytes * (1 if b_d is None else 2)
 
     # ---- tau sweep of the headline workload (config 2 of BASELINE.json), both granularities
     sweep = []
@@ -538,7 +559,11 @@ def run_single(args, torch, P, local: int) -> None:
         "cpu_baseline": cpu,
         "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "result": "product tree as packed leaves (keys + leaf records)"},
+                "operands": "host trees as packed leaves (keys + 16x16 blocks, pinned), QuadtreeMatrix.from_packed",
+                "result": "product tree as packed leaves (keys + leaf records)",
+                "from_dense": {"value": flops / (e2e_dense_ms * 1e-3) / 1e9, "ms_per_step": e2e_dense_ms,
+                               "h2d_bytes_per_step": int(h2d_dense), "d2h_bytes_per_step": int(d2h),
+                               "operands": "dense host matrix (pinned), QuadtreeMatrix.from_dense"}},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "sweep": sweep,

@@ -116,6 +116,12 @@ int spamm_build_interior(const double *leaf_sq, int depth, float *norm, float *n
 int spamm_leaf_norms_packed(float *values, int64_t nleaf, float *values_t, double *leaf_sq,
                             void *stream);
 
+/* The same from plain leaf blocks: `blocks` holds nleaf row-major 16x16 blocks (256 floats each, the
+ * value array of the reference's packed_leaves(), core.py:387-405); writes the whole `values` and
+ * `values_t` records and leaf_sq [nleaf].  All pointers are device pointers. */
+int spamm_leaves_from_blocks(const float *blocks, int64_t nleaf, float *values, float *values_t,
+                             double *leaf_sq, void *stream);
+
 /* QuadtreeMatrix.sparsify (core.py:347-383) on packed leaves: zeroes every 4x4 sub-block with
  * 0 < sub-norm < eps in both record layouts, refreshes the norms of the leaves it touched
  * (compute_norms order) and sets leaf_sq of the untouched ones to float64(norm)^2, the value the
@@ -156,15 +162,19 @@ int spamm_to_dense(const spamm_tree_view *t, float *out, int64_t ld, void *strea
  * at packed index first + popcount(present16 & ((1 << morton4(r,c)) - 1)). */
 #define STEP_FIRST (1u << 16)   /* first record of its super-tile */
 #define STEP_LAST (1u << 17)    /* last record of its super-tile  */
-/* Work units of the numeric phase.  A unit is a run of consecutive step records of one super-tile.
- * With many more super-tiles than CTAs every tile is one unit (counts[12] == 0, unit = node).
- * Otherwise the planner cuts the tiles that are handed out last into segments of about counts[12]
- * records, so that the persistent CTAs of the numeric kernel finish together: unit =
- * node | segment << 20 | segments << 26, segment s of nseg covering records
- * [s * ns / nseg, (s + 1) * ns / nseg) of a tile with ns records.  The accumulators of a tile pass
- * from one segment to the next through C's own value records (chain[] holds, per product leaf, the
- * number of finished segments), which keeps the ascending-k summation order.  A unit's
- * predecessor always comes earlier in tile_order. */
+/* Work units of the numeric phase (tile_order).  A unit is a run [b, e) of consecutive step
+ * records, stored as the pair (b, e).  The numeric kernel runs two teams of warps per SM; the
+ * planner cuts the record stream into counts[12] pieces of equal weight (live tasks plus a constant
+ * per record), a whole number of rounds of one piece per team: units [0, counts[12]).  A piece may
+ * begin and end inside a super-tile; the kernel then runs the head of the tile it begins at its
+ * end first, its whole tiles next and the rest of the tile it starts in last, so that a piece never
+ * waits long for the piece before it.  Only a plan with fewer than three records per team gets a
+ * second region: its last quarter is cut into short segments of single tiles, five ranges of
+ * counts[16..20] units at unit index counts[12] + x * counts[21], handed out after the pieces.  The
+ * accumulators of a tile pass from one unit to the next through C's own value records; chain[]
+ * holds, per product leaf, the record index up to which the sums there are complete, which keeps
+ * the ascending-k summation order.  Word 15 of a step record = records of its tile | position of
+ * the record in the tile << 16. */
 #define SPAMM_UNIT_EXTRA 8192   /* room in tile_order beyond one unit per super-tile */
 typedef struct {
     uint32_t kblock;       /* K: contraction block index, k = 4K + kk                      */
@@ -183,23 +193,24 @@ typedef struct {
                               in the halves of dead[0], kk = 2, 3 in dead[1]; a task in
                               neither set is gated per micro product by the numeric kernel
                               (all zero when the operands carry no sub-norm ranges)         */
-    uint32_t pad;
+    uint32_t tile_pos;     /* records of this super-tile | position of this record in it << 16 */
 } spamm_step;
 
-/* counts[]: [0] product leaves nC, [1] unused,
- * [2] overflow flag, [3] largest intermediate list, [4] step records, [5] work units in
+/* counts[]: [0] product leaves nC, [1] super-tiles with at least one task,
+ * [2] overflow flag, [3] largest intermediate list, [4] step records, [5] unit slots used in
  * tile_order, [6..7] tasks T as one uint64, [8..9] executed 4x4x4 products as one uint64
  * (spamm_multiply only), [10] scratch, [11] all super-tile nodes (tile_off has one more entry),
- * [12] records per segment (0: every unit is a whole super-tile), [13..14] the numeric kernel's
- * hand-out and exit counters (zero between launches), [15] set by the numeric kernel if a wait for
- * a chained segment ever gives up (a scheduling bug, never in a correct run): results invalid */
+ * [12] pieces, [16..20] units in the five ranges of short segments and [21] the stride between
+ * the ranges (see "work units" above), [13..14] the numeric kernel's hand-out and exit counters
+ * when it is launched by spamm_execute (zero between launches), [15] set by the numeric kernel if a
+ * wait for a chained unit ever gives up (a scheduling bug, never in a correct run): results invalid */
 #define SPAMM_PLAN_COUNTS 32
 typedef struct {
     spamm_step *steps;       /* [step_capacity]                                   */
     uint32_t *c_keys;        /* [leaf_capacity] product leaf keys, ascending      */
     int32_t *tile_off;       /* [leaf_capacity + 1] first step of each super-tile node */
-    int32_t *tile_order;     /* [leaf_capacity + SPAMM_UNIT_EXTRA] work units in hand-out order */
-    int32_t *chain;          /* [leaf_capacity] finished segments per product leaf (numeric phase scratch) */
+    int32_t *tile_order;     /* [leaf_capacity + SPAMM_UNIT_EXTRA] work units (b, e), two words each */
+    int32_t *chain;          /* [leaf_capacity] hand-over state per product leaf (numeric phase scratch, zero between launches) */
     int64_t step_capacity;
     int64_t leaf_capacity;
     int32_t *counts;         /* [SPAMM_PLAN_COUNTS]                               */

@@ -69,6 +69,7 @@ SIGNATURES = {
     "spamm_pack_leaves": (C.c_int, [vp, i64, i64, i64, C.c_int, vp, i64, vp, vp, vp, vp]),
     "spamm_build_interior": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int, vp]),
     "spamm_leaf_norms_packed": (C.c_int, [vp, i64, vp, vp, vp]),
+    "spamm_leaves_from_blocks": (C.c_int, [vp, i64, vp, vp, vp, vp]),
     "spamm_transpose_records": (C.c_int, [vp, i64, vp, vp]),
     "spamm_sparsify_leaves": (C.c_int, [vp, vp, vp, i64, C.c_float, vp, vp]),
     "spamm_index_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp]),

@@ -47,6 +47,13 @@
 #define EX_PREFETCH 4
 #define EX_BLOCK_BYTES (16 * SPAMM_REC_BYTES)     // one 4x4 block of leaf records
 #define EX_TRACE2_RECORDS 96
+#ifndef EX_KK_UNROLL
+#define EX_KK_UNROLL 4
+#endif
+#ifndef EX_FINE_ROLLED
+#define EX_FINE_ROLLED 1    // fine4: a rolled loop that skips the r no lane of the warp runs
+#endif
+#define EX_ZERO_BYTES 256      // per team: zeros read in place of gated-off operand sub-blocks
 
 // A stage's descriptor: the step record as it is in the plan (one store per lane of the producer), the
 // shared-memory addresses of the staged leaves, and what the producer adds (run flags, record index).
@@ -85,6 +92,7 @@ struct ExecArgs {
     int sub2;                    // leaves per super-tile (16; 4 or 1 for tiny trees)
     int nstages;                 // depth of the shared-memory ring
     uint32_t producer_nap_ns;    // pause between the producer's polls for a free stage (SPAMM_EX_NAP, ns)
+    uint32_t leaf_copy_below;    // copy leaf by leaf when under this many 128ths of a record's leaves are touched (SPAMM_EX_LEAFCOPY)
     int32_t *error_flag;         // plan counts[15]: set when a hand-over wait gives up (never in a correct run)
     uint32_t *clean_ptr;         // the planner's shared state, returned to zero here on behalf of the planner
     int clean_words;             // (spamm_multiply; 0 otherwise)
@@ -147,7 +155,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
     // have schedulers 0 and 2 to themselves and the odd warps (team 1) schedulers 1 and 3.
     const int team = EX_TEAMS == 1 ? 0 : (warp & 1);
     const int vwarp = EX_TEAMS == 1 ? warp : (warp >> 1);          // 0 .. 7 consumers, 8 = the team's producer
-    const size_t team_bytes = (size_t)nstages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16);
+    const size_t team_bytes = (size_t)nstages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16) + EX_ZERO_BYTES;
     static_assert(sizeof(StageDesc) == 208 && sizeof(spamm_step) == 64, "StageDesc layout");
     unsigned char *tbase = smem_raw + (size_t)team * team_bytes;
     unsigned char *sA = tbase;
@@ -155,6 +163,8 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
     StageDesc *desc = reinterpret_cast<StageDesc *>(tbase + (size_t)nstages * 2 * EX_BLOCK_BYTES);
     uint64_t *full_bar = reinterpret_cast<uint64_t *>(desc + EX_MAX_STAGES);
     uint64_t *empty_bar = full_bar + EX_MAX_STAGES;
+    // zeros that stand in for the operand sub-blocks of a gated-off micro product (fine4)
+    const float *zeros = reinterpret_cast<const float *>(empty_bar + EX_MAX_STAGES);
 
     // everything that does not depend on the preceding kernel comes before the wait for it
     if (vwarp == EX_CONSUMERS && lane == 0) {
@@ -163,6 +173,10 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
             mbar_init(&empty_bar[s], EX_CONSUMERS);
         }
         fence_barrier_init();
+    }
+    if (vwarp == EX_CONSUMERS) {
+        float *z = const_cast<float *>(zeros);
+        for (int x = (int)lane; x < EX_ZERO_BYTES / 4; x += 32) z[x] = 0.0f;
     }
     // First piece: pieces are drawn from one counter, in stream order.  A team only ever waits for
     // partial sums of the piece before one of its own, which was drawn earlier by a team that is
@@ -183,16 +197,20 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
 
     if (vwarp == EX_CONSUMERS) {
         // ============ producer: stream step records, stage leaf blocks with bulk copies ============
+        // the plan's counts are requested before the ticket so that the two round trips overlap
+        const int c_over = g.counts[2], c_pieces = g.counts[12], stride = g.counts[21];
+        int nr[5];
+#pragma unroll
+        for (int x = 0; x < 5; ++x) nr[x] = g.counts[16 + x];
         if (!g.ticket_early) {
             if (lane == 0) piece = (int)atomicAdd(g.ticket, 1u);
             piece = __shfl_sync(FULL_MASK, piece, 0);
         }
-        const bool plan_ok = g.counts[2] == 0;                  // an overflowed plan is incomplete: do nothing
+        const bool plan_ok = c_over == 0;                       // an overflowed plan is incomplete: do nothing
         // unit slots: region A's pieces [0, P), then region B's five ranges, range x at P + x * stride with nr[x] in use
-        const int P = plan_ok ? g.counts[12] : 0, stride = g.counts[21];
-        int nr[5];
+        const int P = plan_ok ? c_pieces : 0;
 #pragma unroll
-        for (int x = 0; x < 5; ++x) nr[x] = plan_ok ? g.counts[16 + x] : 0;
+        for (int x = 0; x < 5; ++x) nr[x] = plan_ok ? nr[x] : 0;
         const int first_piece = piece;
         const uint32_t *words = reinterpret_cast<const uint32_t *>(g.steps);
         const int2 *units = reinterpret_cast<const int2 *>(g.pieces);
@@ -297,25 +315,38 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
                 d[48] = f;
                 d[49] = meta & 0x3FFFFFFFu;                  // record index
             }
-            {
-                // leaf (r,c) of a block sits at index popc(present & below(morton4(r,c)))
-                const int x = (int)(lane & 15u) >> 2, kk = (int)(lane & 3u);
-                const uint32_t idx = lane < 16 ? __popc(ap & ((1u << step_pos(x, kk)) - 1u))
-                                               : __popc(bp & ((1u << step_pos(kk, x)) - 1u));
-                const unsigned char *base = (lane < 16 ? sA : sB) + (size_t)stage * EX_BLOCK_BYTES;
-                d[16 + lane] = smem_u32(base) + idx * SPAMM_REC_BYTES;
-            }
-            __syncwarp();
+            // leaf (r,c) of a block sits at index popc(present & below(morton4(r,c))); lane l < 16 is leaf
+            // A(x, kk), lane l >= 16 leaf B(kk, x)
+            const int x = (int)(lane & 15u) >> 2, kk = (int)(lane & 3u);
+            const uint32_t idx = lane < 16 ? __popc(ap & ((1u << step_pos(x, kk)) - 1u))
+                                           : __popc(bp & ((1u << step_pos(kk, x)) - 1u));
+            unsigned char *dst = (lane < 16 ? sA : sB) + (size_t)stage * EX_BLOCK_BYTES + (size_t)idx * SPAMM_REC_BYTES;
+            d[16 + lane] = smem_u32(dst);
+            // a leaf is touched when one of the tasks of its row (A) or column (B) of the super-tile runs at kk
+            uint32_t lv = __shfl_sync(FULL_MASK, cur, 8 + kk) & 0xFFFFu;
+            if (FINE) lv &= ~(__shfl_sync(FULL_MASK, cur, 13 + (kk >> 1)) >> ((kk & 1) * 16));
+            const uint32_t sel = lane < 16 ? 0x0033u << (((x >> 1) << 3) | ((x & 1) << 1)) : 0x0505u << (((x >> 1) << 2) | (x & 1));
+            const bool touched = (lv & sel) != 0u;
+            const uint32_t ntouched = __popc(__ballot_sync(FULL_MASK, touched));
+            const uint32_t a_first = __shfl_sync(FULL_MASK, cur, 4), b_first = __shfl_sync(FULL_MASK, cur, 6);
             const bool copy = !(DBG && (g.dbg & 1));
             const uint32_t na = __popc(ap), nb = __popc(bp);
-            if (lane == 0) mbar_arrive_expect_tx(&full_bar[stage], copy ? (na + nb) * SPAMM_REC_BYTES : 0u);
+            // two copies of the whole blocks when most of their leaves are touched, else one copy per touched leaf
+            const bool per_leaf = ntouched * 128u < (na + nb) * g.leaf_copy_below;
+            if (lane == 0) mbar_arrive_expect_tx(&full_bar[stage], copy ? (per_leaf ? ntouched : na + nb) * SPAMM_REC_BYTES : 0u);
             __syncwarp();
-            if (copy && lane == 4)
-                bulk_copy_g2s(sA + (size_t)stage * EX_BLOCK_BYTES, g.a_values_t + (size_t)cur * SPAMM_REC,
-                              na * SPAMM_REC_BYTES, &full_bar[stage]);
-            if (copy && lane == 6)
-                bulk_copy_g2s(sB + (size_t)stage * EX_BLOCK_BYTES, g.b_values + (size_t)cur * SPAMM_REC,
-                              nb * SPAMM_REC_BYTES, &full_bar[stage]);
+            if (copy && per_leaf) {
+                if (touched)
+                    bulk_copy_g2s(dst, (lane < 16 ? g.a_values_t + (size_t)a_first * SPAMM_REC : g.b_values + (size_t)b_first * SPAMM_REC) +
+                                           (size_t)idx * SPAMM_REC, SPAMM_REC_BYTES, &full_bar[stage]);
+            } else if (copy) {
+                if (lane == 4)
+                    bulk_copy_g2s(sA + (size_t)stage * EX_BLOCK_BYTES, g.a_values_t + (size_t)cur * SPAMM_REC,
+                                  na * SPAMM_REC_BYTES, &full_bar[stage]);
+                if (lane == 6)
+                    bulk_copy_g2s(sB + (size_t)stage * EX_BLOCK_BYTES, g.b_values + (size_t)cur * SPAMM_REC,
+                                  nb * SPAMM_REC_BYTES, &full_bar[stage]);
+            }
             if (t2p) g.trace2[(prec * 9 + 8) * 4 + 2] = clock64();
             ++prec;
             if (++stage == nstages) { stage = 0; phase ^= 1u; }
@@ -405,11 +436,12 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
             dead01 = ds.rec.dead[0];
             dead23 = ds.rec.dead[1];
         }
-#pragma unroll     // all four k unrolled: +4-5 % (their addresses become constants), measured
+        constexpr int kk_unroll = EX_KK_UNROLL;
+#pragma unroll kk_unroll     // all four k unrolled: +4-5 % (their addresses become constants), measured
         for (int kk = 0; kk < 4; ++kk) {
             const uint32_t lw = kk == 0 ? live4.x : kk == 1 ? live4.y : kk == 2 ? live4.z : live4.w;
             // fine4: a task the planner found dead runs no micro product (and counts none)
-            const uint32_t dead = FINE ? ((kk < 2 ? dead01 : dead23) >> (16 * (kk & 1))) : 0u;
+            const uint32_t dead = FINE && !(DBG && (g.dbg & 8)) ? ((kk < 2 ? dead01 : dead23) >> (16 * (kk & 1))) : 0u;
             const uint32_t live = lw & 0xFFFFu & ~dead;
             if (!((live >> (2 * vwarp)) & 3u) || (DBG && (g.dbg & 2))) continue;
             const bool mine = (live >> mypos) & 1u;
@@ -417,7 +449,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
             const float *Bs = shared_ptr(kk == 0 ? b_at.x : kk == 1 ? b_at.y : kk == 2 ? b_at.z : b_at.w);
             uint32_t on = 0;       // bit r: micro product (p,q,r) of my task runs
             if (FINE) {
-                if (mine && ((lw >> (16 + mypos)) & 1u)) {
+                if (mine && (((lw >> (16 + mypos)) & 1u) || (DBG && (g.dbg & 4)))) {
                     on = 15u;
                 } else if (mine) {
                     const float4 sa = *reinterpret_cast<const float4 *>(As + 256 + 4 * p);   // subA[p][0..3]
@@ -439,55 +471,51 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
             } else {
                 on = mine ? 15u : 0u;
             }
-            // Fast path (the common case away from the band edge): every lane runs all four r or
-            // none, so the 16 k of the task form one branch-free block and the compiler overlaps the
-            // shared-memory reads of r+1 with the multiplies of r.
-            if (!FINE || __all_sync(FULL_MASK, on == 15u || on == 0u)) {
+            // One multiply-accumulate block per r: 4 k of the leaf product.  A lane whose micro product
+            // (p,q,r) is gated off reads zeros in place of both operand sub-blocks, so the warp stays
+            // converged and the sums it keeps are unchanged (x + 0*0 = x; only a -0 would become +0).
+            auto micro = [&](const float *ar, const float *br) {
+                float4 a[4], b[4];
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    a[x] = *reinterpret_cast<const float4 *>(ar + x * 16);
+                    b[x] = *reinterpret_cast<const float4 *>(br + x * 16);
+                }
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                    const float2 a01 = make_float2(a[x].x, a[x].y), a23 = make_float2(a[x].z, a[x].w);
+                    const float bv[4] = {b[x].x, b[x].y, b[x].z, b[x].w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        mac2<EXACT>(acc2[0][j], a01, bv[j]);
+                        mac2<EXACT>(acc2[1][j], a23, bv[j]);
+                    }
+                }
+            };
+            if (!FINE) {
+                // every lane runs all four r or none: one branch-free block, the compiler overlaps the
+                // shared-memory reads of r+1 with the multiplies of r
                 if (on) {
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        float4 a[4], b[4];
+                    for (int r = 0; r < 4; ++r) micro(As + 64 * r + 4 * p, Bs + 64 * r + 4 * q);
+                }
+                continue;
+            }
+            const uint32_t onany = __reduce_or_sync(FULL_MASK, on);      // r that some lane of the warp runs
+            if (onany == 15u || !EX_FINE_ROLLED) {
+                if (!EX_FINE_ROLLED && !onany) continue;
 #pragma unroll
-                        for (int x = 0; x < 4; ++x) {
-                            a[x] = *reinterpret_cast<const float4 *>(As + (4 * r + x) * 16 + 4 * p);
-                            b[x] = *reinterpret_cast<const float4 *>(Bs + (4 * r + x) * 16 + 4 * q);
-                        }
-#pragma unroll
-                        for (int x = 0; x < 4; ++x) {
-                            const float2 a01 = make_float2(a[x].x, a[x].y), a23 = make_float2(a[x].z, a[x].w);
-                            const float bv[4] = {b[x].x, b[x].y, b[x].z, b[x].w};
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                mac2<EXACT>(acc2[0][j], a01, bv[j]);
-                                mac2<EXACT>(acc2[1][j], a23, bv[j]);
-                            }
-                        }
-                    }
+                for (int r = 0; r < 4; ++r) {
+                    const bool go = (on >> r) & 1u;
+                    micro(go ? As + 64 * r + 4 * p : zeros, go ? Bs + 64 * r + 4 * q : zeros);
                 }
                 continue;
             }
 #pragma unroll 1
             for (int r = 0; r < 4; ++r) {
+                if (!((onany >> r) & 1u)) continue;
                 const bool go = (on >> r) & 1u;
-                if (!__any_sync(FULL_MASK, go)) continue;
-                if (go) {
-                    float4 a[4], b[4];
-#pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        a[x] = *reinterpret_cast<const float4 *>(As + (4 * r + x) * 16 + 4 * p);
-                        b[x] = *reinterpret_cast<const float4 *>(Bs + (4 * r + x) * 16 + 4 * q);
-                    }
-#pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        const float2 a01 = make_float2(a[x].x, a[x].y), a23 = make_float2(a[x].z, a[x].w);
-                        const float bv[4] = {b[x].x, b[x].y, b[x].z, b[x].w};
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            mac2<EXACT>(acc2[0][j], a01, bv[j]);
-                            mac2<EXACT>(acc2[1][j], a23, bv[j]);
-                        }
-                    }
-                }
+                micro(go ? As + 64 * r + 4 * p : zeros, go ? Bs + 64 * r + 4 * q : zeros);
             }
         }
         uint32_t c_base = 0, present = 0, tile_id = 0, seg_done = 0;
@@ -585,7 +613,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
     }
 }
 
-struct ExecTuning { int stages, ctas_per_sm, dbg, nap; };
+struct ExecTuning { int stages, ctas_per_sm, dbg, nap, leaf_copy; };
 static ExecTuning exec_tuning();
 int spamm_execute_grid()
 {
@@ -596,12 +624,14 @@ int spamm_execute_grid()
 int spamm_execute_piece_base() { return spamm_execute_grid() * EX_TEAMS; }
 static ExecTuning exec_tuning()
 {
-    ExecTuning t{3, EX_CTAS_PER_SM, 0, 256};
+    ExecTuning t{3, EX_CTAS_PER_SM, 0, 256, 96};
     if (const char *e = getenv("SPAMM_EX_STAGES")) t.stages = atoi(e);
     if (const char *e = getenv("SPAMM_EX_CTAS")) t.ctas_per_sm = atoi(e);
     if (const char *e = getenv("SPAMM_EX_DEBUG")) t.dbg = atoi(e);
     if (const char *e = getenv("SPAMM_EX_NAP")) t.nap = atoi(e);
+    if (const char *e = getenv("SPAMM_EX_LEAFCOPY")) t.leaf_copy = atoi(e);
     if (t.nap < 0) t.nap = 0;
+    if (t.leaf_copy < 0) t.leaf_copy = 0;
     if (t.stages < 2) t.stages = 2;
     if (t.stages > EX_MAX_STAGES) t.stages = EX_MAX_STAGES;
     if (t.ctas_per_sm < 1) t.ctas_per_sm = 1;
@@ -662,9 +692,10 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
     static const ExecTuning tune = exec_tuning();
     g.nstages = tune.stages;
     g.producer_nap_ns = (uint32_t)tune.nap;
+    g.leaf_copy_below = (uint32_t)tune.leaf_copy;
     g.dbg = tune.dbg;
     const int grid = SPAMM_NUM_SMS * tune.ctas_per_sm;
-    const size_t smem = EX_TEAMS * ((size_t)tune.stages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16));
+    const size_t smem = EX_TEAMS * ((size_t)tune.stages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16) + EX_ZERO_BYTES);
     const bool fine = granularity == SPAMM_FINE4;
     static const char *trace2_path = getenv("SPAMM_EX_TRACE2");   // tuning aids: allocate and synchronise
     static const char *trace_path = getenv("SPAMM_EX_TRACE");

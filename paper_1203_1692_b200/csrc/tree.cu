@@ -374,22 +374,28 @@ __device__ __forceinline__ double leaf_total_refresh(double S)
     return r;
 }
 
-__global__ void __launch_bounds__(256) leaf_norms_packed_kernel(float *__restrict__ values, int64_t nleaf,
-                                                                float *__restrict__ values_t,
+// src == nullptr: the values sit in the records already; else src holds plain 16x16 blocks (256 floats per
+// leaf, the reference's packed_leaves() value array, `core.py:387-405`) and the record's value part is written too
+__global__ void __launch_bounds__(256) leaf_norms_packed_kernel(const float *__restrict__ src, float *__restrict__ values,
+                                                                int64_t nleaf, float *__restrict__ values_t,
                                                                 double *__restrict__ leaf_sq)
 {
     const int64_t leaf = (int64_t)blockIdx.x * 16 + (threadIdx.x >> 4);
     const int t = threadIdx.x & 15, p = t >> 2, q = t & 3;
     const bool ok = leaf < nleaf;
+    const float *in = src ? src + leaf * 256 : values + leaf * SPAMM_REC;
     float4 r[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-        r[i] = ok ? *reinterpret_cast<const float4 *>(values + leaf * SPAMM_REC + (4 * p + i) * 16 + 4 * q)
-                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        r[i] = ok ? *reinterpret_cast<const float4 *>(in + (4 * p + i) * 16 + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
     const double S = sub_block_sq(r[0], r[1], r[2], r[3]);
     const double total = leaf_total_refresh(S);
     if (!ok) return;
     const float sn = (float)sqrt(S);
+    if (src) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) *reinterpret_cast<float4 *>(values + leaf * SPAMM_REC + (4 * p + i) * 16 + 4 * q) = r[i];
+    }
     values[leaf * SPAMM_REC + 256 + q * 4 + p] = sn;
     if (t == 0) leaf_sq[leaf] = total;
     float *vt = values_t + leaf * SPAMM_REC;
@@ -404,8 +410,19 @@ extern "C" int spamm_leaf_norms_packed(float *values, int64_t nleaf, float *valu
 {
     if (nleaf == 0) return SPAMM_OK;
     if (!values || !values_t || nleaf < 0) return SPAMM_EINVAL;
-    leaf_norms_packed_kernel<<<(unsigned)((nleaf + 15) / 16), 256, 0, (cudaStream_t)stream>>>(values, nleaf, values_t,
-                                                                                            leaf_sq);
+    leaf_norms_packed_kernel<<<(unsigned)((nleaf + 15) / 16), 256, 0, (cudaStream_t)stream>>>(nullptr, values, nleaf,
+                                                                                            values_t, leaf_sq);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
+}
+
+extern "C" int spamm_leaves_from_blocks(const float *blocks, int64_t nleaf, float *values, float *values_t,
+                                        double *leaf_sq, void *stream)
+{
+    if (nleaf == 0) return SPAMM_OK;
+    if (!blocks || !values || !values_t || !leaf_sq || nleaf < 0) return SPAMM_EINVAL;
+    leaf_norms_packed_kernel<<<(unsigned)((nleaf + 15) / 16), 256, 0, (cudaStream_t)stream>>>(blocks, values, nleaf,
+                                                                                            values_t, leaf_sq);
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
 }

@@ -2,8 +2,13 @@
 
 Mirrors the part of the reference's ``QuadtreeMatrix`` the multiply path touches
 (`pkg/src/spamm/core.py:146-405`): ``from_dense``, ``to_dense``, ``packed_leaves``,
-``put_leaf`` / ``clear`` / ``compute_norms``, ``norm``, ``leaf_count``, ``node``.  Element
-mutation, ``sparsify`` and ``drop_tolerance`` are outside the path.
+``put_leaf`` / ``clear`` / ``compute_norms``, ``norm``, ``leaf_count``, ``node``, plus
+``sparsify`` / ``drop_tolerance`` and the host-side accessors ``leaf_items``, ``node_count``,
+``get_element``.  Not provided (outside the path): ``set_element``
+(raises ``NotImplementedError``), ``DenseMatrix``'s precision handling (``precision``,
+``to_single`` / ``to_double``, ``frobenius``), ``n_b != 16`` and the dense-leaf foil
+``execute_plan_dense_leaf``.  Added: ``from_packed`` (host or device packed leaves) and
+``from_reference`` (a tree of the reference package).
 
 Layout in HBM (see ``include/spamm_b200.h``): stored 16x16 leaves packed in ascending
 Morton-key order -- row-major (``values``) and transposed (``values_t``, the staging layout of
@@ -308,6 +313,33 @@ class QuadtreeMatrix:
         q._adopt_packed(torch.from_numpy(keys).to(q.device), values, values_t, torch.from_numpy(leaf_sq).to(q.device), n)
         return q
 
+    @classmethod
+    def from_packed(cls, m: int, n: int, keys, blocks, device=None) -> "QuadtreeMatrix":
+        """Tree from packed leaves: ``keys`` = ascending Morton keys of the stored leaves, ``blocks`` =
+        their 16x16 values, shape (nleaf, 16, 16) or (nleaf, 256) float32 -- the first two arrays of
+        the reference's ``packed_leaves()`` (`core.py:387-405`).  Host arrays (numpy, or torch tensors,
+        pinned for an asynchronous copy) or device tensors.  Equivalent to ``put_leaf`` for every
+        leaf followed by ``compute_norms`` (`core.py:315-345`): all norms are recomputed on the device."""
+        q = cls(m, n, DEFAULT_BLOCK, device)
+        keys_t = torch.as_tensor(keys)
+        blocks_t = torch.as_tensor(blocks)
+        nl = int(keys_t.numel())
+        if blocks_t.dtype != torch.float32 or blocks_t.numel() != nl * 256:
+            raise ValueError("blocks must hold one float32 16x16 block per key")
+        if nl == 0:
+            return q
+        if nl > (1 << (2 * q.depth)):
+            raise ValueError("more leaves than the tree has")
+        dev_blocks = blocks_t.reshape(nl, 256).to(q.device, non_blocking=True).contiguous()
+        dev_keys = keys_t.to(q.device, non_blocking=True).to(torch.int32)
+        values = q._alloc((nl, _lib.REC), torch.float32)
+        values_t = q._alloc((nl, _lib.REC), torch.float32)
+        leaf_sq = q._alloc((nl,), torch.float64)
+        _lib.check(_lib.lib().spamm_leaves_from_blocks(dev_blocks.data_ptr(), nl, values.data_ptr(), values_t.data_ptr(),
+                                                      leaf_sq.data_ptr(), _stream()), "leaves_from_blocks")
+        q._adopt_packed(dev_keys, values, values_t, leaf_sq, nl)
+        return q
+
     def _build_from_device_dense(self, d: torch.Tensor) -> None:
         lib = _lib.lib()
         st = _stream()
@@ -474,6 +506,40 @@ class QuadtreeMatrix:
             return None
         v = float(self.level_norms(tier)[i, j])
         return TreeNode(tier, index, v) if v >= 0 else None
+
+    # -- host-side accessors of the reference tree (`core.py:176-211`); each call copies from the device
+    def leaf_items(self) -> list[tuple[int, TreeNode]]:
+        """Stored leaves as (key, node) in ascending key order; node.norm is the leaf's Frobenius norm."""
+        if self.nleaf == 0:
+            return []
+        keys = self.packed_leaves()[0]
+        i, j = morton.decode_array(keys.astype(np.uint64))
+        norms = self.level_norms(self.depth)[i, j]
+        return [(int(k), TreeNode(self.depth, int(k), float(v))) for k, v in zip(keys.tolist(), norms)]
+
+    @property
+    def node_count(self) -> int:
+        """Stored nodes of all tiers (`core.py:188-190`)."""
+        if self.nleaf == 0:
+            return 0
+        return int(sum(int(np.count_nonzero(self.level_norms(t) >= 0)) for t in range(self.depth + 1)))
+
+    def get_element(self, i: int, j: int) -> float:
+        """Stored value at (i, j); 0.0 where no leaf is stored (`core.py:202-211`)."""
+        i, j = int(i), int(j)
+        if not (0 <= i < self.m and 0 <= j < self.n):
+            raise IndexError(f"element ({i}, {j}) outside {self.m} x {self.n}")
+        if self.nleaf == 0:
+            return 0.0
+        self._flush_guard()
+        g = self.grids()
+        slot = int(g.slot[(i // 16) * (1 << self.depth) + (j // 16)].item())
+        return 0.0 if slot < 0 else float(self.values[slot, (i % 16) * 16 + (j % 16)].item())
+
+    def set_element(self, i: int, j: int, value: float) -> None:
+        """Not part of the multiply path (SURVEY.md section 8 marks `core.py:280-313` out of scope): edit the
+        tree with put_leaf / compute_norms, or build it with from_dense / from_packed."""
+        raise NotImplementedError("set_element is outside the B200 multiply path; use put_leaf + compute_norms")
 
     # -- staged mutation: put_leaf ... compute_norms (`core.py:315-345`) --------------------------
     def put_leaf(self, key: int, values: np.ndarray) -> None:

@@ -15,7 +15,7 @@ qa = P.QuadtreeMatrix.from_dense(a)
 qb = qa if b is None else P.QuadtreeMatrix.from_dense(b)
 cfg = P.MultiplyConfig(tau=tau, granularity=gran)
 c, plan, k = P.multiply(qa, qb, cfg)
-flush = torch.empty((256 << 20,), dtype=torch.uint8, device="cuda")
+flush = torch.empty((1 if os.environ.get("PROBE_WARM_L2") else 256 << 20,), dtype=torch.uint8, device="cuda")
 ms = bench.kernel_time_execute(P, torch, plan, qa, qb, cfg, 10, flush)
 fl = 128 * k.products4 if gran == "fine4" else 8192 * len(plan)
 print(json.dumps({"env": {k_: v for k_, v in os.environ.items() if k_.startswith("SPAMM_")}, "workload": name, "n": int(a.shape[0]), "tau": tau,

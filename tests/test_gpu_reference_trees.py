@@ -110,3 +110,61 @@ def test_reference_trees_as_operands_and_accumulator():
     with pytest.raises(ValueError):
         bad = RefLikeTree(300, 300, n_b=8)
         P.multiply(bad, bad, cfg)
+
+
+@pytest.mark.parametrize("n,lam", [(256, 0.8), (1000, 0.9)])
+def test_from_packed_equals_from_dense(n, lam):
+    """QuadtreeMatrix.from_packed (the key and value arrays of `core.py:387-405` from host memory) builds the
+    tree from_dense builds: same records in both layouts, same norms at every tier, same product."""
+    import torch
+    import paper_1203_1692_b200 as P
+    from paper_1203_1692_b200 import inputs
+    a = inputs.exponential_decay(n, lam, seed=5)
+    q0 = P.QuadtreeMatrix.from_dense(a)
+    keys, vals, subs = q0.packed_leaves()
+    for blocks in (vals, torch.from_numpy(vals.reshape(-1, 256).copy()).pin_memory()):
+        q1 = P.QuadtreeMatrix.from_packed(n, n, keys.astype(np.int64), blocks)
+        assert q1.nleaf == q0.nleaf and q1.depth == q0.depth
+        k1, v1, s1 = q1.packed_leaves()
+        assert np.array_equal(k1, keys) and np.array_equal(v1, vals) and np.array_equal(s1, subs)
+        assert torch.equal(q1.values_t[: q1.nleaf], q0.values_t[: q0.nleaf])
+        for tier in range(q0.depth + 1):
+            assert np.array_equal(q1.level_norms(tier), q0.level_norms(tier))
+        c0, _, _ = P.multiply(q0, q0, P.MultiplyConfig(tau=1e-6))
+        c1, _, _ = P.multiply(q1, q1, P.MultiplyConfig(tau=1e-6))
+        for x, y in zip(c0.packed_leaves(), c1.packed_leaves()):
+            assert np.array_equal(x, y)
+    # the oracle's tree of the same matrix holds the same leaves
+    t = O.tree_from_dense(a)
+    assert np.array_equal(np.asarray(t.keys, np.int64), keys.astype(np.int64))
+    assert np.array_equal(np.asarray(t.values, np.float32).reshape(-1, 16, 16), vals)
+    empty = P.QuadtreeMatrix.from_packed(n, n, np.zeros(0, np.int64), np.zeros((0, 16, 16), np.float32))
+    assert empty.nleaf == 0
+    with pytest.raises(ValueError):
+        P.QuadtreeMatrix.from_packed(n, n, keys, vals.astype(np.float64))
+
+
+def test_host_accessors_match_the_oracle_tree():
+    """leaf_items / node_count / get_element (`core.py:176-211`) on the device tree against the oracle's tree."""
+    import paper_1203_1692_b200 as P
+    from paper_1203_1692_b200 import inputs
+    a = inputs.exponential_decay(200, 0.7, seed=2)
+    a[a < 1e-30] = 0.0
+    q = P.QuadtreeMatrix.from_dense(a)
+    t = O.tree_from_dense(a)
+    items = q.leaf_items()
+    assert [k for k, _ in items] == [int(k) for k in t.keys.tolist()]
+    i, j = _decode_all(t.keys)
+    assert np.array_equal(np.array([nd.norm for _, nd in items], np.float32), t.leaf_norm[i, j].astype(np.float32))
+    assert q.node_count == sum(int(np.count_nonzero(q.level_norms(tier) >= 0)) for tier in range(q.depth + 1))
+    for (r, c) in [(0, 0), (17, 3), (199, 199), (5, 190)]:
+        assert q.get_element(r, c) == float(a[r, c])
+    with pytest.raises(IndexError):
+        q.get_element(200, 0)
+    with pytest.raises(NotImplementedError):
+        q.set_element(0, 0, 1.0)
+
+
+def _decode_all(keys):
+    ij = np.array([_decode(int(k)) for k in keys.tolist()], np.int64).reshape(-1, 2)
+    return ij[:, 0], ij[:, 1]
