@@ -163,8 +163,9 @@ int spamm_to_dense(const spamm_tree_view *t, float *out, int64_t ld, void *strea
 #define STEP_FIRST (1u << 16)   /* first record of its super-tile */
 #define STEP_LAST (1u << 17)    /* last record of its super-tile  */
 /* Work units of the numeric phase (tile_order).  A unit is a run [b, e) of consecutive step
- * records, stored as the pair (b, e).  The numeric kernel runs two teams of warps per SM; the
- * planner cuts the record stream into counts[12] pieces of equal weight (live tasks plus a constant
+ * records, stored as four ints (b, tb, ts, e): tb = end of the super-tile record b lies in (b
+ * itself when b starts a tile), ts = start of the tile record e - 1 lies in (e itself when e
+ * ends one).  The numeric kernel runs two teams of warps per SM; the planner cuts the record stream into counts[12] pieces of equal weight (live tasks plus a constant
  * per record), a whole number of rounds of one piece per team: units [0, counts[12]).  A piece may
  * begin and end inside a super-tile; the kernel then runs the head of the tile it begins at its
  * end first, its whole tiles next and the rest of the tile it starts in last, so that a piece never
@@ -209,7 +210,7 @@ typedef struct {
     spamm_step *steps;       /* [step_capacity]                                   */
     uint32_t *c_keys;        /* [leaf_capacity] product leaf keys, ascending      */
     int32_t *tile_off;       /* [leaf_capacity + 1] first step of each super-tile node */
-    int32_t *tile_order;     /* [leaf_capacity + SPAMM_UNIT_EXTRA] work units (b, e), two words each */
+    int32_t *tile_order;     /* [leaf_capacity + SPAMM_UNIT_EXTRA] work units, four words each, 16-byte aligned */
     int32_t *chain;          /* [leaf_capacity] hand-over state per product leaf (numeric phase scratch, zero between launches) */
     int64_t step_capacity;
     int64_t leaf_capacity;

@@ -157,6 +157,8 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
     const int vwarp = EX_TEAMS == 1 ? warp : (warp >> 1);          // 0 .. 7 consumers, 8 = the team's producer
     const size_t team_bytes = (size_t)nstages * 2 * EX_BLOCK_BYTES + EX_MAX_STAGES * (sizeof(StageDesc) + 16) + EX_ZERO_BYTES;
     static_assert(sizeof(StageDesc) == 208 && sizeof(spamm_step) == 64, "StageDesc layout");
+    static_assert((EX_MAX_STAGES * (sizeof(StageDesc) + 16) + EX_ZERO_BYTES) % 16 == 0 && EX_BLOCK_BYTES % 128 == 0,
+                  "the second team's buffers must stay aligned for the bulk copies");
     unsigned char *tbase = smem_raw + (size_t)team * team_bytes;
     unsigned char *sA = tbase;
     unsigned char *sB = tbase + (size_t)nstages * EX_BLOCK_BYTES;
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
         for (int x = 0; x < 5; ++x) nr[x] = plan_ok ? nr[x] : 0;
         const int first_piece = piece;
         const uint32_t *words = reinterpret_cast<const uint32_t *>(g.steps);
-        const int2 *units = reinterpret_cast<const int2 *>(g.pieces);
+        const int4 *units = reinterpret_cast<const int4 *>(g.pieces);
         auto slot_of = [&](int t) -> int {          // claim number -> unit slot, -1 = no work left
             if (t < P) return t;
             t -= P;
@@ -226,14 +228,13 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
         };
         // Cursor over the records of my units.  A unit [b, e) is run as: the head segment [me, e) of a tile
         // that the next unit finishes, the whole tiles [mb, me), the tail segment [b, mb) of a tile another
-        // unit began; mb and me follow from the first and the last record's tile length and position.
-        // The next unit is claimed in three steps while the last three records of the current one are
-        // fetched (counter, unit, its end records), so that none of the latencies is exposed.
+        // unit began; the planner stores with b and e where b's tile ends and where the tile of e - 1 starts.
+        // The next unit is claimed in two steps while the last records of the current one are fetched
+        // (counter, unit), so that neither latency is exposed.
         int run = 2, r = 0, rend = 0, rbeg = 0, left = 0, units_done = 0;
         int ub = 0, umb = 0, ume = 0, ue = 0;
-        int cstate = 1, tk = piece;               // 0: nothing claimed, 1: counter drawn, 2: unit loaded, 3: end records loaded, 4: no work left
-        int2 nu = make_int2(0, 0);
-        uint32_t wf = 0, wl = 0;
+        int cstate = 1, tk = piece;               // 0: nothing claimed, 1: counter drawn, 3: unit loaded, 4: no work left
+        int4 nu = make_int4(0, 0, 0, 0);
         bool more = true;
         auto claim_step = [&]() {
             if (cstate == 0) {
@@ -242,13 +243,7 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
             } else if (cstate == 1) {
                 const int slot = slot_of(__shfl_sync(FULL_MASK, tk, 0));
                 if (slot < 0) cstate = 4;
-                else { nu = __ldg(units + slot); cstate = 2; }
-            } else if (cstate == 2) {
-                if (nu.y > nu.x) {
-                    wf = __ldg(words + (size_t)nu.x * 16 + 15);
-                    wl = __ldg(words + (size_t)(nu.y - 1) * 16 + 15);
-                }
-                cstate = 3;
+                else { nu = __ldg(units + slot); cstate = 3; }
             }
         };
         // fetch: the next record of the cursor -> (word of lane l < 16, meta); meta = rec | first << 30 | last << 31, ~0 = none
@@ -262,21 +257,15 @@ __global__ void __launch_bounds__(EX_THREADS, EX_CTAS_PER_SM) execute_kernel(Exe
             }
             for (;;) {
                 if (!more) { wd = 0u; meta = 0xFFFFFFFFu; return; }
-                if (cstate < 3 && left <= 3 - cstate) claim_step();
+                if (cstate < 3 && left <= 2 - cstate) claim_step();
                 if (r < rend) break;
                 ++run;
                 if (run == 3) {
                     while (cstate < 3) claim_step();
                     if (cstate == 4) { more = false; continue; }
-                    ub = nu.x; ue = nu.y;
-                    umb = ub; ume = ue;
-                    if (ue > ub) {
-                        const int pos_b = (int)(wf >> 16), len_b = (int)(wf & 0xFFFFu);
-                        const int pos_l = (int)(wl >> 16), len_l = (int)(wl & 0xFFFFu);
-                        const int ts_l = ue - 1 - pos_l;
-                        umb = pos_b == 0 ? ub : min(ub - pos_b + len_b, ue);
-                        ume = ts_l + len_l == ue ? ue : max(ts_l, umb);
-                    }
+                    ub = nu.x; ue = nu.w;
+                    umb = ue > ub ? min(nu.y, ue) : ub;
+                    ume = ue > ub ? max(nu.z, umb) : ue;
                     left = ue - ub;
                     cstate = 0;
                     run = 0;

@@ -749,9 +749,14 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
         const unsigned long long x = (unsigned long long)g * WA / (unsigned long long)P;
         return x < 1ull ? 1ull : x;
     };
+    // a unit is (b, tb, ts, e): records [b, e); tb = end of the tile record b lies in (= b when b starts a
+    // tile), ts = start of the tile record e - 1 lies in (= e when e ends a tile).  The numeric kernel runs
+    // the head [max(ts, min(tb, e)), e) first, the whole tiles in between next and the tail [b, min(tb, e)) last.
     if (gtid == 0 && P > 0) {
-        uw[0] = 0;                              // piece 0 begins at record 0
-        uw[2 * (P - 1) + 1] = (int32_t)RA;      // the last piece ends with region A
+        uw[0] = 0;                              // piece 0 begins at record 0, at a tile start
+        uw[1] = 0;
+        uw[4 * (P - 1) + 2] = (int32_t)RA;      // the last piece ends with region A, at a tile end
+        uw[4 * (P - 1) + 3] = (int32_t)RA;
     }
     // one warp per tile: the records' weights in parallel, a warp scan, every lane places the cuts that
     // fall behind its record (cut g = boundary after the first record at which the prefix reaches target(g))
@@ -785,8 +790,11 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
                 if (g < 1) g = 1;
                 while (g < P && target_of(g) <= lo_w) ++g;
                 for (; g < P && target_of(g) <= hi_w; ++g) {
-                    uw[2 * g] = r + 1;                 // b of piece g
-                    uw[2 * (g - 1) + 1] = r + 1;       // e of piece g - 1
+                    const int c = r + 1;               // the cut: in (ts, te]
+                    uw[4 * g] = c;                            // b of piece g
+                    uw[4 * g + 1] = te;                       // its tile ends at te (c == te: b starts the next tile)
+                    uw[4 * (g - 1) + 2] = c == te ? c : ts;   // piece g - 1 ends in this tile
+                    uw[4 * (g - 1) + 3] = c;                  // e of piece g - 1
                 }
             }
             run += __shfl_sync(FULL_MASK, inc, 31);
@@ -818,9 +826,8 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
                 slot0 = __shfl_sync(FULL_MASK, slot0, __ffs(m) - 1);
                 if (in) {
                     const int se = l + 1 == nseg ? te : (l == 0 ? te - (nseg - 1) * sl : sb + sl);
-                    int32_t *u = uw + 2 * (P + (long long)x * nB + slot0 + __popc(m & lanemask_lt()));
-                    u[0] = sb;
-                    u[1] = se;
+                    int32_t *u = uw + 4 * (P + (long long)x * nB + slot0 + __popc(m & lanemask_lt()));
+                    *reinterpret_cast<int4 *>(u) = make_int4(sb, sb == ts ? sb : te, se == te ? se : ts, se);
                     sb = se;
                 }
             }

@@ -51,8 +51,8 @@ __host__ __device__ __forceinline__ uint32_t step_colmask(int dj)
     return dj == 0 ? 0x0505u : dj == 1 ? 0x0A0Au : dj == 2 ? 0x5050u : 0xA0A0u;
 }
 
-// plan.tile_order holds 2 ints per work unit (b, e), see plan_order_kernel
+// plan.tile_order holds 4 ints per work unit (b, end of b's tile, start of the tile of e - 1, e), see plan_order_kernel
 __host__ __device__ __forceinline__ int64_t spamm_unit_capacity(int64_t leaf_capacity)
 {
-    return (leaf_capacity + SPAMM_UNIT_EXTRA) / 2;
+    return (leaf_capacity + SPAMM_UNIT_EXTRA) / 4;
 }

@@ -24,6 +24,6 @@ print(json.dumps({"env": {k_: v for k_, v in os.environ.items() if k_.startswith
 if os.environ.get("SPAMM_EX_TRACE"):
     # for the weight model of the planner's partition: the pieces (region A units) and per-record work of this plan
     npieces = int(plan.counts[12].item())
-    pieces = plan.tile_order[: 2 * npieces].cpu().numpy().reshape(npieces, 2)
+    pieces = plan.tile_order[: 4 * npieces].cpu().numpy().reshape(npieces, 4)
     rec = plan.step_records()
     np.savez(os.environ["SPAMM_EX_TRACE"] + ".plan.npz", pieces=pieces, rec=rec)

@@ -27,7 +27,7 @@ for gran in ("fine4", "coarse16"):
             assert np.array_equal(c.level_norms(t), oc.level_norm(t)), (gran, it, "norms", t)
     cnt = plan.counts.cpu().numpy()
     npieces = int(cnt[12])
-    u = plan.tile_order[: 2 * npieces].cpu().numpy().reshape(npieces, 2)
+    u = plan.tile_order[: 4 * npieces].cpu().numpy().reshape(npieces, 4)[:, [0, 3]]
     flags = plan.step_records()[:, 1]
     chained = int(np.count_nonzero((flags[u[u[:, 1] > u[:, 0], 0]] & (1 << 16)) == 0))     # pieces that begin inside a super-tile
     print(f"{gran}: pieces={npieces} ranges={cnt[16:21].tolist()} chained={chained + int(cnt[19]) + int(cnt[20])} ")

@@ -19,10 +19,17 @@ def _units(plan):
     """(pieces of region A, [segments of layer 0, 1, 2 of region B], step records) of a device plan."""
     cnt = plan.counts.cpu().numpy()
     P, n, stride = int(cnt[12]), [int(x) for x in cnt[16:21]], int(cnt[21])
-    raw = plan.tile_order[: 2 * (P + 5 * stride)].cpu().numpy().reshape(-1, 2).astype(np.int64)
+    raw4 = plan.tile_order[: 4 * (P + 5 * stride)].cpu().numpy().reshape(-1, 4).astype(np.int64)
+    # a unit is (b, end of b's tile, start of the tile of e - 1, e); checked against the records below
+    _units.raw4 = np.concatenate([raw4[:P]] + [raw4[P + x * stride: P + x * stride + n[x]] for x in range(5)])
+    raw = raw4[:, [0, 3]]
     rng = [raw[P + x * stride: P + x * stride + n[x]] for x in range(5)]
     # ranges 0..2: first segments of the tiles with 3, 2, 1 segments; 3: second segments; 4: third segments
     return raw[:P], [np.concatenate(rng[:3]), rng[3], rng[4]], int(cnt[4])
+
+
+def lens_of(rec, r):
+    return int(rec[r, 15] & 0xFFFF)
 
 
 @pytest.mark.parametrize("n,tau", [(256, 1e-6), (1024, 1e-6), (2048, 1e-8), (4096, 1e-8), (4096, 1e-4)])
@@ -56,6 +63,13 @@ def test_units_cover_the_plan(n, tau):
     lens = np.diff(np.concatenate([starts, [R]]))
     assert np.array_equal(rec[:, 15] & 0xFFFF, np.repeat(lens, lens))
     assert np.array_equal(rec[:, 15] >> 16, np.concatenate([np.arange(x) for x in lens]))
+    # the tile bounds stored with every unit: end of the tile of record b (b itself at a tile start), start of
+    # the tile of record e - 1 (e itself at a tile end)
+    tile_start = np.repeat(starts, lens)
+    for ub, utb, uts, ue in _units.raw4:
+        if ue > ub:
+            assert utb == (ub if first[ub] else tile_start[ub] + lens_of(rec, ub)), (ub, utb)
+            assert uts == (ue if first[ue] else tile_start[ue - 1]), (ue, uts)
     # region A: equal weights; weight = live tasks + rec_weight per record (default 32)
     w = np.zeros(R, np.int64)
     for kk in range(4):
