@@ -223,38 +223,42 @@ __device__ __forceinline__ uint32_t lb_lo(unsigned long long w) { return (uint32
 __device__ __forceinline__ uint32_t lb_hi(unsigned long long w) { return (uint32_t)((w >> 31) & 0x7FFFFFFFull); }
 __device__ __forceinline__ unsigned long long lb_status(unsigned long long w) { return w >> 62; }
 
-// The same result for at most 128 tiles whose blocks are all resident: every tile publishes its
-// aggregate and reads ALL of its predecessors in one batch (four per lane, loads in flight
-// together) instead of walking back 32 at a time -- one memory round trip after the slowest tile.
+// The same result when block b takes tile b (blocks start in index order, so every predecessor is running
+// or done): every tile publishes its aggregate and reads ALL of its predecessors in batches of 256 (eight
+// per lane, loads in flight together) instead of walking back 32 at a time -- one memory round trip after
+// the slowest tile for up to 256 tiles.
+#define PLAN_ALL_EXCLUSIVE_MAX 1024
 __device__ __forceinline__ void all_exclusive_warp(volatile unsigned long long *state, int tile, uint32_t agg_lo,
                                                    uint32_t agg_hi, uint32_t &ex_lo, uint32_t &ex_hi)
 {
     const int lane = (int)(threadIdx.x & 31u);
     if (lane == 0) state[tile] = lb_pack(LB_AGGREGATE, agg_lo, agg_hi);   // the word is the whole message: no fence
-    unsigned long long w[4];
-    bool need[4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-        need[x] = lane + 32 * x < tile;
-        w[x] = 0ull;
-    }
-    bool again;
-    do {
-        again = false;
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-            if (need[x]) w[x] = state[lane + 32 * x];
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-            if (need[x]) {
-                if (lb_status(w[x]) == LB_INVALID) again = true;
-                else need[x] = false;
-            }
-    } while (__any_sync(0xFFFFFFFFu, again));
     uint32_t lo = 0, hi = 0;
+    for (int base = 0; base < tile; base += 256) {
+        unsigned long long w[8];
+        bool need[8];
 #pragma unroll
-    for (int x = 0; x < 4; ++x)
-        if (lane + 32 * x < tile) { lo += lb_lo(w[x]); hi += lb_hi(w[x]); }
+        for (int x = 0; x < 8; ++x) {
+            need[x] = base + lane + 32 * x < tile;
+            w[x] = 0ull;
+        }
+        bool again;
+        do {
+            again = false;
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+                if (need[x]) w[x] = state[base + lane + 32 * x];
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+                if (need[x]) {
+                    if (lb_status(w[x]) == LB_INVALID) again = true;
+                    else need[x] = false;
+                }
+        } while (__any_sync(0xFFFFFFFFu, again));
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+            if (base + lane + 32 * x < tile) { lo += lb_lo(w[x]); hi += lb_hi(w[x]); }
+    }
     ex_lo = __reduce_add_sync(0xFFFFFFFFu, lo);
     ex_hi = __reduce_add_sync(0xFFFFFFFFu, hi);
 }
@@ -375,33 +379,35 @@ __device__ __forceinline__ unsigned long long lb64_exclusive_warp(volatile unsig
     }
     return sum;
 }
-// at most 128 tiles, all resident (see all_exclusive_warp): aggregates only, read in one batch
+// block b takes tile b (see all_exclusive_warp): aggregates only, read in batches of 256
 __device__ __forceinline__ unsigned long long all64_exclusive_warp(volatile unsigned long long *state, int tile)
 {
     const int lane = (int)(threadIdx.x & 31u);
-    unsigned long long w[4];
-    bool need[4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-        need[x] = lane + 32 * x < tile;
-        w[x] = 0ull;
-    }
-    bool again;
-    do {
-        again = false;
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-            if (need[x]) w[x] = state[lane + 32 * x];
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-            if (need[x]) {
-                if (lb_status(w[x]) == LB_INVALID) again = true;
-                else need[x] = false;
-            }
-    } while (__any_sync(0xFFFFFFFFu, again));
     unsigned long long s = 0ull;
+    for (int base = 0; base < tile; base += 256) {
+        unsigned long long w[8];
+        bool need[8];
 #pragma unroll
-    for (int x = 0; x < 4; ++x)
-        if (lane + 32 * x < tile) s += w[x] & LB64_MASK;
+        for (int x = 0; x < 8; ++x) {
+            need[x] = base + lane + 32 * x < tile;
+            w[x] = 0ull;
+        }
+        bool again;
+        do {
+            again = false;
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+                if (need[x]) w[x] = state[base + lane + 32 * x];
+#pragma unroll
+            for (int x = 0; x < 8; ++x)
+                if (need[x]) {
+                    if (lb_status(w[x]) == LB_INVALID) again = true;
+                    else need[x] = false;
+                }
+        } while (__any_sync(0xFFFFFFFFu, again));
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+            if (base + lane + 32 * x < tile) s += w[x] & LB64_MASK;
+    }
     return warp_sum_u64(s);
 }

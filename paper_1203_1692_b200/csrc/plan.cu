@@ -284,7 +284,7 @@ struct TileArgs {
     unsigned long long *trace;   // tuning aid (SPAMM_PLAN_TRACE): per block 6 timestamps
     unsigned long long *tile_wprefix;   // tasks in the super-tile nodes before each node (one extra entry: all)
     volatile unsigned long long *tile_state_w;   // look-back states of that prefix
-    int all_resident;            // every block of the grid is resident at once (one per SM on this device)
+    int all_resident;            // block b may take tile b: the grid has a block per tile
     const float *norm_a;      // leaf level grid of A, row-major (i,k)
     const float *norm_bt;     // leaf level grid of B transposed (j,k)
     const int32_t *slot_a;    // leaf slots of A (i,k)
@@ -409,11 +409,12 @@ __device__ __forceinline__ LaneTests tile_tests(const TileArgs &a, const LaneNor
 
 // DENSE: there is no list from a coarser level; every super-tile node of the 2^tl x 2^tl grid
 // (tl <= PLAN_DENSE_MAX_LEVEL) builds its candidate list itself from the level-tl norms, into shared memory.
-#define TILE_WARPS 32          // one super-tile node per warp, 32 per block: short look-back chains
-#define TILE_THREADS (TILE_WARPS * 32)
-template <bool DENSE>
-__global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
+// TW: super-tile nodes (= warps) per block.  32 keeps the look-back chains of a large product short; a small
+// dense start uses 8, so that the blocks on the band -- the only ones with work -- spread over all SMs.
+template <bool DENSE, int TW>
+__global__ void __launch_bounds__(TW * 32, 2048 / (TW * 32) / 2) plan_tiles_kernel(TileArgs a)
 {
+    constexpr int TILE_WARPS = TW;
     pdl_enter();
     __shared__ int s_tile;
     __shared__ uint32_t s_wsteps[TILE_WARPS], s_wleaves[TILE_WARPS], s_wtasks[TILE_WARPS];
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(TILE_THREADS) plan_tiles_kernel(TileArgs a)
             if (lane == 0) lb64_publish(a.tile_state_w, tile, (unsigned long long)rt);
             uint32_t ex_lo, ex_hi;
             unsigned long long ex_w;
-            if (fixed_tiles && ntiles <= 128) {
+            if (fixed_tiles && ntiles <= PLAN_ALL_EXCLUSIVE_MAX) {
                 all_exclusive_warp(a.tile_state, tile, rs, rl, ex_lo, ex_hi);
                 ex_w = all64_exclusive_warp(a.tile_state_w, tile);
             } else {
@@ -867,6 +868,366 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
     for (int x = t; x < (int)(sizeof(PlanShared) / 4); x += blockDim.x) sh[x] = 0u;
 }
 
+// ---- small dense products (n <= 4096): count, then emit and cut ----------------------------------
+// Two kernels instead of plan_tiles + plan_order.  Only the super-tiles on the band have work, and with
+// one node per warp and 32 warps per block they sit in a quarter of the blocks; here a block has 8
+// nodes, so the band spreads over all SMs, and nobody polls: plan_count_kernel leaves one aggregate
+// per block, plan_emit_kernel (after it, programmatic dependent launch) sums the aggregates of its
+// predecessors, writes the records and -- the totals being known to every block -- places the cuts of
+// the numeric kernel's pieces while the records' live words are still in registers.
+#define SMALL_WARPS 8
+#define SMALL_MAX_TILES 512          // 64 x 64 super-tile nodes / 8
+struct SmallArgs {
+    TileArgs t;
+    unsigned long long *node_info;   // per node, between the kernels: records | present << 8 | tasks << 24 (= tile_wprefix)
+    unsigned long long *agg_a;       // per block: records | product leaves << 32
+    unsigned long long *agg_b;       // per block: tasks | super-tiles with records << 32
+    int32_t *units;
+    int64_t unit_capacity;
+    int num_teams, piece_records, rec_weight, tail_records, tail_percent;
+};
+
+__device__ __forceinline__ void small_clear(const TileArgs &a)
+{
+    if (blockIdx.x == 0 && threadIdx.x < 8) a.out_counts[16 + threadIdx.x] = 0;     // accumulated by plan_emit_kernel
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gsz = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t x = gtid; x < a.chain_words; x += gsz) a.chain[x] = 0;
+    if (a.c_slot) {
+        for (int64_t x = gtid; x < a.cells; x += gsz) {
+            a.c_slot[x] = -1;
+            a.c_slot_t[x] = -1;
+            a.c_norm[x] = -1.0f;
+            a.c_norm_t[x] = -1.0f;
+            a.c_leaf_sq_grid[x] = 0.0;
+        }
+    }
+}
+
+// candidates K of node (I,J): the level-tl test (symbolic.py:118-125 one level up); returns their number
+__device__ __forceinline__ int small_candidates(const TileArgs &a, uint32_t I, uint32_t J, uint32_t rowok, uint32_t *ks)
+{
+    const uint32_t lane = lane_id();
+    int e = 0;
+    if (rowok) {
+        for (int k0 = 0; k0 < a.St; k0 += 32) {
+            const int K = k0 + (int)lane;
+            const bool pass = K < a.St && norm_test(__ldg(a.norm_a_t + (int64_t)I * a.St + K),
+                                                    __ldg(a.norm_bt_t + (int64_t)J * a.St + K), a.tau);
+            const uint32_t bal = __ballot_sync(FULL_MASK, pass);
+            if (pass) ks[e + __popc(bal & lanemask_lt())] = (uint32_t)K;
+            e += __popc(bal);
+        }
+    }
+    __syncwarp();
+    return e;
+}
+
+__global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_count_kernel(SmallArgs sa)
+{
+    const TileArgs &a = sa.t;
+    pdl_enter();
+    __shared__ uint32_t s_ks[SMALL_WARPS][1 << PLAN_DENSE_MAX_LEVEL];
+    __shared__ uint32_t s_steps[SMALL_WARPS], s_leaves[SMALL_WARPS], s_tasks[SMALL_WARPS];
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = lane_id();
+    const int n_nodes = a.St * a.St;
+    const int sub = a.sub, per = 32 / sub;
+    const uint32_t kk = lane % sub;
+    small_clear(a);
+    const int pidx = (int)blockIdx.x * SMALL_WARPS + warp;
+    uint32_t nsteps = 0, present = 0, ntasks = 0;
+    if (pidx < n_nodes) {
+        uint32_t I, J, rowok = 0;
+        morton_decode((uint32_t)pidx, I, J);
+        for (int d = 0; d < sub; ++d) {
+            const int row = (int)(sub * I + d);
+            if (row >= a.row0 && row < a.row1) rowok |= 1u << d;
+        }
+        const uint32_t *ks = s_ks[warp];
+        const int e = small_candidates(a, I, J, rowok, s_ks[warp]);
+        LaneNorms nrm = tile_norms(a, I, J, ((int)lane / sub < e) ? sub * ks[(int)lane / sub] + kk : 0u, (int)lane / sub < e);
+        for (int b = 0; b < e; b += per) {
+            const int t = b + (int)lane / sub, t2 = t + per;
+            const LaneNorms nxt = tile_norms(a, I, J, t2 < e ? sub * ks[t2] + kk : 0u, t2 < e);
+            uint32_t live = 0;
+            if (t < e) live = tile_tests<false>(a, nrm, rowok).live;
+            nrm = nxt;
+            uint32_t groups = __ballot_sync(FULL_MASK, live != 0);
+            if (sub >= 2) groups |= groups >> 1;
+            if (sub >= 4) groups |= groups >> 2;
+            groups &= (sub == 4 ? 0x11111111u : sub == 2 ? 0x55555555u : 0xFFFFFFFFu);
+            nsteps += __popc(groups);
+            present |= live;
+            ntasks += __popc(live);
+        }
+        present = __reduce_or_sync(FULL_MASK, present);
+        ntasks = __reduce_add_sync(FULL_MASK, ntasks);
+        if (lane == 0)
+            sa.node_info[pidx] = (unsigned long long)nsteps | ((unsigned long long)present << 8) | ((unsigned long long)ntasks << 24);
+    }
+    if (lane == 0) { s_steps[warp] = nsteps; s_leaves[warp] = __popc(present); s_tasks[warp] = ntasks; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long st = 0, lv = 0, tk = 0, ne = 0;
+        for (int w = 0; w < SMALL_WARPS; ++w) { st += s_steps[w]; lv += s_leaves[w]; tk += s_tasks[w]; ne += s_steps[w] ? 1u : 0u; }
+        sa.agg_a[blockIdx.x] = st | (lv << 32);
+        sa.agg_b[blockIdx.x] = tk | (ne << 32);
+    }
+}
+
+__global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArgs sa)
+{
+    const TileArgs &a = sa.t;
+    __shared__ uint32_t s_ks[SMALL_WARPS][1 << PLAN_DENSE_MAX_LEVEL];
+    __shared__ unsigned long long s_a[SMALL_MAX_TILES], s_b[SMALL_MAX_TILES];     // exclusive prefixes of the block aggregates
+    __shared__ unsigned long long s_wa[SMALL_WARPS], s_wb[SMALL_WARPS], s_tot[2];
+    __shared__ int s_bB;
+    const int warp = threadIdx.x >> 5, t = threadIdx.x;
+    const uint32_t lane = lane_id();
+    const int n_nodes = a.St * a.St;
+    const int ntiles = (int)gridDim.x;
+    const int sub = a.sub, per = 32 / sub;
+    const uint32_t kk = lane % sub, grp = (lane / sub) * sub;
+    const int pidx = (int)blockIdx.x * SMALL_WARPS + warp;
+    const bool valid = pidx < n_nodes;
+    uint32_t I = 0, J = 0, rowok = 0;
+    if (valid) {
+        morton_decode((uint32_t)pidx, I, J);
+        for (int d = 0; d < sub; ++d) {
+            const int row = (int)(sub * I + d);
+            if (row >= a.row0 && row < a.row1) rowok |= 1u << d;
+        }
+    }
+    // the candidate lists again (level-tl norms: independent of the preceding kernel)
+    const uint32_t *ks = s_ks[warp];
+    const int e = valid ? small_candidates(a, I, J, rowok, s_ks[warp]) : 0;
+    pdl_enter();
+    // ---- every block: prefix sums over ALL block aggregates (at most 512: two per thread)
+    {
+        unsigned long long va[2], vb[2];
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+            const int i = 2 * t + x;
+            va[x] = i < ntiles ? __ldcg(sa.agg_a + i) : 0ull;
+            vb[x] = i < ntiles ? __ldcg(sa.agg_b + i) : 0ull;
+        }
+        unsigned long long ia = va[0] + va[1], ib = vb[0] + vb[1];       // inclusive scan of the pair sums
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long xa = __shfl_up_sync(FULL_MASK, ia, d), xb = __shfl_up_sync(FULL_MASK, ib, d);
+            if (lane >= (uint32_t)d) { ia += xa; ib += xb; }
+        }
+        if (lane == 31) { s_wa[warp] = ia; s_wb[warp] = ib; }
+        __syncthreads();
+        unsigned long long oa = 0, ob = 0;
+        for (int w = 0; w < warp; ++w) { oa += s_wa[w]; ob += s_wb[w]; }
+        const unsigned long long ea = oa + ia - (va[0] + va[1]), eb = ob + ib - (vb[0] + vb[1]);     // exclusive, first of the pair
+        if (2 * t < SMALL_MAX_TILES) { s_a[2 * t] = ea; s_b[2 * t] = eb; }
+        if (2 * t + 1 < SMALL_MAX_TILES) { s_a[2 * t + 1] = ea + va[0]; s_b[2 * t + 1] = eb + vb[0]; }
+        if (t == SMALL_WARPS * 32 - 1) { s_tot[0] = oa + ia; s_tot[1] = ob + ib; }
+        if (t == 0) s_bB = -1;
+        __syncthreads();
+    }
+    const long long R = (long long)(s_tot[0] & 0xFFFFFFFFull), LC = (long long)(s_tot[0] >> 32);
+    const unsigned long long T = s_tot[1] & 0xFFFFFFFFull;
+    const int n_tiles = (int)(s_tot[1] >> 32);                   // super-tiles with at least one record
+    const bool overflow = R > a.cap_steps || LC > a.cap_leaves;
+    const unsigned long long RW = (unsigned long long)sa.rec_weight;
+    const unsigned long long W = T + RW * (unsigned long long)R;
+    auto wblock = [&](int i) -> unsigned long long { return (s_b[i] & 0xFFFFFFFFull) + RW * (s_a[i] & 0xFFFFFFFFull); };
+    // ---- region B (plan_order_kernel's rule, at block granularity): where it begins
+    int bB = ntiles;
+    const int max_b_nodes = (int)(sa.unit_capacity / 10 < ORDER_MAX_B_NODES ? sa.unit_capacity / 10 : ORDER_MAX_B_NODES);
+    const int tail_records = sa.tail_records >= 0 ? sa.tail_records : (R < 3ll * sa.num_teams ? 3 : 0);
+    if (tail_records > 0 && n_tiles > 0 && R > 0 && max_b_nodes >= SMALL_WARPS && !overflow) {
+        unsigned long long wB = W * (unsigned long long)sa.tail_percent / 100ull;
+        const unsigned long long wmin = W * (unsigned long long)(sa.num_teams + sa.num_teams / 4) / (unsigned long long)n_tiles;
+        if (wB < wmin) wB = wmin;
+        const unsigned long long targetA = wB >= W ? 0ull : W - wB;
+        const int lo = ntiles > max_b_nodes / SMALL_WARPS ? ntiles - max_b_nodes / SMALL_WARPS : 0;       // region B is capped
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+            const int i = 2 * t + x;
+            if (i < ntiles && (i == lo || (i > lo && wblock(i) <= targetA))) atomicMax(&s_bB, i);
+        }
+        __syncthreads();
+        bB = s_bB;
+    }
+    const long long RA = bB < ntiles ? (long long)(s_a[bB] & 0xFFFFFFFFull) : R;
+    const unsigned long long WA = bB < ntiles ? wblock(bB) : W;
+    const int idxB = bB < ntiles ? bB * SMALL_WARPS : n_nodes;
+    const int nB = n_nodes - idxB;
+    // ---- region A: pieces, one per team, or several rounds of them when the product is large
+    long long rounds = RA / ((long long)sa.num_teams * sa.piece_records);
+    if (rounds < 1) rounds = 1;
+    if (rounds > 64) rounds = 64;
+    const int64_t cap_a = sa.unit_capacity - 5ll * max_b_nodes;
+    if (rounds * sa.num_teams > cap_a) rounds = cap_a / sa.num_teams;
+    const long long P = (RA > 0 && !overflow) ? (rounds >= 1 ? rounds * sa.num_teams : cap_a) : 0;
+    int32_t *__restrict__ uw = sa.units;
+    auto target_of = [&](long long g) -> unsigned long long {
+        const unsigned long long x = (unsigned long long)g * WA / (unsigned long long)P;
+        return x < 1ull ? 1ull : x;
+    };
+    if (blockIdx.x == 0) {
+        // the plan's counts (spamm_b200.h); [16..20] are accumulated below by the blocks of region B
+        if (t < 16) {
+            int32_t v = 0;
+            if (t == 0) v = (int32_t)LC;
+            if (t == 1) v = n_tiles;
+            if (t == 2) v = overflow ? 1 : 0;
+            if (t == 4) v = (int32_t)R;
+            if (t == 5) v = (int32_t)(P + 5ll * nB);
+            if (t == 6) v = (int32_t)(T & 0xFFFFFFFFull);
+            if (t == 7) v = (int32_t)(T >> 32);
+            if (t == 11) v = n_nodes;
+            if (t == 12) v = (int32_t)P;
+            a.out_counts[t] = v;
+        }
+        if (t == 16) a.out_counts[21] = nB;
+        if (t == 17) { a.tile_off[n_nodes] = (int32_t)R; sa.node_info[n_nodes] = T; }
+        if (t == 18 && P > 0) {
+            uw[0] = 0;                              // piece 0 begins at record 0, at a tile start
+            uw[1] = 0;
+            uw[4 * (P - 1) + 2] = (int32_t)RA;      // the last piece ends with region A, at a tile end
+            uw[4 * (P - 1) + 3] = (int32_t)RA;
+        }
+    }
+    // ---- my node: what plan_count_kernel found, and where its records and leaves go
+    unsigned long long info = valid ? __ldcg(sa.node_info + pidx) : 0ull;
+    __syncthreads();                                 // every warp has its node's word before any is overwritten
+    const uint32_t nsteps = (uint32_t)(info & 0xFFu), present = (uint32_t)((info >> 8) & 0xFFFFu);
+    const uint32_t ntasks = (uint32_t)(info >> 24), nleaves = __popc(present);
+    if (lane == 0) { s_wa[warp] = nsteps | ((unsigned long long)nleaves << 32); s_wb[warp] = ntasks; }
+    __syncthreads();
+    unsigned long long oa = s_a[blockIdx.x], ob = s_b[blockIdx.x] & 0xFFFFFFFFull;
+    for (int w = 0; w < warp; ++w) { oa += s_wa[w]; ob += s_wb[w]; }
+    int64_t sb = (int64_t)(oa & 0xFFFFFFFFull);
+    const int64_t cb = (int64_t)(oa >> 32);
+    if (valid && lane == 0) {
+        a.tile_off[pidx] = (int32_t)sb;
+        sa.node_info[pidx] = ob;                     // tasks before this node (tile_wprefix)
+    }
+    if (!valid || nsteps == 0 || overflow) return;
+    const int ts = (int)sb, te = (int)sb + (int)nsteps;
+    // ---- region B: layered segments of this node (lane 0), slots by one atomic per range
+    if (pidx >= idxB) {
+        if (lane == 0) {
+            const int sl = tail_records > 0 ? tail_records : 1;
+            const int ns = te - ts;
+            const int nseg = ns <= sl ? 1 : (ns <= 2 * sl ? 2 : 3);
+            int sbeg = ts;
+#pragma unroll
+            for (int x = 0; x < 5; ++x) {
+                const int l = x < 3 ? 0 : x - 2;
+                const bool in = x < 3 ? nseg == 3 - x : nseg > l;
+                if (!in) continue;
+                const int slot = atomicAdd(&a.out_counts[16 + x], 1);
+                const int se = l + 1 == nseg ? te : (l == 0 ? te - (nseg - 1) * sl : sbeg + sl);
+                *reinterpret_cast<int4 *>(uw + 4 * (P + (long long)x * nB + slot)) =
+                    make_int4(sbeg, sbeg == ts ? sbeg : te, se == te ? se : ts, se);
+                sbeg = se;
+            }
+        }
+    }
+    // does a cut of region A fall into this tile?  (cut g sits behind the first record at which the weight
+    // prefix reaches target(g))
+    const unsigned long long w0 = ob + RW * (unsigned long long)ts;
+    const unsigned long long w1 = w0 + ntasks + RW * (unsigned long long)nsteps;
+    bool cuts = false;
+    if (pidx < idxB && P > 1) {
+        long long g0 = (long long)(w0 * (unsigned long long)P / WA);
+        if (g0 < 1) g0 = 1;
+        while (g0 < P && target_of(g0) <= w0) ++g0;
+        cuts = g0 < P && target_of(g0) <= w1;
+    }
+    // ---- product leaf keys and step records, in ascending K (plan_tiles_kernel's phase 3)
+    if (lane < 16 && (present >> lane & 1u))
+        a.c_keys[cb + __popc(present & ((1u << lane) - 1u))] = (uint32_t)pidx * (uint32_t)(sub * sub) + lane;
+    const int64_t s_first = sb, s_last = sb + nsteps - 1;
+    const uint32_t lt = lanemask_lt();
+    const uint32_t lead_mask = (sub == 4 ? 0x11111111u : sub == 2 ? 0x55555555u : 0xFFFFFFFFu);
+    unsigned long long run = w0;
+    LaneNorms nrm = tile_norms(a, I, J, ((int)lane / sub < e) ? sub * ks[(int)lane / sub] + kk : 0u, (int)lane / sub < e);
+    for (int b = 0; b < e; b += per) {
+        const int tt = b + (int)lane / sub, t2 = tt + per;
+        const LaneNorms nxt = tile_norms(a, I, J, t2 < e ? sub * ks[t2] + kk : 0u, t2 < e);
+        LaneTests lt4{0u, 0u, 0u, 0u, 0u};
+        uint32_t K = 0;
+        if (tt < e) {
+            K = ks[tt];
+            lt4 = tile_tests<true>(a, nrm, rowok, I, J, (uint32_t)sub * K + kk);
+        }
+        nrm = nxt;
+        uint32_t live4[4] = {0, 0, 0, 0}, dead4[4] = {0, 0, 0, 0}, a_present = 0, b_present = 0, any = 0;
+        int a_best = 16, b_best = 16;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            const int src = (int)grp + (x < sub ? x : 0);
+            const uint32_t lv = __shfl_sync(FULL_MASK, lt4.live | (lt4.full << 16), src);
+            const uint32_t dd = __shfl_sync(FULL_MASK, lt4.dead, src);
+            const uint32_t ah = __shfl_sync(FULL_MASK, lt4.a_here, src);
+            const uint32_t bh = __shfl_sync(FULL_MASK, lt4.b_here, src);
+            if (x < sub) {
+                live4[x] = lv;
+                dead4[x] = dd;
+                any |= lv & 0xFFFFu;
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                    if (ah >> d & 1u) { a_present |= 1u << step_pos(d, x); }
+                    if (bh >> d & 1u) { b_present |= 1u << step_pos(x, d); }
+                }
+            }
+        }
+        if (a_present) a_best = __ffs(a_present) - 1;
+        if (b_present) b_best = __ffs(b_present) - 1;
+        const bool writer = any != 0 && lane == grp;
+        const uint32_t bal = __ballot_sync(FULL_MASK, writer);
+        const int64_t x = sb + __popc(bal & lt);
+        if (writer) {
+            uint32_t flags = 0;
+            if (x == s_first) flags |= STEP_FIRST;
+            if (x == s_last) flags |= STEP_LAST;
+            const uint32_t a_first = (uint32_t)__ldg(
+                a.slot_a + (int64_t)(sub * I + step_pos_di(a_best)) * a.L + (sub * K + step_pos_dj(a_best)));
+            const uint32_t b_first = (uint32_t)__ldg(
+                a.slot_bt + (int64_t)(sub * J + step_pos_dj(b_best)) * a.L + (sub * K + step_pos_di(b_best)));
+            uint4 *rec = reinterpret_cast<uint4 *>(a.steps + x);
+            rec[0] = make_uint4(K, flags, (uint32_t)cb, (uint32_t)pidx);
+            rec[1] = make_uint4(a_first, a_present, b_first, b_present);
+            rec[2] = make_uint4(live4[0], live4[1], live4[2], live4[3]);
+            rec[3] = make_uint4(present, dead4[0] | (dead4[1] << 16), dead4[2] | (dead4[3] << 16),
+                                nsteps | ((uint32_t)(x - s_first) << 16));
+        }
+        if (cuts) {
+            // weight prefix behind every record of this pass, in record order (the writers, ascending lanes)
+            const unsigned long long wr = writer ? RW + __popc(live4[0] & 0xFFFFu) + __popc(live4[1] & 0xFFFFu) +
+                                                       __popc(live4[2] & 0xFFFFu) + __popc(live4[3] & 0xFFFFu) : 0ull;
+            unsigned long long inc = wr;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const unsigned long long y = __shfl_up_sync(FULL_MASK, inc, d);
+                if (lane >= (uint32_t)d) inc += y;
+            }
+            const unsigned long long hi_w = run + inc, lo_w = hi_w - wr;
+            if (writer) {
+                long long g = (long long)(lo_w * (unsigned long long)P / WA);
+                if (g < 1) g = 1;
+                while (g < P && target_of(g) <= lo_w) ++g;
+                for (; g < P && target_of(g) <= hi_w; ++g) {
+                    const int c = (int)x + 1;                 // the cut: in (ts, te]
+                    uw[4 * g] = c;
+                    uw[4 * g + 1] = te;
+                    uw[4 * (g - 1) + 2] = c == te ? c : ts;
+                    uw[4 * (g - 1) + 3] = c;
+                }
+            }
+            run += __shfl_sync(FULL_MASK, inc, 31);
+        }
+        sb += __popc(bal & lead_mask);
+    }
+}
+
 // ---- host side ---------------------------------------------------------------------------------
 int spamm_execute_piece_base();     // pieces per round = teams of the numeric kernel (execute.cu)
 
@@ -1012,8 +1373,11 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     TileArgs t;
     t.trace = nullptr;
     static const char *trace_path = getenv("SPAMM_PLAN_TRACE");      // tuning aid: allocates and synchronises
-    // two 1024-thread blocks per SM; a dense start with at most one tile per SM (n <= 4096) keeps one
-    const int tgrid = (dense && tl <= 6) ? SPAMM_NUM_SMS : SPAMM_NUM_SMS * 2;
+    // a small dense start (n <= 4096): blocks of 8 nodes, count + emit kernels; else two 1024-thread blocks
+    // per SM that draw tiles of 32 nodes from a counter
+    static const bool small_off = getenv("SPAMM_PLAN_SMALL") && atoi(getenv("SPAMM_PLAN_SMALL")) == 0;    // tuning aid
+    const bool small = dense && tl <= 6 && !small_off;
+    const int tgrid = small ? ((1 << (2 * tl)) + SMALL_WARPS - 1) / SMALL_WARPS : (dense && tl <= 6) ? SPAMM_NUM_SMS : SPAMM_NUM_SMS * 2;
     if (trace_path && cudaMalloc(&t.trace, 8 * 6 * tgrid) == cudaSuccess) cudaMemsetAsync(t.trace, 0, 8 * 6 * tgrid, st);
     t.norm_a_t = a->norm + spamm_level_offset(tl);
     t.norm_bt_t = b->norm_t + spamm_level_offset(tl);
@@ -1061,10 +1425,6 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     }
     t.tile_counter = &w.shared->tile_counter[PLAN_MAX_LEVELS];
     t.tile_state = w.tile_state[PLAN_MAX_LEVELS];
-    if (spamm_launch_pdl(dense ? plan_tiles_kernel<true> : plan_tiles_kernel<false>,
-                         dim3(tgrid), dim3(TILE_THREADS), 0, st, t) != cudaSuccess)
-        return SPAMM_ECUDA;
-    SPAMM_CHECK_LAUNCH();
     // tuning aids: records per piece from which a product is cut into several rounds of pieces,
     // and the weight of a record (in tasks) in the balance
     static const int piece_records = plan_env("SPAMM_PIECE_RECORDS", 192, 1, 1 << 20);
@@ -1073,6 +1433,32 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     // (SPAMM_TAIL_RECORDS = -1: decide by the size of the plan; 0: never; n: always, n records per short segment)
     static const int tail_records = plan_env("SPAMM_TAIL_RECORDS", -1, -1, 64);
     static const int tail_percent = plan_env("SPAMM_TAIL_PERCENT", 25, 0, 100);
+    if (small) {
+        // count, then emit + cut: two kernels, no look-back, no separate ordering kernel (see plan_count_kernel)
+        SmallArgs sa;
+        sa.t = t;
+        sa.node_info = w.tile_wprefix;
+        sa.agg_a = reinterpret_cast<unsigned long long *>(w.buf[0].node);      // level lists: unused by a dense start
+        sa.agg_b = reinterpret_cast<unsigned long long *>(w.buf[1].node);
+        sa.units = out->tile_order;
+        sa.unit_capacity = spamm_unit_capacity(out->leaf_capacity);
+        sa.num_teams = spamm_execute_piece_base(); sa.piece_records = piece_records; sa.rec_weight = rec_weight;
+        sa.tail_records = tail_records;
+        sa.tail_percent = tail_percent;
+        if (spamm_launch_pdl(plan_count_kernel, dim3(tgrid), dim3(SMALL_WARPS * 32), 0, st, sa) != cudaSuccess) return SPAMM_ECUDA;
+        SPAMM_CHECK_LAUNCH();
+        if (spamm_launch_pdl(plan_emit_kernel, dim3(tgrid), dim3(SMALL_WARPS * 32), 0, st, sa) != cudaSuccess) return SPAMM_ECUDA;
+        SPAMM_CHECK_LAUNCH();
+        if (clean_words) {
+            *clean_ptr = reinterpret_cast<uint32_t *>(w.shared);
+            *clean_words = cgrid != nullptr ? (int)(offsetof(PlanShared, exec_ticket) / 4) : 0;
+        }
+        return SPAMM_OK;
+    }
+    if (spamm_launch_pdl(dense ? plan_tiles_kernel<true, 32> : plan_tiles_kernel<false, 32>,
+                         dim3(tgrid), dim3(32 * 32), 0, st, t) != cudaSuccess)
+        return SPAMM_ECUDA;
+    SPAMM_CHECK_LAUNCH();
     if (t.trace) {
         unsigned long long *h = (unsigned long long *)malloc(8 * 6 * tgrid);
         cudaStreamSynchronize(st);
