@@ -25,8 +25,8 @@ extern "C" int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b
 {
     if (!a || !b || !plan || !c) return SPAMM_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    // Four kernels, no memset: plan tiles, plan order (which also empties C's leaf grids, publishes
-    // the counts and returns the workspace to its all-zero state), execute, interior norms.
+    // Four kernels, no memset: plan count (which also empties C's leaf grids), plan emit (records, pieces,
+    // counts), execute, interior norms; deep trees: root / expand / tiles / order in place of the first two.
     if (!plan_ws) return SPAMM_EWORKSPACE;
     static const int stop = getenv("SPAMM_PIPE_STOP") ? atoi(getenv("SPAMM_PIPE_STOP")) : 0;   // tuning aid: truncate
     uint32_t *clean_ptr = nullptr;      // planner state the numeric kernel returns to zero

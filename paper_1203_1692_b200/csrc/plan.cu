@@ -885,6 +885,7 @@ struct SmallArgs {
     int32_t *units;
     int64_t unit_capacity;
     int num_teams, piece_records, rec_weight, tail_records, tail_percent;
+    int dbg;                         // tuning aid (SPAMM_PLAN_DEBUG, with SPAMM_PIPE_STOP=2 only): 1 = place no cuts, 2 = no classification
 };
 
 __device__ __forceinline__ void small_clear(const TileArgs &a)
@@ -926,6 +927,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_count_kernel(SmallAr
 {
     const TileArgs &a = sa.t;
     pdl_enter();
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6] = plan_timer();
     __shared__ uint32_t s_ks[SMALL_WARPS][1 << PLAN_DENSE_MAX_LEVEL];
     __shared__ uint32_t s_steps[SMALL_WARPS], s_leaves[SMALL_WARPS], s_tasks[SMALL_WARPS];
     const int warp = threadIdx.x >> 5;
@@ -972,6 +974,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_count_kernel(SmallAr
         for (int w = 0; w < SMALL_WARPS; ++w) { st += s_steps[w]; lv += s_leaves[w]; tk += s_tasks[w]; ne += s_steps[w] ? 1u : 0u; }
         sa.agg_a[blockIdx.x] = st | (lv << 32);
         sa.agg_b[blockIdx.x] = tk | (ne << 32);
+        if (a.trace) a.trace[blockIdx.x * 6 + 1] = plan_timer();
     }
 }
 
@@ -1001,7 +1004,9 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArg
     // the candidate lists again (level-tl norms: independent of the preceding kernel)
     const uint32_t *ks = s_ks[warp];
     const int e = valid ? small_candidates(a, I, J, rowok, s_ks[warp]) : 0;
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 2] = plan_timer();
     pdl_enter();
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 3] = plan_timer();
     // ---- every block: prefix sums over ALL block aggregates (at most 512: two per thread)
     {
         unsigned long long va[2], vb[2];
@@ -1028,6 +1033,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArg
         if (t == 0) s_bB = -1;
         __syncthreads();
     }
+    if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 6 + 4] = plan_timer();
     const long long R = (long long)(s_tot[0] & 0xFFFFFFFFull), LC = (long long)(s_tot[0] >> 32);
     const unsigned long long T = s_tot[1] & 0xFFFFFFFFull;
     const int n_tiles = (int)(s_tot[1] >> 32);                   // super-tiles with at least one record
@@ -1065,10 +1071,13 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArg
     if (rounds * sa.num_teams > cap_a) rounds = cap_a / sa.num_teams;
     const long long P = (RA > 0 && !overflow) ? (rounds >= 1 ? rounds * sa.num_teams : cap_a) : 0;
     int32_t *__restrict__ uw = sa.units;
+    // the same function of g in every thread (all that matters); products stay below 2^53
+    const double wa_over_p = (double)WA / (double)(P > 0 ? P : 1), p_over_wa = (double)P / (double)(WA > 0 ? WA : 1);
     auto target_of = [&](long long g) -> unsigned long long {
-        const unsigned long long x = (unsigned long long)g * WA / (unsigned long long)P;
+        const unsigned long long x = (unsigned long long)((double)g * wa_over_p);
         return x < 1ull ? 1ull : x;
     };
+    auto piece_of = [&](unsigned long long w) -> long long { const long long g = (long long)((double)w * p_over_wa) - 1; return g < 1 ? 1 : g; };
     if (blockIdx.x == 0) {
         // the plan's counts (spamm_b200.h); [16..20] are accumulated below by the blocks of region B
         if (t < 16) {
@@ -1108,7 +1117,10 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArg
         a.tile_off[pidx] = (int32_t)sb;
         sa.node_info[pidx] = ob;                     // tasks before this node (tile_wprefix)
     }
-    if (!valid || nsteps == 0 || overflow) return;
+    if (!valid || nsteps == 0 || overflow) {
+        if (a.trace && lane == 0) atomicMax(a.trace + blockIdx.x * 6 + 5, plan_timer());
+        return;
+    }
     const int ts = (int)sb, te = (int)sb + (int)nsteps;
     // ---- region B: layered segments of this node (lane 0), slots by one atomic per range
     if (pidx >= idxB) {
@@ -1135,9 +1147,8 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArg
     const unsigned long long w0 = ob + RW * (unsigned long long)ts;
     const unsigned long long w1 = w0 + ntasks + RW * (unsigned long long)nsteps;
     bool cuts = false;
-    if (pidx < idxB && P > 1) {
-        long long g0 = (long long)(w0 * (unsigned long long)P / WA);
-        if (g0 < 1) g0 = 1;
+    if (pidx < idxB && P > 1 && !(sa.dbg & 1)) {
+        long long g0 = piece_of(w0);
         while (g0 < P && target_of(g0) <= w0) ++g0;
         cuts = g0 < P && target_of(g0) <= w1;
     }
@@ -1211,8 +1222,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArg
             }
             const unsigned long long hi_w = run + inc, lo_w = hi_w - wr;
             if (writer) {
-                long long g = (long long)(lo_w * (unsigned long long)P / WA);
-                if (g < 1) g = 1;
+                long long g = piece_of(lo_w);
                 while (g < P && target_of(g) <= lo_w) ++g;
                 for (; g < P && target_of(g) <= hi_w; ++g) {
                     const int c = (int)x + 1;                 // the cut: in (ts, te]
@@ -1226,6 +1236,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArg
         }
         sb += __popc(bal & lead_mask);
     }
+    if (a.trace && lane == 0) atomicMax(a.trace + blockIdx.x * 6 + 5, plan_timer());
 }
 
 // ---- host side ---------------------------------------------------------------------------------
@@ -1433,6 +1444,20 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     // (SPAMM_TAIL_RECORDS = -1: decide by the size of the plan; 0: never; n: always, n records per short segment)
     static const int tail_records = plan_env("SPAMM_TAIL_RECORDS", -1, -1, 64);
     static const int tail_percent = plan_env("SPAMM_TAIL_PERCENT", 25, 0, 100);
+    auto dump_trace = [&]() {          // tuning aid (SPAMM_PLAN_TRACE): six time stamps per block
+        if (!t.trace) return;
+        unsigned long long *h = (unsigned long long *)malloc(8 * 6 * tgrid);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, t.trace, 8 * 6 * tgrid, cudaMemcpyDeviceToHost);
+        if (FILE *f = fopen(trace_path, "w")) {
+            for (int x = 0; x < tgrid; ++x)
+                fprintf(f, "%d %llu %llu %llu %llu %llu %llu\n", x, h[6 * x], h[6 * x + 1], h[6 * x + 2], h[6 * x + 3],
+                        h[6 * x + 4], h[6 * x + 5]);
+            fclose(f);
+        }
+        free(h);
+        cudaFree(t.trace);
+    };
     if (small) {
         // count, then emit + cut: two kernels, no look-back, no separate ordering kernel (see plan_count_kernel)
         SmallArgs sa;
@@ -1445,10 +1470,14 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
         sa.num_teams = spamm_execute_piece_base(); sa.piece_records = piece_records; sa.rec_weight = rec_weight;
         sa.tail_records = tail_records;
         sa.tail_percent = tail_percent;
+        static const int small_dbg = plan_env("SPAMM_PLAN_DEBUG", 0, 0, 3);
+        sa.dbg = small_dbg;
+        if (small_dbg & 2) sa.t.sub_a = sa.t.sub_bt = nullptr;
         if (spamm_launch_pdl(plan_count_kernel, dim3(tgrid), dim3(SMALL_WARPS * 32), 0, st, sa) != cudaSuccess) return SPAMM_ECUDA;
         SPAMM_CHECK_LAUNCH();
         if (spamm_launch_pdl(plan_emit_kernel, dim3(tgrid), dim3(SMALL_WARPS * 32), 0, st, sa) != cudaSuccess) return SPAMM_ECUDA;
         SPAMM_CHECK_LAUNCH();
+        dump_trace();
         if (clean_words) {
             *clean_ptr = reinterpret_cast<uint32_t *>(w.shared);
             *clean_words = cgrid != nullptr ? (int)(offsetof(PlanShared, exec_ticket) / 4) : 0;
@@ -1459,19 +1488,7 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
                          dim3(tgrid), dim3(32 * 32), 0, st, t) != cudaSuccess)
         return SPAMM_ECUDA;
     SPAMM_CHECK_LAUNCH();
-    if (t.trace) {
-        unsigned long long *h = (unsigned long long *)malloc(8 * 6 * tgrid);
-        cudaStreamSynchronize(st);
-        cudaMemcpy(h, t.trace, 8 * 6 * tgrid, cudaMemcpyDeviceToHost);
-        if (FILE *f = fopen(trace_path, "w")) {
-            for (int x = 0; x < tgrid; ++x)
-                fprintf(f, "%d %llu %llu %llu %llu %llu %llu\n", x, h[6 * x], h[6 * x + 1], h[6 * x + 2], h[6 * x + 3],
-                        h[6 * x + 4], h[6 * x + 5]);
-            fclose(f);
-        }
-        free(h);
-        cudaFree(t.trace);
-    }
+    dump_trace();
     OrderArgs oa;
     oa.defer_clean = (cgrid != nullptr && clean_words) ? 1 : 0;
     if (clean_words) {

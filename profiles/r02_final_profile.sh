@@ -21,7 +21,7 @@ cap r02_ncu_k3_cfg2_coarse16 execute_kernel python profiles/k3_probe.py cfg2 1e-
 cap r02_ncu_k3_cfg3_fine4 execute_kernel python profiles/k3_probe.py cfg3 1e-8 fine4
 cap r02_ncu_k3_cfg5_fine4 execute_kernel python profiles/k3_probe.py cfg5 1e-8 fine4
 cap r02_ncu_k3_cfg5_coarse16 execute_kernel python profiles/k3_probe.py cfg5 1e-8 coarse16
-cap r02_ncu_plan_tiles plan_tiles_kernel python profiles/stage_probe.py cfg2
-cap r02_ncu_plan_order plan_order_kernel python profiles/stage_probe.py cfg2
+cap r02_ncu_plan_count plan_count_kernel python profiles/stage_probe.py cfg2
+cap r02_ncu_plan_emit plan_emit_kernel python profiles/stage_probe.py cfg2
 rm -f $O/r02_ncu_k3_cfg5_*.ncu-rep      # large; the summaries stay
 ls -la $O
