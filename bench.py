@@ -462,8 +462,8 @@ def run_single(args, torch, P, local: int) -> None:
         ta = P.QuadtreeMatrix.from_dense(host_a)
         return ta, (ta if b_d is None else P.QuadtreeMatrix.from_dense(host_b))
 
-    e2e_ms, d2h = e2e_time(make_packed)
     e2e_dense_ms, _ = e2e_time(make_dense)
+    e2e_ms, d2h = e2e_time(make_packed)
     h2d = sum(int(t.numel()) * t.element_size() for t in pk_a) * (1 if b_d is None else 2)
     h2d_dense = a_d.nbytes * (1 if b_d is None else 2)
 

@@ -703,11 +703,13 @@ __global__ void __launch_bounds__(256) plan_order_kernel(OrderArgs a)
     const int n_tiles = counts[2] ? 0 : counts[1];
     auto wnode = [&](int i) -> unsigned long long { return a.tile_wprefix[i] + RW * (unsigned long long)tile_off[i]; };
     int idxB = n_nodes;
-    // room in the plan: half of the unit slots for region A, the rest for up to three units per node of B
-    const int max_b_nodes = (int)(a.unit_capacity / 10 < ORDER_MAX_B_NODES ? a.unit_capacity / 10 : ORDER_MAX_B_NODES);
     // measured (B200): with a piece of several tiles per team the static split alone finishes within a few
     // per cent; the layered tail is worth its hand-overs only when a team's share is shorter than a tile
     const int tail_records = a.tail_records >= 0 ? a.tail_records : (R < 3ll * a.num_teams ? 3 : 0);
+    // room in the plan: region B (only plans that use it) may take all unit slots but one round of pieces,
+    // five slots per node
+    const int64_t b_room = tail_records > 0 ? (a.unit_capacity - a.num_teams) / 5 : 0;
+    const int max_b_nodes = (int)(b_room < 0 ? 0 : (b_room < ORDER_MAX_B_NODES ? b_room : ORDER_MAX_B_NODES));
     if (tail_records > 0 && n_tiles > 0 && R > 0 && max_b_nodes > 0) {
         // (64-bit products: a plan's weight stays far below 2^48 -- at most 2^31 records of at most 96 -- and
         // the factors here below 2^15)
@@ -1043,8 +1045,10 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArg
     auto wblock = [&](int i) -> unsigned long long { return (s_b[i] & 0xFFFFFFFFull) + RW * (s_a[i] & 0xFFFFFFFFull); };
     // ---- region B (plan_order_kernel's rule, at block granularity): where it begins
     int bB = ntiles;
-    const int max_b_nodes = (int)(sa.unit_capacity / 10 < ORDER_MAX_B_NODES ? sa.unit_capacity / 10 : ORDER_MAX_B_NODES);
     const int tail_records = sa.tail_records >= 0 ? sa.tail_records : (R < 3ll * sa.num_teams ? 3 : 0);
+    // room in the plan: region B (only plans that use it) may take all unit slots but one round of pieces
+    const int64_t b_room = tail_records > 0 ? (sa.unit_capacity - sa.num_teams) / 5 : 0;
+    const int max_b_nodes = (int)(b_room < 0 ? 0 : (b_room < ORDER_MAX_B_NODES ? b_room : ORDER_MAX_B_NODES));
     if (tail_records > 0 && n_tiles > 0 && R > 0 && max_b_nodes >= SMALL_WARPS && !overflow) {
         unsigned long long wB = W * (unsigned long long)sa.tail_percent / 100ull;
         const unsigned long long wmin = W * (unsigned long long)(sa.num_teams + sa.num_teams / 4) / (unsigned long long)n_tiles;
