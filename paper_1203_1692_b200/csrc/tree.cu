@@ -239,8 +239,10 @@ __device__ __forceinline__ void interior_fold(const double *__restrict__ child_s
 #pragma unroll
             for (int qd = 0; qd < 4; ++qd) {
                 const int64_t ci = 2 * pi + (qd >> 1), cj = 2 * pj + (qd & 1);
-                const bool pr = norm[off_c + ci * Sc + cj] >= 0.0f;
-                acc.add(pr, pr ? child_sq[ci * Sc + cj] : 0.0);
+                // both loads in flight together (the square sum of an absent child is simply not used)
+                const float nv = norm[off_c + ci * Sc + cj];
+                const double sv = child_sq[ci * Sc + cj];
+                acc.add(nv >= 0.0f, sv);
             }
             present = acc.seen > 0;
             sq = present ? acc.total() : 0.0;
