@@ -692,6 +692,13 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
     a_local = mine_tree
     b_have = parallel.tree_from_shard(m, n, parallel.allgather_shards(mine), transposed=False)
     local_ms, _ = timed(lambda: multiply_async(a_local, b_have, cfg, None), max(2, min(args.steps, 10)), 3)
+    # the dominant kernel on this rank's rows, alone (as at N = 1): rank 0's figure goes into the line
+    c_r, plan_r, k_r = multiply_async(a_local, b_have, cfg, None, row_range=(r0, r1))
+    torch.cuda.synchronize()
+    k3_ms = kernel_time_execute(P, torch, plan_r, a_local, b_have, cfg, max(3, min(args.steps, 10)), flush)
+    k3_flops = 128.0 * k_r.products4 if cfg.granularity == "fine4" else 8192.0 * len(plan_r)
+    pk = peaks()
+    fp32_peak = 2 * 128 * torch.cuda.get_device_properties(local).multi_processor_count * pk["sm_max_mhz"] * 1e6 / 1e12
     d2h = host_out.get("bytes", 0)
     io = torch.tensor([float(host_rows.numel() * 4), float(d2h)], dtype=torch.float64, device="cuda")
     dist.all_reduce(io)
@@ -713,12 +720,17 @@ def run_sharded(args, torch, dist, P, local: int) -> None:
                                             "note": "B already replicated, trees prebuilt: the local multiply alone"},
                        "tasks_per_rank": [int(w[1]) for w in per_rank],
                        "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write)"},
-            "roofline": None, "cpu_baseline": None,
+            "roofline": {"bound": "fp32", "kernel": "execute_kernel on rank 0's rows, timed alone", "achieved": k3_flops / (k3_ms * 1e-3) / 1e12,
+                         "peak": fp32_peak, "unit": "TFLOP/s", "frac": k3_flops / (k3_ms * 1e-3) / 1e12 / fp32_peak,
+                         "peak_source": f"2*128 lanes*SMs*{pk['sm_max_mhz']:.0f} MHz ({pk['source']} max clock); MEASURED_PEAKS.json has no FP32 FMA figure",
+                         "kernel_ms": k3_ms, "traffic": None},
+            "cpu_baseline": None,        # rank 0 at N = 1 only (bench contract)
             "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": int(io[0].item()), "d2h_bytes_per_step": int(io[1].item())},
             "gpu_launches": int(launches), "clocks": clocks.summary(),
         }
-        print(json.dumps(line))
+        return line
+    return None
 
 
 def run_own(args) -> None:
@@ -740,13 +752,26 @@ def run_own(args) -> None:
         if not dist.is_initialized():
             if "MASTER_ADDR" not in os.environ:
                 os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": "29531", "RANK": "0", "WORLD_SIZE": "1"})
-            if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-                os.environ["NCCL_DEBUG"] = "WARN"       # the version banner goes to stdout; the line below must be the only one
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            # NCCL writes its log (at least the version banner) to stdout; the JSON line must be the only one there
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        # ... and whatever else a library prints while the ranks run: file descriptor 1 points at stderr until the
+        # line itself is written
+        sys.stdout.flush()
+        real_stdout = os.dup(1)
+        os.dup2(2, 1)
+        line = None
         try:
-            run_sharded(args, torch, dist, P, local)
+            if not dist.is_initialized():
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            line = run_sharded(args, torch, dist, P, local)
         finally:
-            dist.destroy_process_group()
+            if dist.is_initialized():
+                dist.destroy_process_group()
+            sys.stdout.flush()
+            os.dup2(real_stdout, 1)
+            os.close(real_stdout)
+        if line is not None:
+            print(json.dumps(line))
     else:
         run_single(args, torch, P, local)
 
