@@ -1403,8 +1403,11 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     t.slot_bt = b->slot_t;
     t.sub_a = (a->sub && b->sub_t) ? a->sub : nullptr;
     t.sub_bt = (a->sub && b->sub_t) ? b->sub_t : nullptr;
-    (void)fine_weight;       // the pieces are balanced by live tasks whatever the gating (the layered tail absorbs the rest)
+    // the pieces are balanced by live tasks whatever the gating; a product that is known to run with coarse16
+    // gating (spamm_multiply) skips the classification of its tasks -- a plan without it is still valid for
+    // fine4, every task is then gated by the numeric kernel itself
     t.fine_weight = 0;
+    if (!fine_weight) t.sub_a = t.sub_bt = nullptr;
     t.L = 1 << depth;
     t.sub = 1 << (depth - tl);
     t.row0 = row0; t.row1 = row1; t.tau = tau;
