@@ -268,3 +268,22 @@ def test_c_abi_allgather_with_a_raw_nccl_communicator():
     finally:
         nccl.ncclCommDestroy.argtypes = [C.c_void_p]
         nccl.ncclCommDestroy(comm)
+
+
+def test_sharded_multiply_on_two_gpus():
+    """ShardedMultiply and multiply_sharded under torchrun with one rank per GPU (NCCL over NVLink): every rank's
+    rows of C equal the single-GPU product bit for bit, for both exchanges, with and without the overlap of the
+    interior rows.  Skipped on a single-GPU box (the CPU suite runs the same logic with gloo, world size 2)."""
+    import os
+    import subprocess
+    import sys
+    ngpu = torch.cuda.device_count()
+    if ngpu < 2:
+        pytest.skip("needs at least 2 GPUs")
+    world = 2 if ngpu < 4 else 4
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+           "--master-port", "29541", os.path.join(root, "tests", "sharded_child.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-4000:]
+    assert f"SHARDED OK {world}" in out.stdout
