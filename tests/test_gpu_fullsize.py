@@ -74,6 +74,27 @@ def test_config2_work_is_monotone_in_tau():
     assert tasks == sorted(tasks, reverse=True) and p4 == sorted(p4, reverse=True)
     assert tasks[-1] == 0 and p4[0] == 64 * tasks[0]
 
+@pytest.mark.parametrize("gran", ["fine4", "coarse16"])
+def test_config1_full_size_matches_oracle(gran):
+    """BASELINE config 1 (n = 1024, tau = 1e-6: the reference's own CPU-runnable case) against the oracle at full
+    size: task set, executed micro products, every C value and every norm tier, bit for bit (EXACT mode);
+    FMA mode within the tolerance.  Its plan is the one small enough to be handed out as layered segments only."""
+    import paper_1203_1692_b200 as P
+    a, _ = inputs.make_operands("cfg1")
+    tau = 1e-6
+    oa = O.tree_from_dense(a)
+    qa = _device_tree(P, a)
+    oc, oplan, ok = O.multiply(oa, oa, tau, gran)
+    for rep in range(3):                       # first call: plan + execute; then the fused multiply, twice
+        c, plan, k = P.multiply(qa, qa, P.MultiplyConfig(tau=tau, granularity=gran, exact=True))
+        assert len(plan) == len(oplan) and k.products4 == ok.products4
+        assert np.array_equal(c.to_dense().data, oc.to_dense()), f"repetition {rep}"
+        for t in range(oc.depth + 1):
+            assert np.array_equal(c.level_norms(t), oc.level_norm(t)), f"C norms, tier {t}"
+    c2, _, _ = P.multiply(qa, qa, P.MultiplyConfig(tau=tau, granularity=gran))
+    ref = oc.to_dense()
+    assert np.abs(c2.to_dense().data.astype(np.float64) - ref).max() <= REL_TOL * np.abs(ref).max()
+
 
 def test_config3_full_size_matches_oracle():
     import paper_1203_1692_b200 as P
@@ -105,7 +126,7 @@ def test_config4_full_size_counts_and_slabs(tau):
     masks = O.task_masks(oa, oa, oplan, tau)
     want_p4 = int(np.bitwise_count(masks).sum()) if hasattr(np, "bitwise_count") else int(sum(bin(int(m)).count("1") for m in masks))
     assert k.products4 == want_p4 and k.skipped4 == 64 * len(oplan) - want_p4
-    _slab_rows_match(P, c, oa, oa, oplan, tau, "fine4", [(0, 2), (233, 235), (467, 469)])
+    _slab_rows_match(P, c, oa, oa, oplan, tau, "fine4", [(0, 2), (100, 101), (233, 235), (350, 351), (467, 469)])
     d = c.to_dense().data
     assert np.array_equal(d, d.T)
 
@@ -127,7 +148,7 @@ def test_config5_full_size_counts_and_slabs():
     keys, vals, _ = c.packed_leaves()
     from paper_1203_1692_b200 import morton
     ci, cj = morton.decode_array(keys)
-    for r0, r1 in ((0, 1), (1000, 1001), (2047, 2048)):
+    for r0, r1 in ((0, 1), (3, 4), (511, 513), (1000, 1001), (1536, 1537), (2047, 2048)):
         sel = (oplan.ti >= r0) & (oplan.ti < r1)
         sub = O.OraclePlan(oplan.ti[sel], oplan.tk[sel], oplan.tj[sel], oplan.norm_product[sel], tau)
         oc, _ = O.execute_plan(sub, oa, oa, None, tau)
