@@ -14,7 +14,8 @@ qb = qa if b is None else P.QuadtreeMatrix.from_dense(b)
 cfg = P.MultiplyConfig(tau=tau)
 P.build_plan(qa, qb, tau)            # records the capacity hint without running the pipeline
 flush = torch.empty((256 << 20,), dtype=torch.uint8, device="cuda")
-for label, fl in (("back to back", False), ("L2 flushed", True)):
+modes = (("back to back", False),) if os.environ.get("PROBE_ONLY_WARM") else (("back to back", False), ("L2 flushed", True))
+for label, fl in modes:
     ts = []
     for it in range(30):
         if fl:
