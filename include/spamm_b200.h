@@ -288,9 +288,12 @@ typedef struct {
  * executed micro products (ExecCounters.products4) is left in counts[8..9] (set afresh by every call).  The caller
  * reads plan->counts when it next synchronises; counts[2] != 0 means a capacity was too small
  * (nothing was computed) and the call must be repeated with larger buffers.
- * plan_ws (spamm_plan_workspace_bytes() bytes) must be ALL ZERO when the call is enqueued and is
- * all zero again once the multiply has run: clear it once after allocating it, then reuse it for
- * every multiply on the same stream -- the four kernels of a multiply run without any memset. */
+ * plan_ws (spamm_plan_workspace_bytes() bytes) must be ALL ZERO when it is first used: clear it once
+ * after allocating it, then reuse it for every multiply on the same stream (one workspace per
+ * stream).  The planner keeps the prefix it relies on zero from one multiply to the next, so the
+ * four kernels of a multiply run without any memset; only when the capacities GROW between two
+ * multiplies on the same workspace does the call clear the part of the longer prefix that was
+ * scratch before (one small stream-ordered memset). */
 int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
                    int exact, float alpha, int32_t row0, int32_t row1,
                    const spamm_plan_buffers *plan, void *plan_ws, size_t plan_ws_bytes,

@@ -5,12 +5,16 @@
 // plan.counts[2] for the caller to check whenever it first synchronises.
 #include <stdlib.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 
 int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int32_t row0, int32_t row1,
                     const spamm_plan_buffers *out, void *ws, size_t ws_bytes, bool prezeroed,
                     const spamm_product_buffers *cgrid, uint32_t **clean_ptr, int *clean_words, int fine_weight,
                     void *stream);
+size_t spamm_plan_zero_bytes(int64_t step_capacity, int64_t leaf_capacity);
 int spamm_launch_interior(const double *leaf_sq, int depth, float *norm, float *norm_t, double *sq_levels,
                           unsigned int *ticket, cudaStream_t st);
 int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const spamm_plan_buffers *plan,
@@ -28,6 +32,21 @@ extern "C" int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b
     // Four kernels, no memset: plan count (which also empties C's leaf grids), plan emit (records, pieces,
     // counts), execute, interior norms; deep trees: root / expand / tiles / order in place of the first two.
     if (!plan_ws) return SPAMM_EWORKSPACE;
+    // The planner needs a prefix of its workspace zero and leaves it zero; behind the prefix lie scratch lists.
+    // How long the prefix is depends on the capacities: when they grow from one multiply to the next on the
+    // same workspace, the part of the new prefix that was scratch before is cleared here (stream-ordered).
+    {
+        static std::mutex mu;
+        static std::unordered_map<const void *, size_t> prefix;      // workspace -> zero prefix of its last multiply
+        const size_t zb = spamm_plan_zero_bytes(plan->step_capacity, plan->leaf_capacity);
+        if (zb > plan_ws_bytes) return SPAMM_EWORKSPACE;
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = prefix.find(plan_ws);
+        if (it != prefix.end() && zb > it->second &&
+            cudaMemsetAsync(static_cast<char *>(plan_ws) + it->second, 0, zb - it->second, st) != cudaSuccess)
+            return SPAMM_ECUDA;
+        prefix[plan_ws] = zb;
+    }
     static const int stop = getenv("SPAMM_PIPE_STOP") ? atoi(getenv("SPAMM_PIPE_STOP")) : 0;   // tuning aid: truncate
     uint32_t *clean_ptr = nullptr;      // planner state the numeric kernel returns to zero
     int clean_words = 0;

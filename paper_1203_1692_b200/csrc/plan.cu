@@ -884,6 +884,11 @@ struct SmallArgs {
     unsigned long long *node_info;   // per node, between the kernels: records | present << 8 | tasks << 24 (= tile_wprefix)
     unsigned long long *agg_a;       // per block: records | product leaves << 32
     unsigned long long *agg_b;       // per block: tasks | super-tiles with records << 32
+    // grids of more than 512 blocks (n = 8192): the same sums per group of `group` consecutive blocks, made by
+    // the last block of a group to finish (tickets: zero between launches); plan_emit_kernel sums the groups
+    int group;
+    unsigned long long *grp_a, *grp_b;
+    unsigned int *grp_ticket;
     int32_t *units;
     int64_t unit_capacity;
     int num_teams, piece_records, rec_weight, tail_records, tail_percent;
@@ -976,6 +981,19 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_count_kernel(SmallAr
         for (int w = 0; w < SMALL_WARPS; ++w) { st += s_steps[w]; lv += s_leaves[w]; tk += s_tasks[w]; ne += s_steps[w] ? 1u : 0u; }
         sa.agg_a[blockIdx.x] = st | (lv << 32);
         sa.agg_b[blockIdx.x] = tk | (ne << 32);
+        if (sa.group > 1) {
+            const int g = (int)blockIdx.x / sa.group, first = g * sa.group;
+            const int members = min(sa.group, (int)gridDim.x - first);
+            __threadfence();
+            if (atomicAdd(sa.grp_ticket + g, 1u) == (unsigned int)(members - 1)) {
+                __threadfence();
+                unsigned long long ga = 0, gb = 0;
+                for (int j = 0; j < members; ++j) { ga += __ldcg(sa.agg_a + first + j); gb += __ldcg(sa.agg_b + first + j); }
+                sa.grp_a[g] = ga;
+                sa.grp_b[g] = gb;
+                sa.grp_ticket[g] = 0u;
+            }
+        }
         if (a.trace) a.trace[blockIdx.x * 6 + 1] = plan_timer();
     }
 }
@@ -990,7 +1008,9 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArg
     const int warp = threadIdx.x >> 5, t = threadIdx.x;
     const uint32_t lane = lane_id();
     const int n_nodes = a.St * a.St;
-    const int ntiles = (int)gridDim.x;
+    // the prefix sums below run over the blocks themselves, or over groups of blocks when there are more than 512
+    const int gsz = sa.group, ntiles = ((int)gridDim.x + gsz - 1) / gsz;
+    const unsigned long long *agg_a = gsz > 1 ? sa.grp_a : sa.agg_a, *agg_b = gsz > 1 ? sa.grp_b : sa.agg_b;
     const int sub = a.sub, per = 32 / sub;
     const uint32_t kk = lane % sub, grp = (lane / sub) * sub;
     const int pidx = (int)blockIdx.x * SMALL_WARPS + warp;
@@ -1015,8 +1035,8 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArg
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
             const int i = 2 * t + x;
-            va[x] = i < ntiles ? __ldcg(sa.agg_a + i) : 0ull;
-            vb[x] = i < ntiles ? __ldcg(sa.agg_b + i) : 0ull;
+            va[x] = i < ntiles ? __ldcg(agg_a + i) : 0ull;
+            vb[x] = i < ntiles ? __ldcg(agg_b + i) : 0ull;
         }
         unsigned long long ia = va[0] + va[1], ib = vb[0] + vb[1];       // inclusive scan of the pair sums
 #pragma unroll
@@ -1045,7 +1065,8 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArg
     auto wblock = [&](int i) -> unsigned long long { return (s_b[i] & 0xFFFFFFFFull) + RW * (s_a[i] & 0xFFFFFFFFull); };
     // ---- region B (plan_order_kernel's rule, at block granularity): where it begins
     int bB = ntiles;
-    const int tail_records = sa.tail_records >= 0 ? sa.tail_records : (R < 3ll * sa.num_teams ? 3 : 0);
+    // (a grid in groups is a large product: no layered tail there)
+    const int tail_records = gsz > 1 ? 0 : (sa.tail_records >= 0 ? sa.tail_records : (R < 3ll * sa.num_teams ? 3 : 0));
     // room in the plan: region B (only plans that use it) may take all unit slots but one round of pieces
     const int64_t b_room = tail_records > 0 ? (sa.unit_capacity - sa.num_teams) / 5 : 0;
     const int max_b_nodes = (int)(b_room < 0 ? 0 : (b_room < ORDER_MAX_B_NODES ? b_room : ORDER_MAX_B_NODES));
@@ -1113,7 +1134,11 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 4) plan_emit_kernel(SmallArg
     const uint32_t ntasks = (uint32_t)(info >> 24), nleaves = __popc(present);
     if (lane == 0) { s_wa[warp] = nsteps | ((unsigned long long)nleaves << 32); s_wb[warp] = ntasks; }
     __syncthreads();
-    unsigned long long oa = s_a[blockIdx.x], ob = s_b[blockIdx.x] & 0xFFFFFFFFull;
+    unsigned long long oa = s_a[blockIdx.x / gsz], ob = s_b[blockIdx.x / gsz] & 0xFFFFFFFFull;
+    for (int j = (int)(blockIdx.x / gsz) * gsz; j < (int)blockIdx.x; ++j) {        // the blocks of my group before me
+        oa += __ldcg(sa.agg_a + j);
+        ob += __ldcg(sa.agg_b + j) & 0xFFFFFFFFull;
+    }
     for (int w = 0; w < warp; ++w) { oa += s_wa[w]; ob += s_wb[w]; }
     int64_t sb = (int64_t)(oa & 0xFFFFFFFFull);
     const int64_t cb = (int64_t)(oa >> 32);
@@ -1391,7 +1416,7 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
     // a small dense start (n <= 4096): blocks of 8 nodes, count + emit kernels; else two 1024-thread blocks
     // per SM that draw tiles of 32 nodes from a counter
     static const bool small_off = getenv("SPAMM_PLAN_SMALL") && atoi(getenv("SPAMM_PLAN_SMALL")) == 0;    // tuning aid
-    const bool small = dense && tl <= 6 && !small_off;
+    const bool small = dense && !small_off;      // dense: tl <= PLAN_DENSE_MAX_LEVEL = 7, at most 2048 blocks of 8 nodes
     const int tgrid = small ? ((1 << (2 * tl)) + SMALL_WARPS - 1) / SMALL_WARPS : (dense && tl <= 6) ? SPAMM_NUM_SMS : SPAMM_NUM_SMS * 2;
     if (trace_path && cudaMalloc(&t.trace, 8 * 6 * tgrid) == cudaSuccess) cudaMemsetAsync(t.trace, 0, 8 * 6 * tgrid, st);
     t.norm_a_t = a->norm + spamm_level_offset(tl);
@@ -1472,6 +1497,11 @@ int spamm_plan_impl(const spamm_tree_view *a, const spamm_tree_view *b, double t
         sa.node_info = w.tile_wprefix;
         sa.agg_a = reinterpret_cast<unsigned long long *>(w.buf[0].node);      // level lists: unused by a dense start
         sa.agg_b = reinterpret_cast<unsigned long long *>(w.buf[1].node);
+        sa.group = tgrid > SMALL_MAX_TILES ? (tgrid + SMALL_MAX_TILES - 1) / SMALL_MAX_TILES : 1;
+        sa.grp_a = sa.agg_a + tgrid;
+        sa.grp_b = sa.agg_b + tgrid;
+        // tickets in the part of the workspace that is zero between plans (a look-back array of the other path)
+        sa.grp_ticket = reinterpret_cast<unsigned int *>(w.tile_state[PLAN_MAX_LEVELS]);
         sa.units = out->tile_order;
         sa.unit_capacity = spamm_unit_capacity(out->leaf_capacity);
         sa.num_teams = spamm_execute_piece_base(); sa.piece_records = piece_records; sa.rec_weight = rec_weight;
