@@ -436,14 +436,13 @@ def run_single(args, torch, P, local: int) -> None:
     host_a = torch.from_numpy(a_d).pin_memory()
     host_b = host_a if b_d is None else torch.from_numpy(b_d).pin_memory()
 
-    def e2e_time(make):
+    def e2e_time(step):
         times, d2h_bytes = [], 0
         for it in range(2 + max(3, min(args.steps, 20) // 2)):
             flush.fill_(it)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            ta, tb = make()
-            cc, _, _ = P.multiply(ta, tb, cfg)
+            cc = step()
             nc = cc.nleaf                       # reads the counts back (the one synchronisation of the step)
             host_vals[:nc].copy_(cc.values[:nc], non_blocking=True)
             host_keys[:nc].copy_(cc.keys[:nc], non_blocking=True)
@@ -454,16 +453,32 @@ def run_single(args, torch, P, local: int) -> None:
                 times.append(e0.elapsed_time(e1))
         return float(np.mean(times)), d2h_bytes
 
-    def make_packed():
+    def step_packed():
         ta = P.QuadtreeMatrix.from_packed(n, n, pk_a[0], pk_a[1])
-        return ta, (ta if b_d is None else P.QuadtreeMatrix.from_packed(n, n, pk_b[0], pk_b[1]))
+        tb = ta if b_d is None else P.QuadtreeMatrix.from_packed(n, n, pk_b[0], pk_b[1])
+        return P.multiply(ta, tb, cfg)[0]
 
-    def make_dense():
+    def step_dense():
         ta = P.QuadtreeMatrix.from_dense(host_a)
-        return ta, (ta if b_d is None else P.QuadtreeMatrix.from_dense(host_b))
+        tb = ta if b_d is None else P.QuadtreeMatrix.from_dense(host_b)
+        return P.multiply(ta, tb, cfg)[0]
 
-    e2e_dense_ms, _ = e2e_time(make_dense)
-    e2e_ms, d2h = e2e_time(make_packed)
+    # operands that stay on the host (paper_1203_1692_b200.hosttree): keys, norms and sub-block norms go up, the
+    # plan is made, and the GPU fetches only the leaves that occur in a surviving task from pinned host memory
+    h_a = P.HostTree.from_device(qa)
+    h_b = None if b_d is None else P.HostTree.from_device(qb)
+    fetched_box = {}
+
+    def step_host():
+        cc, _, _, fetched = P.multiply_host(h_a, h_b, cfg)
+        fetched_box["n"] = fetched
+        return cc
+
+    e2e_dense_ms, _ = e2e_time(step_dense)
+    e2e_packed_ms, _ = e2e_time(step_packed)
+    e2e_ms, d2h = e2e_time(step_host)
+    fetched_leaves = int(fetched_box["n"].sum().item())
+    h2d_host = h_a.skeleton_bytes() + (0 if h_b is None else h_b.skeleton_bytes()) + fetched_leaves * 1024
     h2d = sum(int(t.numel()) * t.element_size() for t in pk_a) * (1 if b_d is None else 2)
     h2d_dense = a_d.nbytes * (1 if b_d is None else 2)
 
@@ -558,9 +573,14 @@ def run_single(args, torch, P, local: int) -> None:
                         "frac": k4_bytes / (k4_ms * 1e-3) / 1e9 / pk["hbm_gbs"], "ms": k4_ms, "algorithmic_bytes": int(k4_bytes)},
         "cpu_baseline": cpu,
         "e2e": {"value": flops / (e2e_ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "operands": "host trees as packed leaves (keys + 16x16 blocks, pinned), QuadtreeMatrix.from_packed",
+                "h2d_bytes_per_step": int(h2d_host), "d2h_bytes_per_step": int(d2h),
+                "operands": "host trees (HostTree: the arrays of packed_leaves() + leaf norms, pinned); multiply_host sends keys and "
+                            "norms, plans, and the GPU fetches the leaves that occur in a task from host memory",
+                "operand_leaves_fetched": fetched_leaves,
                 "result": "product tree as packed leaves (keys + leaf records)",
+                "all_leaves": {"value": flops / (e2e_packed_ms * 1e-3) / 1e9, "ms_per_step": e2e_packed_ms,
+                               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                               "operands": "every stored leaf uploaded first (keys + 16x16 blocks, pinned), QuadtreeMatrix.from_packed"},
                 "from_dense": {"value": flops / (e2e_dense_ms * 1e-3) / 1e9, "ms_per_step": e2e_dense_ms,
                                "h2d_bytes_per_step": int(h2d_dense), "d2h_bytes_per_step": int(d2h),
                                "operands": "dense host matrix (pinned), QuadtreeMatrix.from_dense"}},

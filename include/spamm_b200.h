@@ -265,6 +265,29 @@ int spamm_union_leaves(const int32_t *slot_old, const uint32_t *prod_keys, int64
                        int32_t *slot_prod_scratch, uint32_t *out_keys, int32_t *idx_old,
                        int32_t *idx_prod, int32_t *nout_dev, void *ws, size_t ws_bytes, void *stream);
 
+/* ---- operands whose leaf values stay in host memory ----------------------------------
+ * The reference's trees live on the host (core.py:146-405).  For one product only the leaves that
+ * occur in a surviving task are needed on the device -- 28 % of config 2's at tau = 1e-8.  With the
+ * keys, leaf norms and sub-block norms on the device (a few MB) the symbolic phase runs first; these
+ * three calls then bring in exactly the values the numeric phase will read, fetched by the GPU from
+ * pinned (device-readable) host memory. */
+
+/* Sub-norm tails of the leaf records from the reference's sub-norm array subs [nleaf][4][4]
+ * (core.py:387-405; device pointer): values (tail transposed) and / or values_t (tail row-major). */
+int spamm_subnorm_tails(const float *subs, int64_t nleaf, float *values, float *values_t, void *stream);
+
+/* flags_a[x] = 1 / flags_b[x] = 1 for every packed leaf x of the left / right operand that a live
+ * task of the plan reads.  The arrays (one byte per leaf) must be zero on entry and may be the same
+ * array when both operands are one tree. */
+int spamm_mark_touched(const spamm_plan_buffers *plan, unsigned char *flags_a, unsigned char *flags_b,
+                       void *stream);
+
+/* For every flagged leaf: its row-major 16x16 block blocks[leaf*256 ..] -- pinned host memory the
+ * device can read, or device memory -- into the record of `values` (want & 1) and / or transposed
+ * into that of `values_t` (want & 2).  *copied (optional, device) += leaves fetched. */
+int spamm_gather_blocks(const float *blocks, const unsigned char *flags, int64_t nleaf, int want,
+                        float *values, float *values_t, unsigned long long *copied, void *stream);
+
 /* ---- one call: multiply (numeric.py:302-313), beta == 0 ---------------------------- */
 
 /* Storage of the product tree, sized by the plan's leaf_capacity (packed arrays) and by the

@@ -70,6 +70,9 @@ SIGNATURES = {
     "spamm_build_interior": (C.c_int, [vp, C.c_int, vp, vp, vp, C.c_int, vp]),
     "spamm_leaf_norms_packed": (C.c_int, [vp, i64, vp, vp, vp]),
     "spamm_leaves_from_blocks": (C.c_int, [vp, i64, vp, vp, vp, vp]),
+    "spamm_subnorm_tails": (C.c_int, [vp, i64, vp, vp, vp]),
+    "spamm_mark_touched": (C.c_int, [C.POINTER(PlanBuffers), vp, vp, vp]),
+    "spamm_gather_blocks": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp]),
     "spamm_transpose_records": (C.c_int, [vp, i64, vp, vp]),
     "spamm_sparsify_leaves": (C.c_int, [vp, vp, vp, i64, C.c_float, vp, vp]),
     "spamm_index_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp]),

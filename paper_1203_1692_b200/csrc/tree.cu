@@ -6,6 +6,7 @@
 // oracle/spamm_oracle.c for the probe), so every float32 norm is bit-identical.
 #include "common.cuh"
 #include "scan.cuh"
+#include "plan_format.cuh"
 
 // ---------------------------------------------------------------------------------
 // Sum of squares of a 4x4 sub-block held as four float4 rows (core.py:113-114, :230-232):
@@ -425,6 +426,109 @@ extern "C" int spamm_leaves_from_blocks(const float *blocks, int64_t nleaf, floa
     if (!blocks || !values || !values_t || !leaf_sq || nleaf < 0) return SPAMM_EINVAL;
     leaf_norms_packed_kernel<<<(unsigned)((nleaf + 15) / 16), 256, 0, (cudaStream_t)stream>>>(blocks, values, nleaf,
                                                                                             values_t, leaf_sq);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
+}
+
+// ---- operands that stay on the host: only the leaves a product touches cross PCIe ----------------
+// A tree whose leaf VALUES are still in (pinned, device-readable) host memory: keys, leaf norms and sub-block
+// norms are on the device, so the symbolic phase can run; the numeric phase then needs the values of the
+// leaves that occur in a surviving task and of no others.  (1) the sub-norm tails of the records, from the
+// reference's sub-norm array (core.py:387-405, [leaf][p][q]); (2) which leaves a plan touches; (3) their
+// values, read by the GPU straight from host memory into both record layouts.
+__global__ void __launch_bounds__(256) subnorm_tails_kernel(const float *__restrict__ subs, int64_t nleaf,
+                                                            float *__restrict__ values, float *__restrict__ values_t)
+{
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= nleaf * 16) return;
+    const int64_t leaf = x >> 4;
+    const int p = (int)(x & 15) >> 2, q = (int)x & 3;
+    const float v = subs[x];                                 // sub[p][q]
+    if (values) values[leaf * SPAMM_REC + 256 + q * 4 + p] = v;
+    if (values_t) values_t[leaf * SPAMM_REC + 256 + p * 4 + q] = v;
+}
+
+extern "C" int spamm_subnorm_tails(const float *subs, int64_t nleaf, float *values, float *values_t, void *stream)
+{
+    if (nleaf == 0) return SPAMM_OK;
+    if (!subs || nleaf < 0 || (!values && !values_t)) return SPAMM_EINVAL;
+    subnorm_tails_kernel<<<(unsigned)((nleaf * 16 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(subs, nleaf, values, values_t);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
+}
+
+// flags_a[x] / flags_b[x] = 1 for every packed leaf x of the left / right operand that a live task of the plan
+// reads (the arrays must be zero on entry; they may be the same array when both operands are one tree)
+__global__ void __launch_bounds__(256) mark_touched_kernel(const spamm_step *__restrict__ steps, const int32_t *__restrict__ counts,
+                                                           unsigned char *__restrict__ flags_a, unsigned char *__restrict__ flags_b)
+{
+    const int nsteps = counts[2] ? 0 : counts[4];
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nsteps; s += gridDim.x * blockDim.x) {
+        const spamm_step r = steps[s];
+        uint32_t ta = 0, tb = 0;                             // touched leaves of the A block / the B block (bit morton4)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t live = r.live[kk] & 0xFFFFu;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                if (live & step_rowmask(d)) ta |= 1u << step_pos(d, kk);      // A leaf (di = d, kk)
+                if (live & step_colmask(d)) tb |= 1u << step_pos(kk, d);      // B leaf (kk, dj = d)
+            }
+        }
+        for (uint32_t m = ta & r.a_present; m; m &= m - 1) {
+            const int pos = __ffs(m) - 1;
+            flags_a[(int64_t)r.a_first + __popc(r.a_present & ((1u << pos) - 1u))] = 1;
+        }
+        for (uint32_t m = tb & r.b_present; m; m &= m - 1) {
+            const int pos = __ffs(m) - 1;
+            flags_b[(int64_t)r.b_first + __popc(r.b_present & ((1u << pos) - 1u))] = 1;
+        }
+    }
+}
+
+extern "C" int spamm_mark_touched(const spamm_plan_buffers *plan, unsigned char *flags_a, unsigned char *flags_b, void *stream)
+{
+    if (!plan || !flags_a || !flags_b) return SPAMM_EINVAL;
+    mark_touched_kernel<<<SPAMM_NUM_SMS * 4, 256, 0, (cudaStream_t)stream>>>(plan->steps, plan->counts, flags_a, flags_b);
+    SPAMM_CHECK_LAUNCH();
+    return SPAMM_OK;
+}
+
+// One warp per flagged leaf: its 16x16 block from (device-readable) host memory into the row-major record
+// (want & 1) and / or the transposed one (want & 2); `copied` counts the leaves fetched.
+__global__ void __launch_bounds__(256) gather_blocks_kernel(const float *__restrict__ blocks, const unsigned char *__restrict__ flags,
+                                                            int64_t nleaf, int want, float *__restrict__ values,
+                                                            float *__restrict__ values_t, unsigned long long *copied)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    unsigned long long mine = 0;
+    for (int64_t leaf = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); leaf < nleaf; leaf += warps) {
+        if (!flags[leaf]) continue;
+        ++mine;
+        const float4 *src = reinterpret_cast<const float4 *>(blocks + leaf * 256);
+        const float4 v0 = src[lane], v1 = src[lane + 32];        // elements 4*lane .. and 128 + 4*lane ..
+        if (want & 1) {
+            float4 *dst = reinterpret_cast<float4 *>(values + leaf * SPAMM_REC);
+            dst[lane] = v0;
+            dst[lane + 32] = v1;
+        }
+        if (want & 2) {
+            float *dt = values_t + leaf * SPAMM_REC;
+            const int r0 = lane >> 2, c0 = (lane & 3) * 4;       // v0 = row r0, columns c0..c0+3; v1 = row r0 + 8
+            dt[(c0 + 0) * 16 + r0] = v0.x; dt[(c0 + 1) * 16 + r0] = v0.y; dt[(c0 + 2) * 16 + r0] = v0.z; dt[(c0 + 3) * 16 + r0] = v0.w;
+            dt[(c0 + 0) * 16 + r0 + 8] = v1.x; dt[(c0 + 1) * 16 + r0 + 8] = v1.y; dt[(c0 + 2) * 16 + r0 + 8] = v1.z; dt[(c0 + 3) * 16 + r0 + 8] = v1.w;
+        }
+    }
+    if (copied && lane == 0 && mine) atomicAdd(copied, mine);
+}
+
+extern "C" int spamm_gather_blocks(const float *blocks, const unsigned char *flags, int64_t nleaf, int want, float *values,
+                                   float *values_t, unsigned long long *copied, void *stream)
+{
+    if (nleaf == 0) return SPAMM_OK;
+    if (!blocks || !flags || nleaf < 0 || !(want & 3) || ((want & 1) && !values) || ((want & 2) && !values_t)) return SPAMM_EINVAL;
+    gather_blocks_kernel<<<SPAMM_NUM_SMS * 8, 256, 0, (cudaStream_t)stream>>>(blocks, flags, nleaf, want, values, values_t, copied);
     SPAMM_CHECK_LAUNCH();
     return SPAMM_OK;
 }
