@@ -335,6 +335,33 @@ typedef struct {
 } spamm_arena_layout;
 int spamm_multiply_arena_layout(int depth, int c_depth, int64_t step_capacity, int64_t leaf_capacity,
                                 spamm_arena_layout *out);
+
+/* The one-call multiply for operands whose leaf VALUES are still in host memory (see "operands whose
+ * leaf values stay in host memory" above): between the symbolic and the numeric phase the leaves
+ * the plan reads are marked and their blocks fetched by the GPU -- the left operand's into
+ * a->values_t, the right one's into b->values; one tree as both operands (b_blocks NULL or the same
+ * pointers): into both of its layouts.  a_blocks / b_blocks: [nleaf][256] floats in pinned,
+ * device-readable host memory (or device memory); a_flags / b_flags: [nleaf] bytes of device
+ * scratch; fetched (optional, device): [2] counts of leaves fetched (left, right).  Still no host
+ * synchronisation. */
+typedef struct {
+    const float *a_blocks;
+    int64_t a_nleaf;
+    unsigned char *a_flags;
+    const float *b_blocks;
+    int64_t b_nleaf;
+    unsigned char *b_flags;
+    unsigned long long *fetched;
+} spamm_host_operands;
+int spamm_multiply_host(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
+                        int exact, float alpha, int32_t row0, int32_t row1,
+                        const spamm_plan_buffers *plan, void *plan_ws, size_t plan_ws_bytes,
+                        const spamm_product_buffers *c, const spamm_host_operands *host, void *stream);
+int spamm_multiply_arena_host(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
+                              int exact, float alpha, int32_t row0, int32_t row1, int c_depth,
+                              int64_t step_capacity, int64_t leaf_capacity, void *arena, size_t arena_bytes,
+                              void *plan_ws, size_t plan_ws_bytes, const spamm_host_operands *host,
+                              void *stream);
 int spamm_multiply_arena(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
                          int exact, float alpha, int32_t row0, int32_t row1, int c_depth,
                          int64_t step_capacity, int64_t leaf_capacity, void *arena, size_t arena_bytes,

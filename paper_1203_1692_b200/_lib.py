@@ -51,6 +51,13 @@ class ArenaLayout(C.Structure):
                                    "sq_levels", "total")]
 
 
+class HostOperands(C.Structure):
+    """``spamm_host_operands``: leaf blocks in pinned host memory, flag scratch on the device."""
+
+    _fields_ = [("a_blocks", vp), ("a_nleaf", i64), ("a_flags", vp), ("b_blocks", vp), ("b_nleaf", i64), ("b_flags", vp),
+                ("fetched", vp)]
+
+
 REC = 272           # floats per stored leaf record: 256 values + 16 sub-block norms
 STEP_WORDS = 16     # uint32 words per step record (struct spamm_step)
 PLAN_COUNTS = 32
@@ -91,6 +98,10 @@ SIGNATURES = {
     "spamm_multiply_arena_layout": (C.c_int, [C.c_int, C.c_int, i64, i64, C.POINTER(ArenaLayout)]),
     "spamm_multiply_arena": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, C.c_int, C.c_int, f32, i32, i32,
                                        C.c_int, i64, i64, vp, sz, vp, sz, vp]),
+    "spamm_multiply_host": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, C.c_int, C.c_int, f32, i32, i32,
+                                      C.POINTER(PlanBuffers), vp, sz, C.POINTER(ProductBuffers), C.POINTER(HostOperands), vp]),
+    "spamm_multiply_arena_host": (C.c_int, [C.POINTER(TreeView), C.POINTER(TreeView), f64, C.c_int, C.c_int, f32, i32, i32,
+                                            C.c_int, i64, i64, vp, sz, vp, sz, C.POINTER(HostOperands), vp]),
     "spamm_exchange_allgather": (C.c_int, [vp, vp, vp, vp, i64, vp, vp, vp, vp]),
     "spamm_union_leaves": (C.c_int, [vp, vp, i64, C.c_int, vp, vp, vp, vp, vp, vp, sz, vp]),
     "spamm_compose": (C.c_int, [vp, vp, vp, vp, i64, f32, f32, C.c_int, C.c_int, vp, vp]),

@@ -23,9 +23,9 @@ int spamm_execute_impl(const spamm_tree_view *a, const spamm_tree_view *b, const
                        const spamm_product_buffers *cgrid, uint32_t *clean_ptr, int clean_words, void *stream,
                        unsigned long long *gates = nullptr);
 
-extern "C" int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity, int exact,
-                              float alpha, int32_t row0, int32_t row1, const spamm_plan_buffers *plan, void *plan_ws,
-                              size_t plan_ws_bytes, const spamm_product_buffers *c, void *stream)
+static int multiply_impl(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity, int exact,
+                         float alpha, int32_t row0, int32_t row1, const spamm_plan_buffers *plan, void *plan_ws,
+                         size_t plan_ws_bytes, const spamm_product_buffers *c, const spamm_host_operands *host, void *stream)
 {
     if (!a || !b || !plan || !c) return SPAMM_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
@@ -53,6 +53,29 @@ extern "C" int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b
     int rc = spamm_plan_impl(a, b, tau, row0, row1, plan, plan_ws, plan_ws_bytes, true, c, stop == 2 ? nullptr : &clean_ptr,
                              stop == 2 ? nullptr : &clean_words, granularity == SPAMM_FINE4 ? 1 : 0, stream);
     if (rc != SPAMM_OK || stop == 2) return rc;
+    if (host) {
+        // operands whose leaf values are still in host memory: mark the leaves the plan reads and let the GPU
+        // fetch their blocks (the left operand is read through values_t, the right one through values)
+        const bool same = host->b_blocks == nullptr || (host->b_blocks == host->a_blocks && host->b_flags == host->a_flags);
+        if (!host->a_blocks || !host->a_flags || (!same && !host->b_flags)) return SPAMM_EINVAL;
+        unsigned char *fb = same ? host->a_flags : host->b_flags;
+        if (cudaMemsetAsync(host->a_flags, 0, (size_t)host->a_nleaf, st) != cudaSuccess) return SPAMM_ECUDA;
+        if (!same && cudaMemsetAsync(fb, 0, (size_t)host->b_nleaf, st) != cudaSuccess) return SPAMM_ECUDA;
+        if (host->fetched && cudaMemsetAsync(host->fetched, 0, 16, st) != cudaSuccess) return SPAMM_ECUDA;
+        rc = spamm_mark_touched(plan, host->a_flags, fb, stream);
+        if (rc != SPAMM_OK) return rc;
+        if (same) {
+            rc = spamm_gather_blocks(host->a_blocks, host->a_flags, host->a_nleaf, 3, const_cast<float *>(a->values),
+                                     const_cast<float *>(a->values_t), host->fetched, stream);
+        } else {
+            rc = spamm_gather_blocks(host->a_blocks, host->a_flags, host->a_nleaf, 2, nullptr, const_cast<float *>(a->values_t),
+                                     host->fetched, stream);
+            if (rc == SPAMM_OK)
+                rc = spamm_gather_blocks(host->b_blocks, fb, host->b_nleaf, 1, const_cast<float *>(b->values), nullptr,
+                                         host->fetched ? host->fetched + 1 : nullptr, stream);
+        }
+        if (rc != SPAMM_OK) return rc;
+    }
     // executed micro products are counted in plan->counts[8..9]
     rc = spamm_execute_impl(a, b, plan, -1, -1, tau, alpha, granularity, exact, c->values, c->values_t, c->leaf_sq,
                             reinterpret_cast<unsigned long long *>(plan->counts + 8), c, clean_ptr, clean_words, stream);
@@ -60,6 +83,22 @@ extern "C" int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b
     // interior norms of C: compute_norms, numeric.py:179 / core.py:331-345
     return spamm_launch_interior(c->leaf_sq_grid, c->depth, c->norm, c->norm_t, c->sq_levels,
                                  reinterpret_cast<unsigned int *>(plan->counts + 10), st);
+}
+
+extern "C" int spamm_multiply(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity, int exact,
+                              float alpha, int32_t row0, int32_t row1, const spamm_plan_buffers *plan, void *plan_ws,
+                              size_t plan_ws_bytes, const spamm_product_buffers *c, void *stream)
+{
+    return multiply_impl(a, b, tau, granularity, exact, alpha, row0, row1, plan, plan_ws, plan_ws_bytes, c, nullptr, stream);
+}
+
+extern "C" int spamm_multiply_host(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity, int exact,
+                                   float alpha, int32_t row0, int32_t row1, const spamm_plan_buffers *plan, void *plan_ws,
+                                   size_t plan_ws_bytes, const spamm_product_buffers *c, const spamm_host_operands *host,
+                                   void *stream)
+{
+    if (!host) return SPAMM_EINVAL;
+    return multiply_impl(a, b, tau, granularity, exact, alpha, row0, row1, plan, plan_ws, plan_ws_bytes, c, host, stream);
 }
 
 // ---- the same on ONE caller-provided allocation ------------------------------------------------
@@ -98,10 +137,10 @@ extern "C" int spamm_multiply_arena_layout(int depth, int c_depth, int64_t step_
     return SPAMM_OK;
 }
 
-extern "C" int spamm_multiply_arena(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
-                                    int exact, float alpha, int32_t row0, int32_t row1, int c_depth, int64_t step_capacity,
-                                    int64_t leaf_capacity, void *arena, size_t arena_bytes, void *plan_ws,
-                                    size_t plan_ws_bytes, void *stream)
+static int multiply_arena_impl(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
+                               int exact, float alpha, int32_t row0, int32_t row1, int c_depth, int64_t step_capacity,
+                               int64_t leaf_capacity, void *arena, size_t arena_bytes, void *plan_ws,
+                               size_t plan_ws_bytes, const spamm_host_operands *host, void *stream)
 {
     if (!a || !b || !arena || !plan_ws) return SPAMM_EINVAL;
     spamm_arena_layout l;
@@ -129,5 +168,24 @@ extern "C" int spamm_multiply_arena(const spamm_tree_view *a, const spamm_tree_v
     c.leaf_sq_grid = reinterpret_cast<double *>(p + l.leaf_sq_grid);
     c.sq_levels = reinterpret_cast<double *>(p + l.sq_levels);
     c.depth = c_depth;
-    return spamm_multiply(a, b, tau, granularity, exact, alpha, row0, row1, &plan, plan_ws, plan_ws_bytes, &c, stream);
+    return multiply_impl(a, b, tau, granularity, exact, alpha, row0, row1, &plan, plan_ws, plan_ws_bytes, &c, host, stream);
+}
+
+extern "C" int spamm_multiply_arena(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
+                                    int exact, float alpha, int32_t row0, int32_t row1, int c_depth, int64_t step_capacity,
+                                    int64_t leaf_capacity, void *arena, size_t arena_bytes, void *plan_ws,
+                                    size_t plan_ws_bytes, void *stream)
+{
+    return multiply_arena_impl(a, b, tau, granularity, exact, alpha, row0, row1, c_depth, step_capacity, leaf_capacity, arena,
+                               arena_bytes, plan_ws, plan_ws_bytes, nullptr, stream);
+}
+
+extern "C" int spamm_multiply_arena_host(const spamm_tree_view *a, const spamm_tree_view *b, double tau, int granularity,
+                                         int exact, float alpha, int32_t row0, int32_t row1, int c_depth,
+                                         int64_t step_capacity, int64_t leaf_capacity, void *arena, size_t arena_bytes,
+                                         void *plan_ws, size_t plan_ws_bytes, const spamm_host_operands *host, void *stream)
+{
+    if (!host) return SPAMM_EINVAL;
+    return multiply_arena_impl(a, b, tau, granularity, exact, alpha, row0, row1, c_depth, step_capacity, leaf_capacity, arena,
+                               arena_bytes, plan_ws, plan_ws_bytes, host, stream);
 }

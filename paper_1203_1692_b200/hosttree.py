@@ -93,13 +93,32 @@ def multiply_host(a: HostTree, b: HostTree | None, cfg: MultiplyConfig | None = 
     qa = a.skeleton()
     same = b is None or b is a
     qb = qa if same else b.skeleton()
-    plan = build_plan(qa, qb, cfg.tau)
     dev = qa.device
     st = _stream()
     copied = torch.zeros((2,), dtype=torch.int64, device=dev)
+    if a.nleaf == 0 or (not same and b.nleaf == 0) or cfg.alpha == 0:
+        plan = build_plan(qa, qb, cfg.tau)
+        c, counters = execute_plan(plan, qa, qb, None, cfg)
+        return c, plan, counters, copied
+    fa = torch.empty((a.nleaf,), dtype=torch.uint8, device=dev)
+    fb = fa if same else torch.empty((b.nleaf,), dtype=torch.uint8, device=dev)
+    from .symbolic import _capacity_hint, plan_capacity
+    depth = max(qa.depth, qb.depth)
+    key, _ = plan_capacity(qa, qb, cfg.tau, depth, 0, 1 << depth)
+    if key in _capacity_hint:
+        # buffer sizes known from an earlier product of this shape: plan, mark, fetch, leaf products and norms of C
+        # in ONE C call, no host synchronisation
+        from .numeric import multiply_async
+        host = _lib.HostOperands(a.blocks.data_ptr(), a.nleaf, fa.data_ptr(), None if same else b.blocks.data_ptr(),
+                                 0 if same else b.nleaf, None if same else fb.data_ptr(), copied.data_ptr())
+        c, plan, counters = multiply_async(qa, qb, cfg, None, host=host)
+        plan._host_keepalive = (a, b, fa, fb, copied)       # a repeat after an overflow fetches again
+        return c, plan, counters, copied
+    plan = build_plan(qa, qb, cfg.tau)
     if len(plan):
-        fa = torch.zeros((max(a.nleaf, 1),), dtype=torch.uint8, device=dev)
-        fb = fa if same else torch.zeros((max(b.nleaf, 1),), dtype=torch.uint8, device=dev)
+        fa.zero_()
+        if not same:
+            fb.zero_()
         bufs = plan.buffers()
         import ctypes as C
         _lib.check(lib.spamm_mark_touched(C.byref(bufs), fa.data_ptr(), fb.data_ptr(), st), "mark_touched")

@@ -248,8 +248,9 @@ def _planner_workspace(dev, nbytes: int, stream: int | None = None) -> torch.Ten
 
 
 def multiply_async(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig, c: QuadtreeMatrix | None = None,
-                   row_range: tuple[int, int] | None = None) -> tuple[QuadtreeMatrix, MultiplyPlan, ExecCounters]:
-    """C = alpha A B through ``spamm_multiply``: one C call, no host synchronisation."""
+                   row_range: tuple[int, int] | None = None, host=None) -> tuple[QuadtreeMatrix, MultiplyPlan, ExecCounters]:
+    """C = alpha A B through ``spamm_multiply``: one C call, no host synchronisation.
+    ``host``: a ``_lib.HostOperands`` when the operands' leaf values are still in host memory (hosttree.py)."""
     from .symbolic import plan_capacity
     from .tree import _Grids
 
@@ -299,9 +300,14 @@ def multiply_async(a: QuadtreeMatrix, b: QuadtreeMatrix, cfg: MultiplyConfig, c:
         ws = _planner_workspace(dev, lay.plan_ws_bytes, st)
         va, vb = a.view(depth), b.view(depth, left=False)
         try:
-            _lib.check(lib.spamm_multiply_arena(C.byref(va), C.byref(vb), float(cfg.tau), gran, int(cfg.exact), alpha32,
-                                                r0, r1, cd, step_cap, leaf_cap, arena.data_ptr(), lay.total,
-                                                ws.data_ptr(), ws.numel(), st), "multiply")
+            if host is None:
+                _lib.check(lib.spamm_multiply_arena(C.byref(va), C.byref(vb), float(cfg.tau), gran, int(cfg.exact), alpha32,
+                                                    r0, r1, cd, step_cap, leaf_cap, arena.data_ptr(), lay.total,
+                                                    ws.data_ptr(), ws.numel(), st), "multiply")
+            else:
+                _lib.check(lib.spamm_multiply_arena_host(C.byref(va), C.byref(vb), float(cfg.tau), gran, int(cfg.exact),
+                                                         alpha32, r0, r1, cd, step_cap, leaf_cap, arena.data_ptr(), lay.total,
+                                                         ws.data_ptr(), ws.numel(), C.byref(host), st), "multiply_host")
         except Exception:
             _planner_ws.clear()         # a failed enqueue may leave the workspace dirty: start from a fresh one
             raise
