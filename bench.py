@@ -474,10 +474,53 @@ def run_single(args, torch, P, local: int) -> None:
         fetched_box["n"] = fetched
         return cc
 
+    # the same in two blocks of rows of C: block 1 is copied back (side stream) while block 2 is planned, fetched and
+    # multiplied, so that PCIe runs in both directions at once; no synchronisation before the end of the step
+    side = torch.cuda.Stream()
+    part_bufs = {}
+
+    def e2e_time_parts(nparts):
+        times, d2h_bytes = [], 0
+        for it in range(2 + max(3, min(args.steps, 20) // 2)):
+            flush.fill_(it)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            sizes = []
+
+            def copy_back(part):
+                (r0, r1), cc, _plan, _k, _f = part
+                vals, keys = cc.values, cc.keys          # capacity-bounded views: the leaf count is still on the device
+                hv = part_bufs.get((r0, "v"))
+                if hv is None or hv.shape[0] < vals.shape[0]:
+                    hv = part_bufs[(r0, "v")] = torch.empty(tuple(vals.shape), dtype=vals.dtype).pin_memory()
+                    part_bufs[(r0, "k")] = torch.empty((vals.shape[0],), dtype=torch.int32).pin_memory()
+                ev = torch.cuda.Event()
+                ev.record()
+                side.wait_event(ev)
+                with torch.cuda.stream(side):
+                    hv[: vals.shape[0]].copy_(vals, non_blocking=True)
+                    part_bufs[(r0, "k")][: keys.shape[0]].copy_(keys, non_blocking=True)
+                sizes.append(int(vals.shape[0]) * (_lib.REC * 4 + 4))
+
+            res = P.multiply_host_parts(h_a, h_b, cfg, parts=nparts, on_part=copy_back)
+            torch.cuda.current_stream().wait_stream(side)
+            e1.record()
+            torch.cuda.synchronize()
+            fetched_box["parts"] = sum(int(p[4].sum().item()) for p in res)
+            d2h_bytes = sum(sizes)
+            if it >= 2:
+                times.append(e0.elapsed_time(e1))
+        return float(np.mean(times)), d2h_bytes
+
     e2e_dense_ms, _ = e2e_time(step_dense)
     e2e_packed_ms, _ = e2e_time(step_packed)
-    e2e_ms, d2h = e2e_time(step_host)
-    fetched_leaves = int(fetched_box["n"].sum().item())
+    e2e_one_ms, d2h_one = e2e_time(step_host)
+    e2e_two_ms, d2h_two = e2e_time_parts(2)
+    if e2e_one_ms <= e2e_two_ms:      # the better schedule is the headline; both are reported
+        e2e_ms, d2h, e2e_parts = e2e_one_ms, d2h_one, 1
+    else:
+        e2e_ms, d2h, e2e_parts = e2e_two_ms, d2h_two, 2
+    fetched_leaves = int(fetched_box["n"].sum().item()) if e2e_parts == 1 else int(fetched_box["parts"])
     h2d_host = h_a.skeleton_bytes() + (0 if h_b is None else h_b.skeleton_bytes()) + fetched_leaves * 1024
     h2d = sum(int(t.numel()) * t.element_size() for t in pk_a) * (1 if b_d is None else 2)
     h2d_dense = a_d.nbytes * (1 if b_d is None else 2)
@@ -577,6 +620,10 @@ def run_single(args, torch, P, local: int) -> None:
                 "operands": "host trees (HostTree: the arrays of packed_leaves() + leaf norms, pinned); multiply_host sends keys and "
                             "norms, plans, and the GPU fetches the leaves that occur in a task from host memory",
                 "operand_leaves_fetched": fetched_leaves,
+                "row_blocks": e2e_parts,
+                "one_block": {"ms_per_step": e2e_one_ms, "d2h_bytes_per_step": int(d2h_one)},
+                "two_row_blocks": {"ms_per_step": e2e_two_ms, "d2h_bytes_per_step": int(d2h_two),
+                                   "note": "block 1 copied back on a side stream while block 2 is fetched and multiplied"},
                 "result": "product tree as packed leaves (keys + leaf records)",
                 "all_leaves": {"value": flops / (e2e_packed_ms * 1e-3) / 1e9, "ms_per_step": e2e_packed_ms,
                                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

@@ -19,6 +19,6 @@ from .numeric import (  # noqa: F401
     execute_plan,
     multiply,
 )
-from .hosttree import HostTree, multiply_host  # noqa: F401
+from .hosttree import HostTree, multiply_host, multiply_host_parts  # noqa: F401
 
 __version__ = "0.1.0"

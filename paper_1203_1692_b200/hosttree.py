@@ -84,52 +84,74 @@ class HostTree:
 def multiply_host(a: HostTree, b: HostTree | None, cfg: MultiplyConfig | None = None):
     """C = alpha A B for operands in host memory (``b is None``: B is A).  Returns ``(c, plan, counters,
     fetched)``: the product tree on the device, its plan and counters as from ``multiply``, and the number of
-    operand leaves whose values were fetched from the host (left, right)."""
+    operand leaves whose values were fetched from the host (left, right; a device tensor)."""
+    (rows, c, plan, counters, fetched), = multiply_host_parts(a, b, cfg, parts=1)
+    return c, plan, counters, fetched
+
+
+def multiply_host_parts(a: HostTree, b: HostTree | None, cfg: MultiplyConfig | None = None, parts: int = 2, on_part=None):
+    """The same product in ``parts`` blocks of leaf rows of C, enqueued one after the other on the current stream:
+    while block r+1 is planned, fetched and multiplied, the caller can already copy block r back (``on_part(part)``
+    is called right after a block has been enqueued) -- PCIe is used in both directions at once.  Returns the list of
+    ``((row0, row1), c, plan, counters, fetched)``; every ``c`` has the global shape and holds its rows only, and each
+    product leaf is computed in one pass in ascending k, as in ``parallel.ShardedMultiply``."""
     if cfg is None:
         cfg = MultiplyConfig()
     if cfg.beta != 0:
         raise ValueError("multiply_host computes C = alpha A B; merge an accumulator with multiply() (beta != 0)")
+    if parts < 1:
+        raise ValueError(f"parts must be positive, got {parts}")
     lib = _lib.lib()
     qa = a.skeleton()
     same = b is None or b is a
     qb = qa if same else b.skeleton()
     dev = qa.device
     st = _stream()
-    copied = torch.zeros((2,), dtype=torch.int64, device=dev)
-    if a.nleaf == 0 or (not same and b.nleaf == 0) or cfg.alpha == 0:
-        plan = build_plan(qa, qb, cfg.tau)
-        c, counters = execute_plan(plan, qa, qb, None, cfg)
-        return c, plan, counters, copied
-    fa = torch.empty((a.nleaf,), dtype=torch.uint8, device=dev)
-    fb = fa if same else torch.empty((b.nleaf,), dtype=torch.uint8, device=dev)
-    from .symbolic import _capacity_hint, plan_capacity
     depth = max(qa.depth, qb.depth)
-    key, _ = plan_capacity(qa, qb, cfg.tau, depth, 0, 1 << depth)
-    if key in _capacity_hint:
-        # buffer sizes known from an earlier product of this shape: plan, mark, fetch, leaf products and norms of C
-        # in ONE C call, no host synchronisation
-        from .numeric import multiply_async
-        host = _lib.HostOperands(a.blocks.data_ptr(), a.nleaf, fa.data_ptr(), None if same else b.blocks.data_ptr(),
-                                 0 if same else b.nleaf, None if same else fb.data_ptr(), copied.data_ptr())
-        c, plan, counters = multiply_async(qa, qb, cfg, None, host=host)
-        plan._host_keepalive = (a, b, fa, fb, copied)       # a repeat after an overflow fetches again
-        return c, plan, counters, copied
-    plan = build_plan(qa, qb, cfg.tau)
-    if len(plan):
-        fa.zero_()
-        if not same:
-            fb.zero_()
-        bufs = plan.buffers()
-        import ctypes as C
-        _lib.check(lib.spamm_mark_touched(C.byref(bufs), fa.data_ptr(), fb.data_ptr(), st), "mark_touched")
-        if same:
-            _lib.check(lib.spamm_gather_blocks(a.blocks.data_ptr(), fa.data_ptr(), a.nleaf, 3, qa.values.data_ptr(),
-                                               qa.values_t.data_ptr(), copied.data_ptr(), st), "gather_blocks")
+    nrows = 1 << depth
+    # blocks of rows cut at multiples of 4 leaf rows (a super-tile has one owner)
+    cuts = sorted({min(nrows, ((nrows * i // parts + 3) // 4) * 4) for i in range(parts + 1)} | {0, nrows})
+    out = []
+    from .symbolic import _capacity_hint, plan_capacity
+    for r0, r1 in zip(cuts[:-1], cuts[1:]):
+        copied = torch.zeros((2,), dtype=torch.int64, device=dev)
+        rr = None if (r0, r1) == (0, nrows) else (r0, r1)
+        if a.nleaf == 0 or (not same and b.nleaf == 0) or cfg.alpha == 0:
+            plan = build_plan(qa, qb, cfg.tau, rr)
+            c, counters = execute_plan(plan, qa, qb, None, cfg)
         else:
-            # the left operand is read through its transposed records, the right one through the plain ones
-            _lib.check(lib.spamm_gather_blocks(a.blocks.data_ptr(), fa.data_ptr(), a.nleaf, 2, qa.values.data_ptr(),
-                                               qa.values_t.data_ptr(), copied.data_ptr(), st), "gather_blocks")
-            _lib.check(lib.spamm_gather_blocks(b.blocks.data_ptr(), fb.data_ptr(), b.nleaf, 1, qb.values.data_ptr(),
-                                               qb.values_t.data_ptr(), copied.data_ptr() + 8, st), "gather_blocks")
-    c, counters = execute_plan(plan, qa, qb, None, cfg)
-    return c, plan, counters, copied
+            fa = torch.empty((a.nleaf,), dtype=torch.uint8, device=dev)
+            fb = fa if same else torch.empty((b.nleaf,), dtype=torch.uint8, device=dev)
+            key, _ = plan_capacity(qa, qb, cfg.tau, depth, r0, r1)
+            if key in _capacity_hint:
+                # buffer sizes known from an earlier product of this shape: plan, mark, fetch, leaf products and norms
+                # of C in ONE C call, no host synchronisation
+                from .numeric import multiply_async
+                host = _lib.HostOperands(a.blocks.data_ptr(), a.nleaf, fa.data_ptr(), None if same else b.blocks.data_ptr(),
+                                         0 if same else b.nleaf, None if same else fb.data_ptr(), copied.data_ptr())
+                c, plan, counters = multiply_async(qa, qb, cfg, None, row_range=rr, host=host)
+                plan._host_keepalive = (a, b, fa, fb, copied)       # a repeat after an overflow fetches again
+            else:
+                plan = build_plan(qa, qb, cfg.tau, rr)
+                if len(plan):
+                    fa.zero_()
+                    if not same:
+                        fb.zero_()
+                    bufs = plan.buffers()
+                    import ctypes as C
+                    _lib.check(lib.spamm_mark_touched(C.byref(bufs), fa.data_ptr(), fb.data_ptr(), st), "mark_touched")
+                    if same:
+                        _lib.check(lib.spamm_gather_blocks(a.blocks.data_ptr(), fa.data_ptr(), a.nleaf, 3, qa.values.data_ptr(),
+                                                           qa.values_t.data_ptr(), copied.data_ptr(), st), "gather_blocks")
+                    else:
+                        # the left operand is read through its transposed records, the right one through the plain ones
+                        _lib.check(lib.spamm_gather_blocks(a.blocks.data_ptr(), fa.data_ptr(), a.nleaf, 2, qa.values.data_ptr(),
+                                                           qa.values_t.data_ptr(), copied.data_ptr(), st), "gather_blocks")
+                        _lib.check(lib.spamm_gather_blocks(b.blocks.data_ptr(), fb.data_ptr(), b.nleaf, 1, qb.values.data_ptr(),
+                                                           qb.values_t.data_ptr(), copied.data_ptr() + 8, st), "gather_blocks")
+                c, counters = execute_plan(plan, qa, qb, None, cfg)
+        part = ((r0, r1), c, plan, counters, copied)
+        out.append(part)
+        if on_part is not None:
+            on_part(part)
+    return out

@@ -59,3 +59,31 @@ def test_host_resident_two_operands():
     assert (int(fetched[0].item()), int(fetched[1].item())) == (ta, tb)
     with pytest.raises(ValueError):
         P.multiply_host(ha, hb, P.MultiplyConfig(tau=tau, beta=1.0))
+
+
+@pytest.mark.parametrize("parts", [2, 3])
+def test_host_resident_in_row_blocks(parts):
+    """multiply_host_parts: the product in blocks of leaf rows, each enqueued behind the other; together they are the
+    product of fully resident trees, bit for bit, on the first call (plan + execute) and on the fused repeat."""
+    import paper_1203_1692_b200 as P
+    from paper_1203_1692_b200 import inputs
+    n, tau = 2048, 1e-7
+    a = inputs.exponential_decay(n, 0.93, seed=3)
+    qa = P.QuadtreeMatrix.from_dense(a)
+    cfg = P.MultiplyConfig(tau=tau, exact=True)
+    want, wplan, wk = P.multiply(qa, qa, cfg)
+    wd = want.to_dense().data
+    ha = P.HostTree.from_device(qa)
+    for rep in range(3):
+        seen = []
+        res = P.multiply_host_parts(ha, None, cfg, parts=parts, on_part=lambda p: seen.append(p[0]))
+        assert [p[0] for p in res] == seen and len(res) == parts
+        assert res[0][0][0] == 0 and res[-1][0][1] == 128 and all(x[0][1] == y[0][0] for x, y in zip(res[:-1], res[1:]))
+        got = np.zeros_like(wd)
+        for (r0, r1), c, plan, k, fetched in res:
+            assert r0 % 4 == 0
+            d = c.to_dense().data
+            assert not d[: r0 * 16].any() and not d[r1 * 16:].any(), "a block holds its rows only"
+            got[r0 * 16:r1 * 16] = d[r0 * 16:r1 * 16]
+        assert np.array_equal(got, wd), f"repetition {rep}"
+        assert sum(len(p[2]) for p in res) == len(wplan) and sum(p[3].products4 for p in res) == wk.products4
